@@ -1,0 +1,356 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 sliding-window cumulant update (arXiv 1701.06446).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Workload: BASELINE.json configs[1] (d=4, n=96, b=8, T=20000, p=1000), the
+config the metric is quoted on that fits one GPU.  One step = one window
+update of the reference's `step()` (stream.cpp:85-108): exchange p rows,
+moments_update of M1..M4, moms2cums to C1..C4, and the window report with
+nu_3, nu_4 (the config's stated output) read back to the host.
+
+value  = window updates/s with the incoming rows already resident in HBM
+         (device timed with CUDA events on the engine's stream; L2 flushed
+         between steps, the flush outside the events).
+e2e    = the same through the C ABI with HOST buffers (csb_stream_step on
+         pinned rows): H2D of the rows and D2H of the report inside the
+         timed region.
+roofline = the order-4/3 moment kernel (moment_top): algorithmic flops per
+         launch / its event-timed average duration, against the measured
+         FP64 peak (profiles/fp64_peak.json; MEASURED_PEAKS.json has no FP64
+         entry).
+cpu_baseline = the reference itself (oracle/_ref, compiled from
+         /root/reference) on the host cores: prime + 2 steps of the same
+         workload.
+
+--impl reference: the reference CPU library on the same workload, all host
+threads, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from math import comb
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1701_06446_b200.synth import CONFIGS, StreamGen  # noqa: E402
+
+METRIC = "window updates/sec (order-d sliding cumulant update, FP64)"
+UNIT = "window-updates/s"
+
+
+def bell_partition_flops(s: int) -> int:
+    # 1 + sum_sigma sigma * S(s, sigma) over sigma >= 2
+    S = [[0] * (s + 1) for _ in range(s + 1)]
+    S[0][0] = 1
+    for i in range(1, s + 1):
+        for j in range(1, i + 1):
+            S[i][j] = S[i - 1][j - 1] + j * S[i - 1][j]
+    return 1 + sum(sig * S[s][sig] for sig in range(2, s + 1))
+
+
+def algorithmic_flops(cfg) -> dict:
+    n, d, p = cfg.n, cfg.d, cfg.p
+    canon = {s: comb(n + s - 1, s) for s in range(1, d + 1)}
+    f_mom = 4 * p * sum(canon.values())
+    f_m2c = sum(canon[s] * bell_partition_flops(s) for s in range(2, d + 1))
+    f_top = 4 * p * (canon[d] + canon[d - 1])  # the fused order-d/d-1 kernel, per launch
+    return {"F_mom": f_mom, "F_m2c": f_m2c, "F_alg": f_mom + f_m2c, "F_top_launch": f_top}
+
+
+def fp64_peak() -> tuple[float, str]:
+    path = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    try:
+        with open(path) as fh:
+            j = json.load(fh)
+        v = max(j.get("dgemm_cublas_tflops", 0.0), j.get("dfma_tflops", 0.0), j.get("dmma_tflops", 0.0))
+        if v > 0:
+            return v, "measured on B200 (profiles/fp64_peak.json: max of cuBLAS DGEMM, DFMA, DMMA microbenchmarks)"
+    except (OSError, ValueError):
+        pass
+    return 37.2, "nominal 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (no FP64 entry in MEASURED_PEAKS.json)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.device)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+        return False
+
+    def summary(self) -> dict:
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline_sample(cfg, gen_window, batches, steps: int = 2) -> dict | None:
+    """The reference library (oracle/_ref) on a bounded sample of the same
+    workload: prime + `steps` window updates, all host threads."""
+    try:
+        from oracle.oracle import Oracle, RefStream, ref_library_path
+    except Exception:
+        return None
+    if ref_library_path() is None:
+        return None
+    cores = os.cpu_count() or 1
+    ref = Oracle("ref", workers=cores)
+    t0 = time.perf_counter()
+    st = RefStream(ref, cfg.n, cfg.d, cfg.T, cfg.p, cfg.b, gen_window, resync_every=0)
+    t_prime = time.perf_counter() - t0
+    times = []
+    for k in range(steps):
+        t0 = time.perf_counter()
+        st.step(batches[k])
+        times.append(time.perf_counter() - t0)
+    st.close()
+    med = statistics.median(times)
+    return {"value": 1.0 / med, "unit": UNIT, "cores": cores, "kind": "reference",
+            "sample": f"{cfg.name}: prime ({t_prime:.1f} s) + {steps} step() calls of the reference "
+                      f"library (oracle/_ref, {os.path.basename(ref.path)}), median step {med:.3f} s",
+            "s_per_step": med}
+
+
+def run_reference_arm(args, cfg) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    try:
+        from oracle.oracle import Oracle, RefStream, ref_library_path
+    except Exception as e:  # pragma: no cover
+        print(json.dumps({"impl": "reference", "unavailable": f"oracle import failed: {e}"}))
+        return
+    if ref_library_path() is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (make -C oracle ref)"}))
+        return
+    cores = os.cpu_count() or 1
+    gen = StreamGen(cfg)
+    window = gen.window()
+    total = args.warmup + args.steps
+    batches = [gen.batch(1 + (k % cfg.steps)) for k in range(total)]
+    ref = Oracle("ref", workers=cores)
+    t0 = time.perf_counter()
+    st = RefStream(ref, cfg.n, cfg.d, cfg.T, cfg.p, cfg.b, window, resync_every=0)
+    t_prime = time.perf_counter() - t0
+    for k in range(args.warmup):
+        st.step(batches[k])
+    t0 = time.perf_counter()
+    for k in range(args.warmup, total):
+        rep = st.step(batches[k])
+    dt = time.perf_counter() - t0
+    st.close()
+    value = args.steps / dt
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": cfg.name, "d": cfg.d, "n": cfg.n, "b": cfg.b,
+                                         "T": cfg.T, "p": cfg.p},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": f"prime ({t_prime:.1f} s) + {args.warmup} warm-up + {args.steps} timed "
+                                   f"step() calls of the unmodified reference library "
+                                   f"({os.path.basename(ref.path)}, workers={cores})"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "last_report_nu": [float(rep[6]), float(rep[7])],
+    }))
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    cfg = CONFIGS[args.config]
+
+    if args.impl == "reference":
+        run_reference_arm(args, cfg)
+        return
+
+    import torch
+
+    from paper_1701_06446_b200 import capi
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    capi.check(capi.lib().csb_set_device(local if world > 1 else 0))
+    dev = torch.device("cuda", local if world > 1 else 0)
+
+    gen = StreamGen(cfg, seed=1701064460 + rank)
+    window = gen.window()
+    total = args.warmup + 2 * args.steps
+    batches = [gen.batch(1 + (k % cfg.steps)) for k in range(total)]
+
+    st = capi.Stream(cfg.n, cfg.d, cfg.T, cfg.p, cfg.b, window, resync_every=0)
+    cs = torch.cuda.ExternalStream(st.cuda_stream(), device=dev)
+    xdev = [torch.from_numpy(b).to(dev) for b in batches]
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
+    torch.cuda.synchronize()
+
+    for k in range(args.warmup):
+        st.step_dev(xdev[k].data_ptr(), cfg.p, cfg.n, report=True)
+    torch.cuda.synchronize()
+
+    # ---- value: inputs resident in HBM -------------------------------------
+    capi.profile_enable(True)
+    capi.profile_read("moment_top")
+    launches0 = capi.launch_count()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index) as clocks:
+        wall0 = time.perf_counter()
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            torch.cuda.synchronize()
+            ev[k][0].record(cs)
+            rep = st.step_dev(xdev[args.warmup + k].data_ptr(), cfg.p, cfg.n, report=True)
+            ev[k][1].record(cs)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - wall0
+    launches = capi.launch_count() - launches0
+    top_ms, top_n = capi.profile_read("moment_top")
+    capi.profile_enable(False)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    dev_s = sum(step_ms) * 1e-3
+    if dist:
+        t = torch.tensor([dev_s], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_s = float(t.item())
+    value = world * args.steps / dev_s
+
+    # ---- e2e: through the C ABI with host (pinned) buffers -----------------
+    pinned = [torch.from_numpy(b).pin_memory() for b in batches[args.warmup + args.steps:]]
+    ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        flush.fill_(float(k))
+        torch.cuda.synchronize()
+        ev2[k][0].record(cs)
+        xk = pinned[k].numpy()
+        rep2 = st.step(xk, report=True)
+        ev2[k][1].record(cs)
+    torch.cuda.synchronize()
+    e2e_s = sum(a.elapsed_time(b) for a, b in ev2) * 1e-3
+    if dist:
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = world * args.steps / e2e_s
+
+    flops = algorithmic_flops(cfg)
+    peak, peak_src = fp64_peak()
+    top_avg_s = (top_ms / max(1, top_n)) * 1e-3
+    achieved = flops["F_top_launch"] / top_avg_s / 1e12 if top_n else None
+    traffic = None
+    tr_path = os.path.join(ROOT, "profiles", "moment_top_traffic.json")
+    if os.path.exists(tr_path):
+        try:
+            traffic = json.load(open(tr_path)).get("bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_sample(cfg, window, batches[:2])
+
+    if rank == 0:
+        ms_per_step = 1e3 * dev_s / args.steps
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "d": cfg.d, "n": cfg.n, "b": cfg.b, "T": cfg.T, "p": cfg.p,
+                       "l2": "flushed between steps (256 MB write, outside the step events)",
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "step": "exchange + moments_update(M1..M4) + moms2cums(C1..C4) + report(nu3, nu4)"},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "kernel": "moment_pair_kernel<true> (orders 4 and 3)",
+                         "flops_per_launch": flops["F_top_launch"], "avg_launch_ms": top_avg_s * 1e3,
+                         "launches": top_n, "peak_source": peak_src,
+                         "note": "FP64 path: bound is the FP64 pipe (DFMA/DMMA), not bf16 tensor"},
+            "step_flops": {"F_alg": flops["F_alg"], "F_mom": flops["F_mom"], "F_m2c": flops["F_m2c"],
+                           "alg_tflops_per_s": flops["F_alg"] / (dev_s / args.steps) / 1e12},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": cfg.p * cfg.n * 8,
+                    "d2h_bytes_per_step": (cfg.d + 3 * cfg.n) * 8},
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+            "wall_s_timed_region": wall,
+            "last_report": {"window": rep["window"], "nu3": rep["nu"][3], "nu4": rep["nu"][4]},
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    st.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,193 @@
+/*
+ * cumstream_b200 — C ABI of the B200-native sliding-window moment/cumulant
+ * hot path (arXiv 1701.06446).  This is the drop-in boundary: the C++ API
+ * of the reference (namespace cumstream, /root/reference/proj/include/
+ * cumstream/{symten,moments,cumulants,gauge,stream}.hpp) is re-implemented on
+ * top of these entry points
+ * (paper_1701_06446_b200/cpp/), and any FFI (ctypes, cgo, JNI) binds them
+ * directly.
+ *
+ * Conventions
+ *  - Plain pointers and sizes; no C++ or torch types cross the boundary.
+ *  - Every call returns a status: CSB_OK, or one of the error classes below,
+ *    which map 1:1 onto the reference's exception types:
+ *      CSB_EINVAL  -> std::invalid_argument   (shape / usage errors)
+ *      CSB_ERANGE  -> std::out_of_range       (index errors)
+ *      CSB_EDOMAIN -> std::domain_error       (degenerate maths, e.g. nu)
+ *      CSB_ERUNTIME-> std::runtime_error      (CUDA / NCCL / no device)
+ *    csb_last_error() returns the thread's last message.
+ *  - Tensors live on the device in the reference's block storage
+ *    (SymTensor, symten.hpp:85-143): for order s, dim n, block b, only
+ *    blocks with non-decreasing block index are stored, lexicographically,
+ *    each a dense C-order block (edge blocks truncated), one flat array.
+ *    Host transfers use exactly that layout, so a host array is
+ *    interchangeable with SymTensor::data() (symten.hpp:122).
+ *  - There is no CPU fallback: every compute entry point needs a CUDA
+ *    device (sm_100a) and fails with CSB_ERUNTIME otherwise.
+ */
+#ifndef CUMSTREAM_B200_H
+#define CUMSTREAM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CSB_OK 0
+#define CSB_EINVAL 1
+#define CSB_ERANGE 2
+#define CSB_EDOMAIN 3
+#define CSB_ERUNTIME 4
+
+#define CSB_MAX_ORDER 8 /* device path; the reference allows 20 (symten.hpp:87) */
+
+typedef struct csb_series csb_series; /* device-resident M_1..M_d or C_1..C_d */
+typedef struct csb_stream csb_stream; /* device-resident WindowState (stream.hpp:54-60) */
+
+/* ---- library ---------------------------------------------------------- */
+int csb_version(void);
+const char* csb_last_error(void);
+/* Number of visible CUDA devices (0 without a GPU; never fails). */
+int csb_device_count(void);
+/* Select the device subsequent calls on this thread use. */
+int csb_set_device(int device);
+/* rows_read(): rows handed to the moment routines so far in this process;
+ * replaces cumstream::rows_read (moments.hpp:46, moments.cpp:15,216). */
+uint64_t csb_rows_read(void);
+
+/* ---- layout (SymTensor ctor, symten.cpp:105-140) ------------------------ */
+/* Stored doubles and block count of one order. */
+int csb_layout_size(int order, int dim, int block, uint64_t* stored, uint64_t* blocks);
+/* block_multiplicity (symten.cpp:227-241) of a non-decreasing block index. */
+int csb_block_multiplicity(const int* block_index, int order, uint64_t* out);
+
+/* ---- series: the device backing of MomentSeries / CumulantSeries -------- */
+/* (moments.hpp:33-42, cumulants.hpp:30-39) */
+int csb_series_create(int dim, int max_order, int block, csb_series** out);
+int csb_series_destroy(csb_series* s);
+/* Deep device copy; shapes must match (value semantics of the reference). */
+int csb_series_copy(csb_series* dst, const csb_series* src);
+int csb_series_shape(const csb_series* s, int* dim, int* max_order, int* block,
+                     uint64_t* window_len);
+int csb_series_set_window_len(csb_series* s, uint64_t window_len);
+/* Stored doubles of order `order` (1-based). */
+int csb_series_stored(const csb_series* s, int order, uint64_t* stored);
+/* Raw device pointer of order `order` (for zero-copy interop / tests). */
+int csb_series_device_ptr(const csb_series* s, int order, double** dev);
+/* Host <-> device transfers of one order in block storage. count must
+ * equal the stored size. */
+int csb_series_upload(csb_series* s, int order, const double* host, uint64_t count);
+int csb_series_download(const csb_series* s, int order, double* host, uint64_t count);
+
+/* ---- hot path, host buffers ------------------------------------------------ */
+/* moment_series (moments.hpp:52): M_1..M_d of x (rows x cols, row-major).
+ * `out` must have been created with dim == cols; window_len := rows. */
+int csb_moment_series(csb_series* out, const double* x, uint64_t rows, uint64_t cols);
+/* moment_tensor (moments.hpp:49): one order into a series slot.  Only
+ * order `order` of `out` is written. */
+int csb_moment_tensor(csb_series* out, int order, const double* x, uint64_t rows, uint64_t cols);
+/* moments_update (moments.hpp:62): M += (p/T)(M(in) - M(out)), in place.
+ * Pre: rows(in) == rows(out) == p <= window_len, cols == dim. */
+int csb_moments_update(csb_series* m, const double* incoming, const double* outgoing,
+                       uint64_t rows, uint64_t cols);
+/* moms2cums (cumulants.hpp:47): cumulants C_1..C_d of moments m.
+ * `c` must have the same shape; c.window_len := m.window_len. */
+int csb_moms2cums(const csb_series* m, csb_series* c);
+/* combine (moments.hpp:56): out = (s1*m1 + s2*m2)/(s1+s2) elementwise. */
+int csb_combine(const csb_series* m1, uint64_t s1, const csb_series* m2, uint64_t s2,
+                csb_series* out);
+
+/* ---- hot path, device buffers (inputs already resident in HBM) ---------- */
+int csb_moment_series_dev(csb_series* out, const double* x_dev, uint64_t rows, uint64_t cols);
+int csb_moments_update_dev(csb_series* m, const double* in_dev, const double* out_dev,
+                           uint64_t rows, uint64_t cols);
+
+/* ---- norms and gauge ------------------------------------------------------ */
+/* knorm (symten.hpp:156): (sum_blocks mult * sum |e|^k)^(1/k), k >= 1. */
+int csb_knorm(const csb_series* s, int order, double k, double* out);
+/* nu (gauge.hpp:21): knorm(C_d,2) / knorm(C_2,2)^(d/2); CSB_EDOMAIN when
+ * ||C_2|| == 0, CSB_EINVAL unless 3 <= d <= max_order. */
+int csb_nu(const csb_series* c, int d, double* out);
+
+/* WindowReport (gauge.hpp:47-60).  nu[k] holds nu_{k+3}; has_skew/kurt
+ * mirror the std::optional fields. */
+typedef struct {
+  uint64_t window;
+  uint64_t rows;
+  double norm_c1;
+  double norm_c2;
+  double nu[CSB_MAX_ORDER];
+  int n_nu;
+  int has_skewness, has_kurtosis;
+  double max_abs_skewness;
+  double max_abs_kurtosis;
+} csb_report;
+
+/* make_window_report (gauge.hpp:57, gauge.cpp:142-154). */
+int csb_window_report(const csb_series* c, uint64_t window, csb_report* out);
+
+/* ---- sliding-window engine (stream.hpp:19-89) ---------------------------- */
+typedef struct {
+  int dim;               /* n */
+  int max_order;         /* d */
+  uint64_t window_len;   /* t */
+  uint64_t update_len;   /* t_up */
+  int block_size;        /* b */
+  uint64_t resync_every; /* steps between recomputes; 0 disables */
+  int workers;           /* accepted for API parity; host threads only */
+  /* B200 extension: shard of the order-d blocks this process owns
+   * (SURVEY §8e); shard_count <= 1 means the whole tensor. */
+  int shard_index;
+  int shard_count;
+} csb_stream_config;
+
+typedef struct {
+  double update_s;    /* StepTiming::update_s (stream.hpp:63-66), device time */
+  double moms2cums_s; /* StepTiming::moms2cums_s */
+} csb_step_timing;
+
+/* prime (stream.hpp:69): first.rows == window_len. */
+int csb_stream_prime(const csb_stream_config* cfg, const double* first, uint64_t rows,
+                     uint64_t cols, csb_stream** out);
+int csb_stream_destroy(csb_stream* st);
+/* step (stream.hpp:73): exchange + moments_update (or resync) + moms2cums.
+ * x is a host buffer (update_len x dim).  timing and report may be NULL;
+ * when report is non-NULL the window report of the new window is filled. */
+int csb_stream_step(csb_stream* st, const double* x, uint64_t rows, uint64_t cols,
+                    csb_step_timing* timing, csb_report* report);
+/* Same as csb_stream_step with x already in device memory. */
+int csb_stream_step_dev(csb_stream* st, const double* x_dev, uint64_t rows, uint64_t cols,
+                        csb_step_timing* timing, csb_report* report);
+/* Report of the current window (after prime: window 1). */
+int csb_stream_report(csb_stream* st, csb_report* report);
+/* Borrowed views of the state (owned by the stream). */
+int csb_stream_moments(csb_stream* st, const csb_series** m);
+int csb_stream_cumulants(csb_stream* st, const csb_series** c);
+int csb_stream_window(const csb_stream* st, uint64_t* window);
+/* WindowBuffer::materialize (stream.hpp:47): window rows in arrival order. */
+int csb_stream_materialize(const csb_stream* st, double* host, uint64_t count);
+/* Per-block partial squared norms of the owned shard, for the multi-GPU
+ * fixed-order norm reduction (collective C3). */
+int csb_stream_norm_partials(csb_stream* st, int order, double* host, uint64_t count,
+                             uint64_t* first_block);
+/* Device stream (cudaStream_t) the engine launches on, for interop. */
+int csb_stream_cuda_stream(csb_stream* st, void** cuda_stream);
+
+/* ---- instrumentation (bench.py) ------------------------------------------ */
+/* Kernels launched by this library so far in this process. */
+uint64_t csb_launch_count(void);
+/* When enabled, CUDA events bracket every kernel launch on its own stream,
+ * grouped by tag: "moment_top" (the order-d/d-1 pair kernel), "moment_low"
+ * (lower pairs), "moms2cums", "norms". */
+int csb_profile_enable(int on);
+/* Sum of the event-timed durations (ms) and launch count of one tag since the
+ * last read; reading resets the tag.  Synchronizes the recorded events. */
+int csb_profile_read(const char* tag, double* total_ms, uint64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CUMSTREAM_B200_H */

@@ -1,0 +1,361 @@
+"""ctypes binding of the C ABI (include/cumstream_b200.h).
+
+This is the Python-side FFI a maintainer would add to call the B200 hot
+path; tests and bench.py go through it.  There is no CPU
+fallback: if the in-tree library is missing, or a compute call is made
+without a CUDA device, it raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+from typing import Sequence
+
+import numpy as np
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "lib", "libcumstream_b200.so")
+HEADER = os.path.join(os.path.dirname(PKG), "include", "cumstream_b200.h")
+
+OK, EINVAL, ERANGE, EDOMAIN, ERUNTIME = 0, 1, 2, 3, 4
+MAX_ORDER = 8
+
+_u64 = C.c_uint64
+_dp = C.POINTER(C.c_double)
+
+
+class CsbError(RuntimeError):
+    code = ERUNTIME
+
+
+class CsbInvalidArgument(CsbError, ValueError):  # std::invalid_argument
+    code = EINVAL
+
+
+class CsbOutOfRange(CsbError, IndexError):  # std::out_of_range
+    code = ERANGE
+
+
+class CsbDomainError(CsbError, ArithmeticError):  # std::domain_error
+    code = EDOMAIN
+
+
+_ERRS = {EINVAL: CsbInvalidArgument, ERANGE: CsbOutOfRange, EDOMAIN: CsbDomainError,
+         ERUNTIME: CsbError}
+
+
+class Report(C.Structure):
+    _fields_ = [("window", _u64), ("rows", _u64), ("norm_c1", C.c_double),
+                ("norm_c2", C.c_double), ("nu", C.c_double * MAX_ORDER), ("n_nu", C.c_int),
+                ("has_skewness", C.c_int), ("has_kurtosis", C.c_int),
+                ("max_abs_skewness", C.c_double), ("max_abs_kurtosis", C.c_double)]
+
+    def as_dict(self) -> dict:
+        d = {"window": int(self.window), "rows": int(self.rows), "norm_c1": self.norm_c1,
+             "norm_c2": self.norm_c2, "nu": {3 + k: self.nu[k] for k in range(self.n_nu)}}
+        if self.has_skewness:
+            d["max_abs_skewness"] = self.max_abs_skewness
+        if self.has_kurtosis:
+            d["max_abs_kurtosis"] = self.max_abs_kurtosis
+        return d
+
+
+class StreamConfig(C.Structure):
+    _fields_ = [("dim", C.c_int), ("max_order", C.c_int), ("window_len", _u64),
+                ("update_len", _u64), ("block_size", C.c_int), ("resync_every", _u64),
+                ("workers", C.c_int), ("shard_index", C.c_int), ("shard_count", C.c_int)]
+
+
+class StepTiming(C.Structure):
+    _fields_ = [("update_s", C.c_double), ("moms2cums_s", C.c_double)]
+
+
+_lib = None
+
+
+def header_symbols() -> list[str]:
+    """Every csb_* function the public header declares."""
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(csb_[a-z0-9_]+)\s*\(", txt)))
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise CsbError(f"{LIB_PATH} missing: run __graft_entry__.build() "
+                           "(make -C paper_1701_06446_b200/csrc)")
+        L = C.CDLL(LIB_PATH)
+        sig = {
+            "csb_version": ([], C.c_int),
+            "csb_last_error": ([], C.c_char_p),
+            "csb_device_count": ([], C.c_int),
+            "csb_set_device": ([C.c_int], C.c_int),
+            "csb_rows_read": ([], _u64),
+            "csb_layout_size": ([C.c_int, C.c_int, C.c_int, C.POINTER(_u64), C.POINTER(_u64)], C.c_int),
+            "csb_block_multiplicity": ([C.POINTER(C.c_int), C.c_int, C.POINTER(_u64)], C.c_int),
+            "csb_series_create": ([C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)], C.c_int),
+            "csb_series_destroy": ([C.c_void_p], C.c_int),
+            "csb_series_copy": ([C.c_void_p, C.c_void_p], C.c_int),
+            "csb_series_shape": ([C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                  C.POINTER(C.c_int), C.POINTER(_u64)], C.c_int),
+            "csb_series_set_window_len": ([C.c_void_p, _u64], C.c_int),
+            "csb_series_stored": ([C.c_void_p, C.c_int, C.POINTER(_u64)], C.c_int),
+            "csb_series_device_ptr": ([C.c_void_p, C.c_int, C.POINTER(C.c_void_p)], C.c_int),
+            "csb_series_upload": ([C.c_void_p, C.c_int, _dp, _u64], C.c_int),
+            "csb_series_download": ([C.c_void_p, C.c_int, _dp, _u64], C.c_int),
+            "csb_moment_series": ([C.c_void_p, _dp, _u64, _u64], C.c_int),
+            "csb_moment_tensor": ([C.c_void_p, C.c_int, _dp, _u64, _u64], C.c_int),
+            "csb_moments_update": ([C.c_void_p, _dp, _dp, _u64, _u64], C.c_int),
+            "csb_moms2cums": ([C.c_void_p, C.c_void_p], C.c_int),
+            "csb_combine": ([C.c_void_p, _u64, C.c_void_p, _u64, C.c_void_p], C.c_int),
+            "csb_moment_series_dev": ([C.c_void_p, C.c_void_p, _u64, _u64], C.c_int),
+            "csb_moments_update_dev": ([C.c_void_p, C.c_void_p, C.c_void_p, _u64, _u64], C.c_int),
+            "csb_knorm": ([C.c_void_p, C.c_int, C.c_double, _dp], C.c_int),
+            "csb_nu": ([C.c_void_p, C.c_int, _dp], C.c_int),
+            "csb_window_report": ([C.c_void_p, _u64, C.POINTER(Report)], C.c_int),
+            "csb_stream_prime": ([C.POINTER(StreamConfig), _dp, _u64, _u64, C.POINTER(C.c_void_p)], C.c_int),
+            "csb_stream_destroy": ([C.c_void_p], C.c_int),
+            "csb_stream_step": ([C.c_void_p, _dp, _u64, _u64, C.POINTER(StepTiming), C.POINTER(Report)], C.c_int),
+            "csb_stream_step_dev": ([C.c_void_p, C.c_void_p, _u64, _u64, C.POINTER(StepTiming),
+                                     C.POINTER(Report)], C.c_int),
+            "csb_stream_report": ([C.c_void_p, C.POINTER(Report)], C.c_int),
+            "csb_stream_moments": ([C.c_void_p, C.POINTER(C.c_void_p)], C.c_int),
+            "csb_stream_cumulants": ([C.c_void_p, C.POINTER(C.c_void_p)], C.c_int),
+            "csb_stream_window": ([C.c_void_p, C.POINTER(_u64)], C.c_int),
+            "csb_stream_materialize": ([C.c_void_p, _dp, _u64], C.c_int),
+            "csb_stream_norm_partials": ([C.c_void_p, C.c_int, _dp, _u64, C.POINTER(_u64)], C.c_int),
+            "csb_stream_cuda_stream": ([C.c_void_p, C.POINTER(C.c_void_p)], C.c_int),
+            "csb_launch_count": ([], _u64),
+            "csb_profile_enable": ([C.c_int], C.c_int),
+            "csb_profile_read": ([C.c_char_p, C.POINTER(C.c_double), C.POINTER(_u64)], C.c_int),
+        }
+        for name, (args, res) in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc != OK:
+        msg = lib().csb_last_error().decode(errors="replace")
+        raise _ERRS.get(rc, CsbError)(msg)
+
+
+def _dptr(a: np.ndarray):
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_dp)
+
+
+def layout_size(order: int, dim: int, block: int) -> tuple[int, int]:
+    st, nb = _u64(), _u64()
+    check(lib().csb_layout_size(order, dim, block, C.byref(st), C.byref(nb)))
+    return st.value, nb.value
+
+
+def rows_read() -> int:
+    return int(lib().csb_rows_read())
+
+
+def launch_count() -> int:
+    return int(lib().csb_launch_count())
+
+
+def profile_enable(on: bool = True) -> None:
+    check(lib().csb_profile_enable(1 if on else 0))
+
+
+def profile_read(tag: str) -> tuple[float, int]:
+    """(total ms, launches) of one kernel tag since the last read."""
+    ms, cnt = C.c_double(), _u64()
+    check(lib().csb_profile_read(tag.encode(), C.byref(ms), C.byref(cnt)))
+    return ms.value, cnt.value
+
+
+class Series:
+    """Device-resident MomentSeries / CumulantSeries (moments.hpp:33-42)."""
+
+    def __init__(self, dim: int, max_order: int, block: int):
+        h = C.c_void_p()
+        check(lib().csb_series_create(dim, max_order, block, C.byref(h)))
+        self.h = h
+        self.dim, self.max_order, self.block = dim, max_order, block
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().csb_series_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def window_len(self) -> int:
+        wl = _u64()
+        check(lib().csb_series_shape(self.h, None, None, None, C.byref(wl)))
+        return wl.value
+
+    @window_len.setter
+    def window_len(self, v: int):
+        check(lib().csb_series_set_window_len(self.h, v))
+
+    def stored(self, order: int) -> int:
+        st = _u64()
+        check(lib().csb_series_stored(self.h, order, C.byref(st)))
+        return st.value
+
+    def device_ptr(self, order: int) -> int:
+        p = C.c_void_p()
+        check(lib().csb_series_device_ptr(self.h, order, C.byref(p)))
+        return p.value
+
+    def upload(self, order: int, host: np.ndarray):
+        host = np.ascontiguousarray(host, dtype=np.float64)
+        check(lib().csb_series_upload(self.h, order, _dptr(host), host.size))
+
+    def download(self, order: int) -> np.ndarray:
+        out = np.empty(self.stored(order))
+        check(lib().csb_series_download(self.h, order, _dptr(out), out.size))
+        return out
+
+    def tensors(self) -> list[np.ndarray]:
+        return [self.download(s) for s in range(1, self.max_order + 1)]
+
+    def copy_from(self, other: "Series"):
+        check(lib().csb_series_copy(self.h, other.h))
+
+
+def moment_series(x: np.ndarray, max_order: int, block: int) -> Series:
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    s = Series(x.shape[1], max_order, block)
+    check(lib().csb_moment_series(s.h, _dptr(x), x.shape[0], x.shape[1]))
+    return s
+
+
+def moment_tensor(x: np.ndarray, order: int, block: int) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    s = Series(x.shape[1], order, block)
+    check(lib().csb_moment_tensor(s.h, order, _dptr(x), x.shape[0], x.shape[1]))
+    return s.download(order)
+
+
+def moments_update(m: Series, incoming: np.ndarray, outgoing: np.ndarray) -> None:
+    xi = np.ascontiguousarray(incoming, dtype=np.float64)
+    xo = np.ascontiguousarray(outgoing, dtype=np.float64)
+    if xi.shape != xo.shape:
+        raise CsbInvalidArgument("moments_update: batch sizes differ")
+    check(lib().csb_moments_update(m.h, _dptr(xi), _dptr(xo), xi.shape[0], xi.shape[1]))
+
+
+def moms2cums(m: Series) -> Series:
+    c = Series(m.dim, m.max_order, m.block)
+    check(lib().csb_moms2cums(m.h, c.h))
+    return c
+
+
+def combine(m1: Series, s1: int, m2: Series, s2: int) -> Series:
+    out = Series(m1.dim, m1.max_order, m1.block)
+    check(lib().csb_combine(m1.h, s1, m2.h, s2, out.h))
+    return out
+
+
+def knorm(s: Series, order: int, k: float = 2.0) -> float:
+    out = C.c_double()
+    check(lib().csb_knorm(s.h, order, k, C.byref(out)))
+    return out.value
+
+
+def nu(c: Series, d: int) -> float:
+    out = C.c_double()
+    check(lib().csb_nu(c.h, d, C.byref(out)))
+    return out.value
+
+
+def window_report(c: Series, window: int) -> dict:
+    r = Report()
+    check(lib().csb_window_report(c.h, window, C.byref(r)))
+    return r.as_dict()
+
+
+class Stream:
+    """Device-resident sliding-window engine: prime / step (stream.hpp:69,73)."""
+
+    def __init__(self, dim: int, max_order: int, window_len: int, update_len: int, block: int,
+                 first: np.ndarray, resync_every: int = 1000, shard_index: int = 0,
+                 shard_count: int = 1):
+        self.cfg = StreamConfig(dim, max_order, window_len, update_len, block, resync_every, 0,
+                                shard_index, shard_count)
+        first = np.ascontiguousarray(first, dtype=np.float64)
+        h = C.c_void_p()
+        check(lib().csb_stream_prime(C.byref(self.cfg), _dptr(first), first.shape[0],
+                                     first.shape[1] if first.ndim == 2 else 1, C.byref(h)))
+        self.h = h
+        self.timing = StepTiming()
+        self.rep = Report()
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().csb_stream_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def step(self, x: np.ndarray, report: bool = True) -> dict | None:
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        check(lib().csb_stream_step(self.h, _dptr(x), x.shape[0], x.shape[1], C.byref(self.timing),
+                                    C.byref(self.rep) if report else None))
+        return self.rep.as_dict() if report else None
+
+    def step_dev(self, x_dev_ptr: int, rows: int, cols: int, report: bool = False):
+        check(lib().csb_stream_step_dev(self.h, C.c_void_p(x_dev_ptr), rows, cols, None,
+                                        C.byref(self.rep) if report else None))
+        return self.rep.as_dict() if report else None
+
+    def report(self) -> dict:
+        check(lib().csb_stream_report(self.h, C.byref(self.rep)))
+        return self.rep.as_dict()
+
+    def _series(self, fn) -> list[np.ndarray]:
+        p = C.c_void_p()
+        check(fn(self.h, C.byref(p)))
+        d = self.cfg.max_order
+        out = []
+        for s in range(1, d + 1):
+            st = _u64()
+            check(lib().csb_series_stored(p, s, C.byref(st)))
+            a = np.empty(st.value)
+            check(lib().csb_series_download(p, s, _dptr(a), a.size))
+            out.append(a)
+        return out
+
+    def moments(self) -> list[np.ndarray]:
+        return self._series(lib().csb_stream_moments)
+
+    def cumulants(self) -> list[np.ndarray]:
+        return self._series(lib().csb_stream_cumulants)
+
+    @property
+    def window(self) -> int:
+        w = _u64()
+        check(lib().csb_stream_window(self.h, C.byref(w)))
+        return w.value
+
+    def materialize(self) -> np.ndarray:
+        out = np.empty((self.cfg.window_len, self.cfg.dim))
+        check(lib().csb_stream_materialize(self.h, _dptr(out), out.size))
+        return out
+
+    def cuda_stream(self) -> int:
+        p = C.c_void_p()
+        check(lib().csb_stream_cuda_stream(self.h, C.byref(p)))
+        return p.value or 0

@@ -1,0 +1,76 @@
+// Shared host-side helpers: error classes (mirroring the reference's
+// exception types), CUDA error checks, device buffers.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+
+#include "cumstream_b200.h"
+
+namespace csb {
+
+// Status-carrying exception; the C ABI maps it back to CSB_* codes.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+inline void require(bool ok, const std::string& msg) {
+  if (!ok) fail(CSB_EINVAL, msg);
+}
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    fail(CSB_ERUNTIME, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CSB_CUDA(call) ::csb::cuda_check((call), #call)
+
+// Owning device allocation (value-less; copying is explicit).
+template <class T>
+struct DevBuf {
+  T* ptr = nullptr;
+  std::size_t count = 0;
+  DevBuf() = default;
+  explicit DevBuf(std::size_t n) { alloc(n); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : ptr(std::exchange(o.ptr, nullptr)), count(std::exchange(o.count, 0)) {}
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      ptr = std::exchange(o.ptr, nullptr);
+      count = std::exchange(o.count, 0);
+    }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(std::size_t n) {
+    release();
+    if (n) CSB_CUDA(cudaMalloc(&ptr, n * sizeof(T)));
+    count = n;
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    count = 0;
+  }
+  std::size_t bytes() const { return count * sizeof(T); }
+};
+
+inline uint64_t binom(int n, int k) {
+  if (k < 0 || k > n) return 0;
+  if (k > n - k) k = n - k;
+  uint64_t r = 1;
+  for (int i = 1; i <= k; ++i) r = r * static_cast<uint64_t>(n - k + i) / static_cast<uint64_t>(i);
+  return r;
+}
+inline uint64_t multiset_count(int a, int r) { return binom(a + r - 1, r); }
+
+void ensure_device();  // throws CSB_ERUNTIME without a usable CUDA device
+
+}  // namespace csb

@@ -1,0 +1,529 @@
+// sm_100a kernels of the sliding-window moment/cumulant hot path.
+//
+// Arithmetic follows the reference's evaluation order exactly
+// so results are bit-identical to it:
+//   * moment products: left-to-right chain starting at x[i_1]
+//     (moments.cpp:55,71);
+//   * top order d: acc = fma(A, x[i_d], acc) in row order (moments.cpp:47);
+//   * every lower order: acc = acc + round(product) (moments.cpp:44,57);
+//   * means: acc * (1.0 / rows) (moments.cpp:148-150);
+//   * update: M = fma(p/T, a - b, M) for every stored copy (moments.cpp:297);
+//   * cumulants: partition sum in RGS order, no FMA (cumulants.cpp:64-82).
+// The file is compiled with -fmad=false; every intended FMA is an explicit
+// __fma_rn and every unfused product/sum an explicit __dmul_rn/__dadd_rn.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+
+#include "kernels.cuh"
+#include "partitions_gen.cuh"
+
+namespace csb {
+
+namespace {
+
+constexpr int KC = 8;        // data rows per smem chunk
+constexpr int MAXROWS = 1024;  // prefix rows per tile
+constexpr int T = kMomThreads;
+
+__device__ __forceinline__ const double* row_ptr(const RowSource& s, uint32_t k, int n) {
+  return k < s.len0 ? s.seg0 + static_cast<size_t>(k) * n
+                    : s.seg1 + static_cast<size_t>(k - s.len0) * n;
+}
+
+__device__ __forceinline__ bool next_perm(int* a, int len) {
+  // std::next_permutation on a short int range
+  if (len < 2) return false;
+  int i = len - 2;
+  while (i >= 0 && a[i] >= a[i + 1]) --i;
+  if (i < 0) {
+    for (int l = 0, r = len - 1; l < r; ++l, --r) {
+      const int t = a[l];
+      a[l] = a[r];
+      a[r] = t;
+    }
+    return false;
+  }
+  int j = len - 1;
+  while (a[j] <= a[i]) --j;
+  int t = a[i];
+  a[i] = a[j];
+  a[j] = t;
+  for (int l = i + 1, r = len - 1; l < r; ++l, --r) {
+    t = a[l];
+    a[l] = a[r];
+    a[r] = t;
+  }
+  return true;
+}
+
+// Calls f(offset) for every stored copy of a canonical element: all
+// distinct permutations of the in-block offsets o within runs of equal
+// block coordinate j (symten.cpp:195-220).  o must be sorted within runs.
+// Returns the number of copies.
+template <class F>
+__device__ __forceinline__ int for_each_copy(int S, const int* j, int* o, const int* e,
+                                             uint64_t blk_off, F&& f) {
+  bool runs = false;
+  for (int k = 1; k < S; ++k) runs |= (j[k] == j[k - 1]);
+  if (!runs) {
+    uint64_t off = 0;
+    for (int k = 0; k < S; ++k) off = off * e[k] + o[k];
+    f(blk_off + off);
+    return 1;
+  }
+  int rs[kMaxOrder], re[kMaxOrder], nr = 0;
+  for (int s = 0; s < S;) {
+    int t = s + 1;
+    while (t < S && j[t] == j[s]) ++t;
+    rs[nr] = s;
+    re[nr] = t;
+    ++nr;
+    s = t;
+  }
+  int count = 0;
+  for (;;) {
+    uint64_t off = 0;
+    for (int k = 0; k < S; ++k) off = off * e[k] + o[k];
+    f(blk_off + off);
+    ++count;
+    int q = nr - 1;
+    while (q >= 0 && !next_perm(o + rs[q], re[q] - rs[q])) --q;
+    if (q < 0) break;
+  }
+  return count;
+}
+
+__device__ __forceinline__ int ext_of(int j, int n, int b) { return b < n - j * b ? b : n - j * b; }
+
+// Epilogue of one order-S element: RMW (update) or assign every stored copy.
+__device__ __noinline__ void store_top(const MomParams& P, const MomTile& tile, int r, int col,
+                                       const uint16_t* id, double a, double v) {
+  const int n = P.n, b = P.b, L = P.L;
+  if (L > 0 && col < static_cast<int>(id[L - 1])) return;  // below the diagonal: a copy
+  const PrefixRow& pr = P.rows[tile.row0 + r];
+  const int jd = col / b;
+  int jv[kMaxOrder], ov[kMaxOrder], ev[kMaxOrder];
+  for (int q = 0; q < L; ++q) {
+    jv[q] = id[q] / b;
+    ov[q] = id[q] - jv[q] * b;
+    ev[q] = ext_of(jv[q], n, b);
+  }
+  jv[L] = jd;
+  ov[L] = col - jd * b;
+  ev[L] = ext_of(jd, n, b);
+  const uint64_t blk = pr.top_base + static_cast<uint64_t>(pr.vprime) * b * (jd - static_cast<int>(tile.J));
+  double* top = P.top;
+  if (P.npass == 2) {
+    const double delta = __dsub_rn(a, v);
+    const double c = P.c;
+    for_each_copy(L + 1, jv, ov, ev, blk, [&](uint64_t off) { top[off] = __fma_rn(c, delta, top[off]); });
+  } else {
+    for_each_copy(L + 1, jv, ov, ev, blk, [&](uint64_t off) { top[off] = v; });
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Moment pair kernel: orders S (GEMM over prefix rows x columns) and S-1
+// (row sums of the Khatri-Rao operand) for one tile of prefix rows.
+template <bool TOP_FMA>
+__global__ void __launch_bounds__(T, 1) moment_pair_kernel(const MomParams P) {
+  extern __shared__ __align__(16) double smem[];
+  const MomTile tile = P.tiles[blockIdx.x];
+  const int n = P.n, b = P.b, L = P.L;
+  const int N = static_cast<int>(tile.ncols);
+  const int CG = (N + 7) / 8;
+  const int nr = static_cast<int>(tile.nrows);
+  const int RG = (nr + 7) / 8;
+  const int XS = (n + 1) & ~1;
+  const int BS = CG * 8;
+  const int AS = RG * 8;
+  double* xs = smem;
+  double* bs = xs + KC * XS;
+  double* as = bs + KC * BS;
+  double* lowstash = as + KC * AS;
+  uint16_t* ridx = reinterpret_cast<uint16_t*>(lowstash + AS);  // AS x 8
+
+  const int t = threadIdx.x;
+  const int rg = t / CG, cg = t % CG;
+  const bool active = rg < RG;
+
+  for (int e = t; e < AS; e += T) {
+    if (e < nr) {
+      const PrefixRow& pr = P.rows[tile.row0 + e];
+      for (int k = 0; k < 8; ++k) ridx[e * 8 + k] = pr.idx[k];
+    } else {
+      for (int k = 0; k < 8; ++k) ridx[e * 8 + k] = 0;
+    }
+  }
+
+  for (int pass = 0; pass < P.npass; ++pass) {
+    const RowSource src = P.src[pass];
+    double acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+    double lacc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) lacc[i] = 0.0;
+
+    for (uint32_t k0 = 0; k0 < P.K; k0 += KC) {
+      const int kc = static_cast<int>(min(static_cast<uint32_t>(KC), P.K - k0));
+      __syncthreads();
+      for (int e = t; e < KC * XS; e += T) {
+        const int k = e / XS, c = e % XS;
+        xs[e] = (k < kc && c < n) ? row_ptr(src, k0 + k, n)[c] : 0.0;
+      }
+      for (int e = t; e < KC * BS; e += T) {
+        const int k = e / BS, c = e % BS;
+        bs[e] = (k < kc && c < N) ? row_ptr(src, k0 + k, n)[tile.col0 + c] : 0.0;
+      }
+      __syncthreads();
+      if (t < RG) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = 8 * t + i;
+          const uint16_t* id = ridx + r * 8;
+          for (int k = 0; k < KC; ++k) {
+            double a;
+            if (r >= nr || k >= kc) {
+              a = 0.0;
+            } else if (L == 0) {
+              a = 1.0;
+            } else {
+              const double* xr = xs + k * XS;
+              a = xr[id[0]];
+              for (int q = 1; q < L; ++q) a = __dmul_rn(a, xr[id[q]]);
+              lacc[i] = __dadd_rn(lacc[i], a);
+            }
+            as[k * AS + r] = a;
+          }
+        }
+      }
+      __syncthreads();
+      if (active) {
+        for (int k = 0; k < kc; ++k) {
+          double av[8], bv[8];
+          const double2* ap = reinterpret_cast<const double2*>(as + k * AS + 8 * rg);
+          const double2* bp = reinterpret_cast<const double2*>(bs + k * BS + 8 * cg);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const double2 x = ap[q];
+            av[2 * q] = x.x;
+            av[2 * q + 1] = x.y;
+            const double2 y = bp[q];
+            bv[2 * q] = y.x;
+            bv[2 * q + 1] = y.y;
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              if (TOP_FMA)
+                acc[i][j] = __fma_rn(av[i], bv[j], acc[i][j]);
+              else
+                acc[i][j] = __dadd_rn(acc[i][j], __dmul_rn(av[i], bv[j]));
+            }
+        }
+      }
+    }
+
+    const bool final_pass = (pass == P.npass - 1);
+    const size_t sbase = static_cast<size_t>(blockIdx.x) * 64 * T;
+    if (!final_pass) {
+      // stash the incoming means for the fused update epilogue
+      if (active) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            P.scratch[sbase + static_cast<size_t>(i * 8 + j) * T + t] = __dmul_rn(acc[i][j], P.inv);
+      }
+      if (t < RG) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) lowstash[8 * t + i] = __dmul_rn(lacc[i], P.inv);
+      }
+      continue;
+    }
+
+    // ---- epilogue: order S ----
+    if (active) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int r = 8 * rg + i;
+        if (r >= nr) continue;
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          const int cc = 8 * cg + jj;
+          if (cc >= N) continue;
+          const double v = __dmul_rn(acc[i][jj], P.inv);
+          const double a = (P.npass == 2) ? P.scratch[sbase + static_cast<size_t>(i * 8 + jj) * T + t] : 0.0;
+          store_top(P, tile, r, static_cast<int>(tile.col0) + cc, ridx + r * 8, a, v);
+        }
+      }
+    }
+    // ---- epilogue: order S-1 ----
+    if (P.low != nullptr && tile.low && L > 0 && t < RG) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int r = 8 * t + i;
+        if (r >= nr) continue;
+        const PrefixRow& pr = P.rows[tile.row0 + r];
+        const uint16_t* id = ridx + r * 8;
+        const double v = __dmul_rn(lacc[i], P.inv);
+        double delta = 0.0;
+        if (P.npass == 2) delta = __dsub_rn(lowstash[r], v);
+        int jv[kMaxOrder], ov[kMaxOrder], ev[kMaxOrder];
+        for (int q = 0; q < L; ++q) {
+          jv[q] = id[q] / b;
+          ov[q] = id[q] - jv[q] * b;
+          ev[q] = ext_of(jv[q], n, b);
+        }
+        const uint64_t blk = pr.low_off - pr.poff;
+        double* low = P.low;
+        const double cc_ = P.c;
+        if (P.npass == 2) {
+          for_each_copy(L, jv, ov, ev, blk, [&](uint64_t off) { low[off] = __fma_rn(cc_, delta, low[off]); });
+        } else {
+          for_each_copy(L, jv, ov, ev, blk, [&](uint64_t off) { low[off] = v; });
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// moms2cums for order S (cumulants.cpp:128-196): one CTA per stored block.
+__device__ __forceinline__ uint64_t rank_dev(const LayoutDev& L, const int* j, int order) {
+  uint64_t acc = 0;
+  int lo = 0;
+  for (int i = 0; i < order; ++i) {
+    const int rem = order - 1 - i;
+    acc += L.prefix[static_cast<size_t>(rem) * (L.grid + 1) + j[i]] -
+           L.prefix[static_cast<size_t>(rem) * (L.grid + 1) + lo];
+    lo = j[i];
+  }
+  return acc;
+}
+
+constexpr int popcount_c(int m) { return m == 0 ? 0 : (m & 1) + popcount_c(m >> 1); }
+
+template <int S>
+__global__ void __launch_bounds__(256) moms2cums_kernel(const M2CParams P) {
+  constexpr int NM = (1 << S) - 1;  // masks 1..NM-1 are the proper subsets
+  __shared__ uint64_t sbase[NM];
+  __shared__ uint32_t sstride[NM][S];
+  __shared__ double red[8];
+  const uint64_t blk = P.blk0 + blockIdx.x;
+  const LayoutDev& LS = P.lay[S - 1];
+  const int n = P.n, b = P.b;
+  int j[S], e[S];
+#pragma unroll
+  for (int k = 0; k < S; ++k) {
+    j[k] = LS.index[blk * S + k];
+    e[k] = ext_of(j[k], n, b);
+  }
+  const uint64_t boff = LS.offset[blk];
+  const uint64_t vol = LS.offset[blk + 1] - boff;
+  for (int m = 1 + threadIdx.x; m < NM; m += blockDim.x) {
+    int sub[S], cnt = 0;
+    for (int k = 0; k < S; ++k)
+      if (m >> k & 1) sub[cnt++] = j[k];
+    const LayoutDev& Lq = P.lay[cnt - 1];
+    sbase[m] = Lq.offset[rank_dev(Lq, sub, cnt)];
+    // Horner strides of the sub-block (C order over the positions in m)
+    uint32_t stride = 1;
+    for (int k = S - 1; k >= 0; --k) {
+      if (m >> k & 1) {
+        sstride[m][k] = stride;
+        stride *= static_cast<uint32_t>(e[k]);
+      } else {
+        sstride[m][k] = 0;
+      }
+    }
+  }
+  __syncthreads();
+
+  double part = 0.0;
+  for (uint64_t pos = threadIdx.x; pos < vol; pos += blockDim.x) {
+    int o[S];
+    uint64_t rem = pos;
+#pragma unroll
+    for (int k = S - 1; k >= 0; --k) {
+      o[k] = static_cast<int>(rem % e[k]);
+      rem /= e[k];
+    }
+    bool canonical = true;
+#pragma unroll
+    for (int k = 1; k < S; ++k)
+      if (j[k] == j[k - 1] && o[k] < o[k - 1]) canonical = false;
+    if (!canonical) continue;
+    double f[NM];
+#pragma unroll
+    for (int m = 1; m < NM; ++m) {
+      uint64_t a = sbase[m];
+#pragma unroll
+      for (int k = 0; k < S; ++k)
+        if (m >> k & 1) a += static_cast<uint64_t>(o[k]) * sstride[m][k];
+      f[m] = P.lower[popcount_c(m) - 1][a];
+    }
+    const double corr = partition_correction<S>(f);
+    const double v = __dsub_rn(P.m[boff + pos], corr);
+    double* out = P.c;
+    const int copies = for_each_copy(S, j, o, e, boff, [&](uint64_t off) { out[off] = v; });
+    part = __fma_rn(static_cast<double>(copies), __dmul_rn(v, v), part);
+  }
+  // deterministic block reduction
+  for (int s = 16; s > 0; s >>= 1) part = __dadd_rn(part, __shfl_down_sync(0xffffffffu, part, s));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) s = __dadd_rn(s, red[w]);
+    P.partial[blockIdx.x] = s;
+  }
+}
+
+__global__ void copy_c1_kernel(const double* m1, double* c1, double* partial, LayoutDev lay,
+                               uint64_t nblocks) {
+  // C_1 = M_1 (cumulants.cpp:139); one thread per block partial
+  const uint64_t blk = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (blk >= nblocks) return;
+  double s = 0.0;
+  for (uint64_t i = lay.offset[blk]; i < lay.offset[blk + 1]; ++i) {
+    const double v = m1[i];
+    c1[i] = v;
+    s = __fma_rn(v, v, s);
+  }
+  partial[blk] = s;
+}
+
+__global__ void knorm_partials_kernel(const double* t, LayoutDev lay, uint64_t nblocks, double k,
+                                      double* partial) {
+  const uint64_t blk = blockIdx.x;
+  if (blk >= nblocks) return;
+  __shared__ double red[8];
+  double s = 0.0;
+  for (uint64_t i = lay.offset[blk] + threadIdx.x; i < lay.offset[blk + 1]; i += blockDim.x) {
+    const double v = t[i];
+    if (k == 2.0) s = __fma_rn(v, v, s);
+    else if (k == 1.0) s = __dadd_rn(s, fabs(v));
+    else s = __dadd_rn(s, pow(fabs(v), k));
+  }
+  for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) a = __dadd_rn(a, red[w]);
+    partial[blk] = a;
+  }
+}
+
+// One CTA: fixed-order reductions of the per-block partials (x multiplicity)
+// and the diagonal gathers the report needs.  Deterministic for any GPU count.
+__global__ void __launch_bounds__(1024) norm_finalize_kernel(const NormParams P) {
+  __shared__ double red[32];
+  for (int s = 0; s < P.norders; ++s) {
+    double a = 0.0;
+    for (uint64_t i = threadIdx.x; i < P.nblocks[s]; i += blockDim.x)
+      a = __fma_rn(P.mult[s][i], P.partial[s][i], a);
+    for (int o = 16; o > 0; o >>= 1) a = __dadd_rn(a, __shfl_down_sync(0xffffffffu, a, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tot = 0.0;
+      for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) tot = __dadd_rn(tot, red[w]);
+      P.out[s] = tot;
+    }
+    __syncthreads();
+  }
+  for (int q = 0; q < 3; ++q) {
+    if (!P.diag_src[q]) continue;
+    for (int i = threadIdx.x; i < P.n; i += blockDim.x)
+      P.out[P.norders + q * P.n + i] = P.diag_src[q][P.diag_off[q][i]];
+  }
+}
+
+__global__ void combine_kernel(const double* a, const double* b, double w1, double w2, double* out,
+                               uint64_t count) {
+  // combine (moments.cpp:258-262): z = w1 * z + w2 * b, contracted to
+  // fma(w1, z, w2 * b) by the reference build
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[i] = __fma_rn(w1, a[i], __dmul_rn(w2, b[i]));
+}
+
+std::atomic<uint64_t> g_launches{0};
+
+}  // namespace
+
+uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+void launch_moment_pair(const MomParams& p, int ntiles, bool top_fma, cudaStream_t st) {
+  if (ntiles <= 0) return;
+  const int XS = (p.n + 1) & ~1;
+  const int BS = ((p.n + 7) / 8) * 8;
+  const size_t smem = sizeof(double) * (KC * XS + KC * BS + KC * MAXROWS + MAXROWS) +
+                      sizeof(uint16_t) * MAXROWS * 8;
+  if (top_fma) {
+    CSB_CUDA(cudaFuncSetAttribute(moment_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    moment_pair_kernel<true><<<ntiles, T, smem, st>>>(p);
+  } else {
+    CSB_CUDA(cudaFuncSetAttribute(moment_pair_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    moment_pair_kernel<false><<<ntiles, T, smem, st>>>(p);
+  }
+  CSB_CUDA(cudaGetLastError());
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+void launch_moms2cums(int S, const M2CParams& p, uint64_t nblocks, cudaStream_t st) {
+  if (nblocks == 0) return;
+  const unsigned g = static_cast<unsigned>(nblocks);
+  switch (S) {
+    case 2: moms2cums_kernel<2><<<g, 256, 0, st>>>(p); break;
+    case 3: moms2cums_kernel<3><<<g, 256, 0, st>>>(p); break;
+    case 4: moms2cums_kernel<4><<<g, 256, 0, st>>>(p); break;
+    case 5: moms2cums_kernel<5><<<g, 256, 0, st>>>(p); break;
+    case 6: moms2cums_kernel<6><<<g, 256, 0, st>>>(p); break;
+    default: fail(CSB_EINVAL, "moms2cums: device path supports orders <= 6");
+  }
+  CSB_CUDA(cudaGetLastError());
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+void launch_copy_c1(const double* m1, double* c1, double* partial, const LayoutDev& lay,
+                    uint64_t nblocks, uint64_t, cudaStream_t st) {
+  const unsigned g = static_cast<unsigned>((nblocks + 127) / 128);
+  copy_c1_kernel<<<g, 128, 0, st>>>(m1, c1, partial, lay, nblocks);
+  CSB_CUDA(cudaGetLastError());
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+void launch_norm_finalize(const NormParams& p, cudaStream_t st) {
+  norm_finalize_kernel<<<1, 1024, 0, st>>>(p);
+  CSB_CUDA(cudaGetLastError());
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+void launch_knorm_partials(const double* t, const LayoutDev& lay, uint64_t nblocks, double k,
+                           double* partial, cudaStream_t st) {
+  if (!nblocks) return;
+  knorm_partials_kernel<<<static_cast<unsigned>(nblocks), 256, 0, st>>>(t, lay, nblocks, k, partial);
+  CSB_CUDA(cudaGetLastError());
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+void launch_combine(const double* a, const double* b, double w1, double w2, double* out,
+                    uint64_t count, cudaStream_t st) {
+  if (!count) return;
+  combine_kernel<<<592, 256, 0, st>>>(a, b, w1, w2, out, count);
+  CSB_CUDA(cudaGetLastError());
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+}  // namespace csb

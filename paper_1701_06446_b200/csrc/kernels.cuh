@@ -1,0 +1,76 @@
+// Device-side parameter blocks shared by kernels.cu and runtime.cpp.
+#pragma once
+
+#include <cstdint>
+
+#include "layout.hpp"
+
+namespace csb {
+
+// Rows [0, len0) come from seg0, rows [len0, len0 + len1) from seg1
+// (the ring buffer's two segments in arrival order, stream.cpp:39-66).
+struct RowSource {
+  const double* seg0 = nullptr;
+  const double* seg1 = nullptr;
+  uint32_t len0 = 0, len1 = 0;
+};
+
+struct MomParams {
+  RowSource src[2];     // pass 0 (incoming / window), pass 1 (outgoing)
+  int npass = 1;        // 1: assign (moment_series), 2: update (moments_update)
+  uint32_t K = 0;       // rows per pass
+  int n = 0, b = 0, L = 0;
+  const PrefixRow* rows = nullptr;
+  const MomTile* tiles = nullptr;
+  double* top = nullptr;      // M_S
+  double* low = nullptr;      // M_{S-1} (nullptr: not written)
+  double* scratch = nullptr;  // pass-0 stash, tiles x 64 x threads
+  double c = 0.0;             // p / T        (moments.cpp:287)
+  double inv = 1.0;           // 1.0 / rows   (moments.cpp:148)
+};
+
+struct LayoutDev {
+  const uint64_t* offset = nullptr;  // nblocks + 1
+  const uint16_t* index = nullptr;   // nblocks x order
+  const uint64_t* prefix = nullptr;  // order x (grid + 1)
+  int order = 0, grid = 0;
+};
+
+struct M2CParams {
+  const double* m = nullptr;        // M_S
+  double* c = nullptr;              // C_S
+  const double* lower[kMaxOrder];   // C_1 .. C_{S-1}
+  LayoutDev lay[kMaxOrder];         // layouts of orders 1..S (index s-1)
+  int n = 0, b = 0;
+  uint64_t blk0 = 0;                // first block of the shard
+  double* partial = nullptr;        // per block: sum over stored entries of v*v
+};
+
+struct NormParams {
+  const double* partial[kMaxOrder];  // per order, nblocks each
+  const double* mult[kMaxOrder];     // per order block multiplicities (as double)
+  uint64_t nblocks[kMaxOrder];
+  int norders = 0;                   // orders 1..norders
+  const double* diag_src[3];         // C_2, C_3, C_4 (nullptr if absent)
+  const uint64_t* diag_off[3];       // n offsets each
+  int n = 0;
+  double* out = nullptr;             // [norders sums][3 x n diagonals]
+};
+
+void launch_moment_pair(const MomParams& p, int ntiles, bool top_fma, cudaStream_t st);
+void launch_moms2cums(int S, const M2CParams& p, uint64_t nblocks, cudaStream_t st);
+void launch_copy_c1(const double* m1, double* c1, double* partial, const LayoutDev& lay,
+                    uint64_t nblocks, uint64_t stored, cudaStream_t st);
+void launch_norm_finalize(const NormParams& p, cudaStream_t st);
+void launch_knorm_partials(const double* t, const LayoutDev& lay, uint64_t nblocks, double k,
+                           double* partial, cudaStream_t st);
+void launch_combine(const double* a, const double* b, double w1, double w2, double* out,
+                    uint64_t count, cudaStream_t st);
+
+constexpr int kMomThreads = 256;
+
+// Kernels this library has launched in this process (bench.py's
+// gpu_launches claim).
+uint64_t launch_count();
+
+}  // namespace csb

@@ -1,0 +1,167 @@
+#include "layout.hpp"
+
+#include <algorithm>
+#include <numeric>
+
+namespace csb {
+
+Layout::Layout(int order_, int dim_, int block_) : order(order_), dim(dim_), block(block_) {
+  require(order >= 1 && order <= 20, "SymTensor: order must be in [1, 20]");
+  require(dim >= 1, "SymTensor: dim must be positive");
+  require(block >= 1 && block <= dim, "SymTensor: block_size must be in [1, dim]");
+  require(dim <= 65535, "cumstream_b200: dim must be <= 65535");
+  grid = (dim + block - 1) / block;
+  // lexicographic multiset ranker over the block grid (symten.cpp:31-45)
+  prefix.assign(static_cast<std::size_t>(order) * (grid + 1), 0);
+  for (int rem = 0; rem < order; ++rem) {
+    uint64_t acc = 0;
+    for (int v = 0; v <= grid; ++v) {
+      prefix[static_cast<std::size_t>(rem) * (grid + 1) + v] = acc;
+      if (v < grid) acc += multiset_count(grid - v, rem);
+    }
+  }
+  nblocks = multiset_count(grid, order);
+  index.reserve(nblocks * order);
+  offset.reserve(nblocks + 1);
+  int j[20] = {0};
+  uint64_t off = 0;
+  for (;;) {
+    uint64_t vol = 1;
+    for (int k = 0; k < order; ++k) {
+      index.push_back(static_cast<uint16_t>(j[k]));
+      vol *= static_cast<uint64_t>(ext(j[k]));
+    }
+    offset.push_back(off);
+    off += vol;
+    int k = order - 1;
+    while (k >= 0 && j[k] == grid - 1) --k;
+    if (k < 0) break;
+    const int v = j[k] + 1;
+    for (int l = k; l < order; ++l) j[l] = v;
+  }
+  offset.push_back(off);
+  stored = off;
+}
+
+uint64_t Layout::rank(const int* j) const {
+  uint64_t acc = 0;
+  int lo = 0;
+  for (int i = 0; i < order; ++i) {
+    const int rem = order - 1 - i;
+    acc += prefix[static_cast<std::size_t>(rem) * (grid + 1) + j[i]] -
+           prefix[static_cast<std::size_t>(rem) * (grid + 1) + lo];
+    lo = j[i];
+  }
+  return acc;
+}
+
+uint64_t Layout::element_offset(const int* i) const {
+  int j[20];
+  for (int k = 0; k < order; ++k) j[k] = i[k] / block;
+  const uint64_t r = rank(j);
+  uint64_t off = 0;
+  for (int k = 0; k < order; ++k)
+    off = off * static_cast<uint64_t>(ext(j[k])) + static_cast<uint64_t>(i[k] - j[k] * block);
+  return offset[r] + off;
+}
+
+uint64_t block_multiplicity(const int* j, int d) {
+  uint64_t num = 1;
+  for (int i = 2; i <= d; ++i) num *= static_cast<uint64_t>(i);
+  for (int s = 0; s < d;) {
+    int e = s + 1;
+    while (e < d && j[e] == j[s]) ++e;
+    for (int i = 2; i <= e - s; ++i) num /= static_cast<uint64_t>(i);
+    s = e;
+  }
+  return num;
+}
+
+void MomentPlan::build(int S_, int n_, int b_, const Layout& top, const Layout* low, int threads) {
+  S = S_;
+  L = S_ - 1;
+  n = n_;
+  b = b_;
+  rows.clear();
+  tiles.clear();
+  const int grid = top.grid;
+  // canonical L-tuples in lexicographic order, bucketed by J = i_L / b
+  std::vector<std::vector<PrefixRow>> byJ(grid);
+  if (L == 0) {
+    PrefixRow r{};
+    r.top_base = 0;
+    r.low_off = 0;
+    r.vprime = 1;
+    r.poff = 0;
+    byJ[0].push_back(r);
+  } else {
+    int t[8] = {0};
+    int jj[8], full[8];
+    for (;;) {
+      PrefixRow r{};
+      uint32_t vprime = 1, poff = 0;
+      for (int k = 0; k < L; ++k) {
+        r.idx[k] = static_cast<uint16_t>(t[k]);
+        jj[k] = t[k] / b;
+        const int e = top.ext(jj[k]);
+        vprime *= static_cast<uint32_t>(e);
+        poff = poff * static_cast<uint32_t>(e) + static_cast<uint32_t>(t[k] - jj[k] * b);
+      }
+      const int J = jj[L - 1];
+      for (int k = 0; k < L; ++k) full[k] = jj[k];
+      full[L] = J;
+      r.top_base = top.offset[top.rank(full)];
+      r.low_off = low ? low->offset[low->rank(jj)] + poff : 0;
+      r.vprime = vprime;
+      r.poff = poff;
+      byJ[J].push_back(r);
+      int k = L - 1;
+      while (k >= 0 && t[k] == n - 1) --k;
+      if (k < 0) break;
+      const int v = t[k] + 1;
+      for (int l = k; l < L; ++l) t[l] = v;
+    }
+  }
+  constexpr int kMaxTileRows = 1024;
+  for (int J = 0; J < grid; ++J) {
+    const auto& R = byJ[J];
+    if (R.empty()) continue;
+    const uint32_t col0 = static_cast<uint32_t>(J * b);
+    const uint32_t ncols = static_cast<uint32_t>(n - J * b);
+    const int cg = static_cast<int>((ncols + 7) / 8);
+    int rg_max = std::max(1, threads / cg);
+    rg_max = std::min(rg_max, kMaxTileRows / 8);
+    const uint64_t cap = static_cast<uint64_t>(rg_max) * 8;
+    const uint64_t nt = (R.size() + cap - 1) / cap;
+    uint64_t per = (R.size() + nt - 1) / nt;
+    per = (per + 7) / 8 * 8;
+    const uint32_t base = static_cast<uint32_t>(rows.size());
+    rows.insert(rows.end(), R.begin(), R.end());
+    for (uint64_t r0 = 0; r0 < R.size(); r0 += per) {
+      MomTile t{};
+      t.row0 = base + static_cast<uint32_t>(r0);
+      t.nrows = static_cast<uint32_t>(std::min<uint64_t>(per, R.size() - r0));
+      t.J = static_cast<uint32_t>(J);
+      t.col0 = col0;
+      t.ncols = ncols;
+      t.low = (L > 0 && low) ? 1u : 0u;
+      tiles.push_back(t);
+    }
+  }
+  // largest tiles first (the hardware dispatches in blockIdx order)
+  std::stable_sort(tiles.begin(), tiles.end(), [](const MomTile& a, const MomTile& c) {
+    return static_cast<uint64_t>(a.nrows) * a.ncols > static_cast<uint64_t>(c.nrows) * c.ncols;
+  });
+  scratch_per_tile = static_cast<uint64_t>(threads) * 64;
+}
+
+void MomentPlan::upload() {
+  d_rows.alloc(rows.size());
+  d_tiles.alloc(tiles.size());
+  if (!rows.empty())
+    CSB_CUDA(cudaMemcpy(d_rows.ptr, rows.data(), d_rows.bytes(), cudaMemcpyHostToDevice));
+  if (!tiles.empty())
+    CSB_CUDA(cudaMemcpy(d_tiles.ptr, tiles.data(), d_tiles.bytes(), cudaMemcpyHostToDevice));
+}
+
+}  // namespace csb

@@ -1,0 +1,73 @@
+// Host-side block layout and launch plans.
+//
+// Layout reproduces the reference's SymTensor storage bit for bit
+// (/root/reference/proj/src/symten.cpp:105-140): blocks with non-decreasing
+// block index j in lexicographic order, each a dense C-order block with
+// extents min(b, n - j_k b), one flat array.  The block ranker is the
+// reference's lexicographic multiset rank (symten.hpp:19-59).
+//
+// MomentPlan is the GEMM view of one pair of orders (S, S-1) (SURVEY
+// Appendix B): rows = canonical (S-1)-prefixes (i_1 <= ... <= i_{S-1}),
+// grouped by the block J = i_{S-1} / b of their last index; columns =
+// i_S in [J b, n).  M_S[prefix, i_S] = sum_rows A[row, prefix] x[row, i_S]
+// with A the left-to-right product of the prefix columns, and
+// M_{S-1}[prefix] = sum_rows A[row, prefix].
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "common.hpp"
+
+namespace csb {
+
+constexpr int kMaxOrder = CSB_MAX_ORDER;
+
+struct Layout {
+  int order = 0, dim = 0, block = 0, grid = 0;
+  uint64_t nblocks = 0, stored = 0;
+  std::vector<uint16_t> index;    // nblocks x order block coordinates
+  std::vector<uint64_t> offset;   // nblocks + 1 (last = stored)
+  std::vector<uint64_t> prefix;   // ranker table: order x (grid + 1)
+
+  Layout() = default;
+  Layout(int order, int dim, int block);
+
+  int ext(int j) const { return block < dim - j * block ? block : dim - j * block; }
+  uint64_t rank(const int* j) const;          // block rank of a sorted block index
+  uint64_t element_offset(const int* i) const;  // at_sorted_unchecked addressing
+  uint64_t volume(uint64_t r) const { return offset[r + 1] - offset[r]; }
+};
+
+uint64_t block_multiplicity(const int* j, int d);
+
+// One prefix row of the GEMM view (48 bytes, 16-byte aligned).
+struct alignas(16) PrefixRow {
+  uint16_t idx[8];    // i_1..i_L (L = S-1 <= 7)
+  uint64_t top_base;  // offset in M_S of block (j_1..j_L, J)
+  uint64_t low_off;   // offset in M_{S-1} of this prefix's canonical element
+  uint32_t vprime;    // prefix block volume prod_{k<=L} e(j_k)
+  uint32_t poff;      // in-block prefix offset (Horner over o_1..o_L)
+};
+static_assert(sizeof(PrefixRow) == 48, "PrefixRow layout");
+
+struct MomTile {
+  uint32_t row0, nrows;  // range in the row table
+  uint32_t J;            // block of the last prefix index
+  uint32_t col0, ncols;  // absolute column range [col0, col0 + ncols)
+  uint32_t low;          // 1: this tile also owns the M_{S-1} sums of its rows
+  uint32_t pad0, pad1;
+};
+
+struct MomentPlan {
+  int S = 0, L = 0, n = 0, b = 0;
+  std::vector<PrefixRow> rows;
+  std::vector<MomTile> tiles;
+  DevBuf<PrefixRow> d_rows;
+  DevBuf<MomTile> d_tiles;
+  uint64_t scratch_per_tile = 0;  // doubles
+  void build(int S, int n, int b, const Layout& top, const Layout* low, int threads);
+  void upload();
+};
+
+}  // namespace csb

@@ -1,0 +1,915 @@
+// Host runtime of cumstream_b200: device-resident series and window state,
+// cached layouts and launch plans, and the extern "C" entry points declared
+// in include/cumstream_b200.h.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "common.hpp"
+#include "kernels.cuh"
+#include "layout.hpp"
+
+namespace csb {
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_rows_read{0};
+
+struct DevLayout {
+  Layout host;
+  DevBuf<uint64_t> offset;
+  DevBuf<uint16_t> index;
+  DevBuf<uint64_t> prefix;
+  DevBuf<double> mult;
+  LayoutDev view() const {
+    LayoutDev v;
+    v.offset = offset.ptr;
+    v.index = index.ptr;
+    v.prefix = prefix.ptr;
+    v.order = host.order;
+    v.grid = host.grid;
+    return v;
+  }
+};
+
+struct Device {
+  int id = 0;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  std::map<std::tuple<int, int, int>, std::shared_ptr<DevLayout>> layouts;
+  std::map<std::tuple<int, int, int>, std::shared_ptr<MomentPlan>> plans;
+};
+
+std::mutex g_dev_mu;
+std::map<int, std::unique_ptr<Device>> g_devices;
+
+int current_device_id() {
+  int d = 0;
+  CSB_CUDA(cudaGetDevice(&d));
+  return d;
+}
+
+Device& device() {
+  ensure_device();
+  const int id = current_device_id();
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  auto& slot = g_devices[id];
+  if (!slot) {
+    slot = std::make_unique<Device>();
+    slot->id = id;
+    CSB_CUDA(cudaStreamCreateWithFlags(&slot->stream, cudaStreamNonBlocking));
+  }
+  return *slot;
+}
+
+std::shared_ptr<DevLayout> get_layout(Device& dev, int order, int n, int b) {
+  std::lock_guard<std::mutex> lk(dev.mu);
+  auto& slot = dev.layouts[{order, n, b}];
+  if (!slot) {
+    auto L = std::make_shared<DevLayout>();
+    L->host = Layout(order, n, b);
+    const Layout& h = L->host;
+    L->offset.alloc(h.offset.size());
+    L->index.alloc(h.index.size());
+    L->prefix.alloc(h.prefix.size());
+    L->mult.alloc(h.nblocks);
+    std::vector<double> mult(h.nblocks);
+    int j[20];
+    for (uint64_t r = 0; r < h.nblocks; ++r) {
+      for (int k = 0; k < order; ++k) j[k] = h.index[r * order + k];
+      mult[r] = static_cast<double>(block_multiplicity(j, order));
+    }
+    CSB_CUDA(cudaMemcpy(L->offset.ptr, h.offset.data(), L->offset.bytes(), cudaMemcpyHostToDevice));
+    CSB_CUDA(cudaMemcpy(L->index.ptr, h.index.data(), L->index.bytes(), cudaMemcpyHostToDevice));
+    CSB_CUDA(cudaMemcpy(L->prefix.ptr, h.prefix.data(), L->prefix.bytes(), cudaMemcpyHostToDevice));
+    CSB_CUDA(cudaMemcpy(L->mult.ptr, mult.data(), L->mult.bytes(), cudaMemcpyHostToDevice));
+    slot = L;
+  }
+  return slot;
+}
+
+std::shared_ptr<MomentPlan> get_plan(Device& dev, int S, int n, int b) {
+  auto top = get_layout(dev, S, n, b);
+  std::shared_ptr<DevLayout> low = S > 1 ? get_layout(dev, S - 1, n, b) : nullptr;
+  std::lock_guard<std::mutex> lk(dev.mu);
+  auto& slot = dev.plans[{S, n, b}];
+  if (!slot) {
+    auto p = std::make_shared<MomentPlan>();
+    p->build(S, n, b, top->host, low ? &low->host : nullptr, kMomThreads);
+    p->upload();
+    slot = p;
+  }
+  return slot;
+}
+
+// Optional per-launch event timing (csb_profile_enable).
+struct Profiler {
+  std::mutex mu;
+  bool on = false;
+  struct Rec {
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  };
+  std::map<std::string, Rec> recs;
+};
+Profiler g_prof;
+
+struct ProfScope {
+  cudaEvent_t a = nullptr, b = nullptr;
+  cudaStream_t st;
+  const char* tag;
+  ProfScope(const char* tag_, cudaStream_t st_) : st(st_), tag(tag_) {
+    if (!g_prof.on) return;
+    CSB_CUDA(cudaEventCreate(&a));
+    CSB_CUDA(cudaEventCreate(&b));
+    CSB_CUDA(cudaEventRecord(a, st));
+  }
+  ~ProfScope() {
+    if (!a) return;
+    cudaEventRecord(b, st);
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    g_prof.recs[tag].ev.emplace_back(a, b);
+  }
+};
+
+}  // namespace
+
+void ensure_device() {
+  int count = 0;
+  const cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    fail(CSB_ERUNTIME, "cumstream_b200: no CUDA device (this library has no CPU fallback)");
+  }
+}
+
+}  // namespace csb
+
+using namespace csb;
+
+// ---------------------------------------------------------------------------
+struct csb_series {
+  int n = 0, d = 0, b = 0;
+  uint64_t window_len = 0;
+  Device* dev = nullptr;
+  std::vector<std::shared_ptr<DevLayout>> lay;  // orders 1..d
+  std::vector<DevBuf<double>> data;
+};
+
+namespace csb {
+namespace {
+
+std::unique_ptr<csb_series> make_series(int n, int d, int b) {
+  require(n >= 1, "series: dim must be positive");
+  require(d >= 1 && d <= kMaxOrder, "series: max_order must be in [1, 8] on the device path");
+  require(b >= 1 && b <= n, "series: block_size must be in [1, dim]");
+  Device& dev = device();
+  auto s = std::make_unique<csb_series>();
+  s->n = n;
+  s->d = d;
+  s->b = b;
+  s->dev = &dev;
+  for (int k = 1; k <= d; ++k) {
+    s->lay.push_back(get_layout(dev, k, n, b));
+    s->data.emplace_back(s->lay.back()->host.stored);
+    CSB_CUDA(cudaMemsetAsync(s->data.back().ptr, 0, s->data.back().bytes(), dev.stream));
+  }
+  CSB_CUDA(cudaStreamSynchronize(dev.stream));
+  return s;
+}
+
+void check_order(const csb_series* s, int order) {
+  require(s != nullptr, "null series");
+  if (order < 1 || order > s->d) fail(CSB_ERANGE, "series: order out of range");
+}
+
+// Scratch buffer for the pass-0 stash of the update kernel (per device).
+struct Scratch {
+  DevBuf<double> buf;
+  double* get(uint64_t count) {
+    if (buf.count < count) buf.alloc(count);
+    return buf.ptr;
+  }
+};
+thread_local std::map<int, Scratch> g_scratch;
+
+// Orders are processed as pairs (S, S-1): (d, d-1), (d-2, d-3), ... with a
+// lone order 1 when d is odd.  Only the pair topped by d uses the fused
+// multiply-add of the reference's deepest loop (moments.cpp:47).
+void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, double c,
+                 cudaStream_t st, int only_order = 0) {
+  Device& dev = *m->dev;
+  const int d = m->d;
+  for (int S = d; S >= 1; S -= 2) {
+    if (only_order && S != only_order) continue;
+    auto plan = get_plan(dev, S, m->n, m->b);
+    MomParams p;
+    p.src[0] = src[0];
+    p.src[1] = src[1];
+    p.npass = npass;
+    p.K = static_cast<uint32_t>(K);
+    p.n = m->n;
+    p.b = m->b;
+    p.L = S - 1;
+    p.rows = plan->d_rows.ptr;
+    p.tiles = plan->d_tiles.ptr;
+    p.top = m->data[S - 1].ptr;
+    p.low = (S > 1 && !only_order) ? m->data[S - 2].ptr : nullptr;
+    p.c = c;
+    p.inv = 1.0 / static_cast<double>(K);
+    const uint64_t ntiles = plan->tiles.size();
+    if (npass == 2) p.scratch = g_scratch[dev.id].get(ntiles * plan->scratch_per_tile);
+    const bool top = S == (only_order ? only_order : d);
+    ProfScope ps(top ? "moment_top" : "moment_low", st);
+    launch_moment_pair(p, static_cast<int>(ntiles), top, st);
+  }
+}
+
+void check_batch(uint64_t rows, uint64_t cols, const char* what) {
+  if (rows < 1) fail(CSB_EINVAL, std::string(what) + ": empty batch");
+  if (cols < 1) fail(CSB_EINVAL, std::string(what) + ": no columns");
+  if (rows > 0xffffffffull) fail(CSB_EINVAL, std::string(what) + ": too many rows");
+}
+
+// moms2cums into c, with per-block partial squared norms for every order.
+struct NormScratch {
+  std::vector<DevBuf<double>> partial;  // per order
+  DevBuf<double> out;
+  std::vector<double> host;
+};
+
+void run_moms2cums(const csb_series* m, csb_series* c, NormScratch& ns, cudaStream_t st) {
+  const int d = m->d;
+  if (ns.partial.size() != static_cast<size_t>(d)) {
+    ns.partial.clear();
+    for (int s = 1; s <= d; ++s) ns.partial.emplace_back(m->lay[s - 1]->host.nblocks);
+  }
+  ProfScope ps("moms2cums", st);
+  const auto& L1 = m->lay[0];
+  launch_copy_c1(m->data[0].ptr, c->data[0].ptr, ns.partial[0].ptr, L1->view(), L1->host.nblocks,
+                 L1->host.stored, st);
+  for (int s = 2; s <= d; ++s) {
+    M2CParams p;
+    p.m = m->data[s - 1].ptr;
+    p.c = c->data[s - 1].ptr;
+    for (int k = 1; k < s; ++k) p.lower[k - 1] = c->data[k - 1].ptr;
+    for (int k = 1; k <= s; ++k) p.lay[k - 1] = m->lay[k - 1]->view();
+    p.n = m->n;
+    p.b = m->b;
+    p.blk0 = 0;
+    p.partial = ns.partial[s - 1].ptr;
+    launch_moms2cums(s, p, m->lay[s - 1]->host.nblocks, st);
+  }
+  c->window_len = m->window_len;
+}
+
+// Device offsets of the diagonals c_2[i,i], c_3[i,i,i], c_4[i,i,i,i].
+struct DiagTables {
+  DevBuf<uint64_t> off[3];
+};
+
+DiagTables& diag_tables(const csb_series* c) {
+  static thread_local std::map<std::tuple<int, int, int, int>, DiagTables> cache;
+  auto& t = cache[{c->dev->id, c->n, c->b, c->d}];
+  if (!t.off[0].ptr) {
+    for (int q = 0; q < 3; ++q) {
+      const int order = q + 2;
+      if (order > c->d) continue;
+      std::vector<uint64_t> off(c->n);
+      int idx[8];
+      for (int i = 0; i < c->n; ++i) {
+        for (int k = 0; k < order; ++k) idx[k] = i;
+        off[i] = c->lay[order - 1]->host.element_offset(idx);
+      }
+      t.off[q].alloc(c->n);
+      CSB_CUDA(cudaMemcpy(t.off[q].ptr, off.data(), t.off[q].bytes(), cudaMemcpyHostToDevice));
+    }
+  }
+  return t;
+}
+
+// Norm sums of orders 1..d (from partials) + diagonals, to the host.
+void finalize_norms(const csb_series* c, NormScratch& ns, cudaStream_t st) {
+  const int d = c->d;
+  NormParams p;
+  p.norders = d;
+  for (int s = 1; s <= d; ++s) {
+    p.partial[s - 1] = ns.partial[s - 1].ptr;
+    p.mult[s - 1] = c->lay[s - 1]->mult.ptr;
+    p.nblocks[s - 1] = c->lay[s - 1]->host.nblocks;
+  }
+  DiagTables& dt = diag_tables(c);
+  for (int q = 0; q < 3; ++q) {
+    p.diag_src[q] = (q + 2 <= d) ? c->data[q + 1].ptr : nullptr;
+    p.diag_off[q] = dt.off[q].ptr;
+  }
+  p.n = c->n;
+  const uint64_t need = d + 3ull * c->n;
+  if (ns.out.count < need) ns.out.alloc(need);
+  p.out = ns.out.ptr;
+  {
+    ProfScope ps("norms", st);
+    launch_norm_finalize(p, st);
+  }
+  ns.host.resize(need);
+  CSB_CUDA(cudaMemcpyAsync(ns.host.data(), ns.out.ptr, need * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CSB_CUDA(cudaStreamSynchronize(st));
+}
+
+// make_window_report from the finalized sums (gauge.cpp:35-41,64-94,142-154).
+void build_report(const csb_series* c, const NormScratch& ns, uint64_t window, csb_report* r) {
+  const int d = c->d;
+  if (d < 2) fail(CSB_EINVAL, "make_window_report: needs orders up to 2");
+  std::memset(r, 0, sizeof(*r));
+  r->window = window;
+  r->rows = c->window_len;
+  const double* sums = ns.host.data();
+  r->norm_c1 = std::sqrt(sums[0]);
+  r->norm_c2 = std::sqrt(sums[1]);
+  r->n_nu = 0;
+  for (int o = 3; o <= d; ++o) {
+    const double n2 = r->norm_c2;
+    if (n2 <= 0.0) fail(CSB_EDOMAIN, "nu: vanishing second-order cumulant norm");
+    r->nu[r->n_nu++] = std::sqrt(sums[o - 1]) / std::pow(n2, 0.5 * static_cast<double>(o));
+  }
+  const double* c2 = sums + d;
+  if (d >= 3) {
+    const double* c3 = sums + d + c->n;
+    double best = 0.0;
+    for (int i = 0; i < c->n; ++i) {
+      if (c2[i] <= 0.0) fail(CSB_EDOMAIN, "max_abs_diag_skewness: zero variance");
+      best = std::max(best, std::abs(c3[i]) / std::pow(c2[i], 1.5));
+    }
+    r->has_skewness = 1;
+    r->max_abs_skewness = best;
+  }
+  if (d >= 4) {
+    const double* c4 = sums + d + 2 * c->n;
+    double best = 0.0;
+    for (int i = 0; i < c->n; ++i) {
+      if (c2[i] <= 0.0) fail(CSB_EDOMAIN, "max_abs_diag_kurtosis: zero variance");
+      best = std::max(best, std::abs(c4[i]) / (c2[i] * c2[i]));
+    }
+    r->has_kurtosis = 1;
+    r->max_abs_kurtosis = best;
+  }
+}
+
+double knorm_device(const csb_series* s, int order, double k, cudaStream_t st) {
+  if (!(k >= 1.0)) fail(CSB_EINVAL, "knorm: k must be >= 1");
+  const auto& L = s->lay[order - 1];
+  DevBuf<double> partial(L->host.nblocks);
+  launch_knorm_partials(s->data[order - 1].ptr, L->view(), L->host.nblocks, k, partial.ptr, st);
+  NormParams p;
+  p.norders = 1;
+  p.partial[0] = partial.ptr;
+  p.mult[0] = L->mult.ptr;
+  p.nblocks[0] = L->host.nblocks;
+  p.n = 0;
+  DevBuf<double> out(1);
+  p.out = out.ptr;
+  launch_norm_finalize(p, st);
+  double acc = 0.0;
+  CSB_CUDA(cudaMemcpyAsync(&acc, out.ptr, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CSB_CUDA(cudaStreamSynchronize(st));
+  if (k == 2.0) return std::sqrt(acc);
+  if (k == 1.0) return acc;
+  return std::pow(acc, 1.0 / k);
+}
+
+}  // namespace
+}  // namespace csb
+
+// ---------------------------------------------------------------------------
+struct csb_stream {
+  csb_stream_config cfg{};
+  Device* dev = nullptr;
+  cudaStream_t st = nullptr;
+  DevBuf<double> ring;      // window_len x dim, head = oldest row
+  uint64_t head = 0;
+  DevBuf<double> staging;   // update_len x dim
+  std::unique_ptr<csb_series> M, C;
+  uint64_t window = 0;
+  uint64_t steps_since_resync = 0;
+  NormScratch ns;
+  bool norms_valid = false;
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  ~csb_stream() {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+};
+
+namespace {
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return CSB_OK;
+  } catch (const csb::Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    g_last_error = e.what();
+    return CSB_ERUNTIME;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return CSB_ERUNTIME;
+  }
+}
+
+void stream_exchange_and_update(csb_stream* s, const double* x_dev) {
+  const auto& cfg = s->cfg;
+  const uint64_t T = cfg.window_len, p = cfg.update_len, n = cfg.dim;
+  // outgoing rows: ring[head .. head+p) with wrap (WindowBuffer::exchange, stream.cpp:39-54)
+  RowSource out;
+  const uint64_t first = std::min(p, T - s->head);
+  out.seg0 = s->ring.ptr + s->head * n;
+  out.len0 = static_cast<uint32_t>(first);
+  out.seg1 = s->ring.ptr;
+  out.len1 = static_cast<uint32_t>(p - first);
+  const bool resync = cfg.resync_every > 0 && s->steps_since_resync + 1 >= cfg.resync_every;
+  if (!resync) {
+    RowSource src[2];
+    src[0].seg0 = x_dev;
+    src[0].len0 = static_cast<uint32_t>(p);
+    src[1] = out;
+    run_moments(s->M.get(), src, 2, p, static_cast<double>(p) / static_cast<double>(T), s->st);
+    g_rows_read.fetch_add(2 * p, std::memory_order_relaxed);
+  }
+  // incoming rows take the outgoing slots
+  CSB_CUDA(cudaMemcpyAsync(s->ring.ptr + s->head * n, x_dev, first * n * sizeof(double),
+                           cudaMemcpyDeviceToDevice, s->st));
+  if (p > first)
+    CSB_CUDA(cudaMemcpyAsync(s->ring.ptr, x_dev + first * n, (p - first) * n * sizeof(double),
+                             cudaMemcpyDeviceToDevice, s->st));
+  s->head = (s->head + p) % T;
+  if (resync) {
+    // moment_series(materialize()) (stream.cpp:92-95): arrival order from head
+    RowSource src[2];
+    src[0].seg0 = s->ring.ptr + s->head * n;
+    src[0].len0 = static_cast<uint32_t>(T - s->head);
+    src[0].seg1 = s->ring.ptr;
+    src[0].len1 = static_cast<uint32_t>(s->head);
+    run_moments(s->M.get(), src, 1, T, 0.0, s->st);
+    g_rows_read.fetch_add(T, std::memory_order_relaxed);
+    s->steps_since_resync = 0;
+  } else {
+    ++s->steps_since_resync;
+  }
+}
+
+int stream_step_impl(csb_stream* s, const double* x, bool on_device, uint64_t rows, uint64_t cols,
+                     csb_step_timing* timing, csb_report* report) {
+  return guard([&] {
+    require(s != nullptr, "step: null stream");
+    const auto& cfg = s->cfg;
+    if (rows != cfg.update_len || cols != static_cast<uint64_t>(cfg.dim))
+      fail(CSB_EINVAL, "step: batch does not match the configured update");
+    CSB_CUDA(cudaSetDevice(s->dev->id));
+    const double* xd = x;
+    if (!on_device) {
+      CSB_CUDA(cudaMemcpyAsync(s->staging.ptr, x, rows * cols * sizeof(double), cudaMemcpyHostToDevice, s->st));
+      xd = s->staging.ptr;
+    }
+    CSB_CUDA(cudaEventRecord(s->ev[0], s->st));
+    stream_exchange_and_update(s, xd);
+    CSB_CUDA(cudaEventRecord(s->ev[1], s->st));
+    run_moms2cums(s->M.get(), s->C.get(), s->ns, s->st);
+    CSB_CUDA(cudaEventRecord(s->ev[2], s->st));
+    s->norms_valid = false;
+    ++s->window;
+    if (report) {
+      finalize_norms(s->C.get(), s->ns, s->st);
+      s->norms_valid = true;
+      build_report(s->C.get(), s->ns, s->window, report);
+    }
+    if (timing) {
+      CSB_CUDA(cudaEventSynchronize(s->ev[2]));
+      float a = 0, b = 0;
+      CSB_CUDA(cudaEventElapsedTime(&a, s->ev[0], s->ev[1]));
+      CSB_CUDA(cudaEventElapsedTime(&b, s->ev[1], s->ev[2]));
+      timing->update_s = a * 1e-3;
+      timing->moms2cums_s = b * 1e-3;
+    }
+  });
+}
+
+}  // namespace
+
+extern "C" {
+
+int csb_version(void) { return 1; }
+const char* csb_last_error(void) { return g_last_error.c_str(); }
+
+int csb_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int csb_set_device(int d) {
+  return guard([&] {
+    ensure_device();
+    CSB_CUDA(cudaSetDevice(d));
+  });
+}
+
+uint64_t csb_rows_read(void) { return g_rows_read.load(std::memory_order_relaxed); }
+
+int csb_layout_size(int order, int dim, int block, uint64_t* stored, uint64_t* blocks) {
+  return guard([&] {
+    require(stored && blocks, "layout_size: null output");
+    Layout L(order, dim, block);
+    *stored = L.stored;
+    *blocks = L.nblocks;
+  });
+}
+
+int csb_block_multiplicity(const int* j, int order, uint64_t* out) {
+  return guard([&] {
+    require(order >= 1, "block_multiplicity: empty index");
+    require(order <= 20, "block_multiplicity: order too large for exact count");
+    for (int k = 1; k < order; ++k)
+      require(j[k - 1] <= j[k], "block_multiplicity: index not non-decreasing");
+    *out = block_multiplicity(j, order);
+  });
+}
+
+int csb_series_create(int dim, int max_order, int block, csb_series** out) {
+  return guard([&] {
+    require(out != nullptr, "series_create: null output");
+    *out = make_series(dim, max_order, block).release();
+  });
+}
+
+int csb_series_destroy(csb_series* s) {
+  return guard([&] { delete s; });
+}
+
+int csb_series_copy(csb_series* dst, const csb_series* src) {
+  return guard([&] {
+    require(dst && src, "series_copy: null series");
+    require(dst->n == src->n && dst->d == src->d && dst->b == src->b, "series_copy: shape mismatch");
+    for (int k = 0; k < src->d; ++k)
+      CSB_CUDA(cudaMemcpyAsync(dst->data[k].ptr, src->data[k].ptr, src->data[k].bytes(),
+                               cudaMemcpyDeviceToDevice, src->dev->stream));
+    CSB_CUDA(cudaStreamSynchronize(src->dev->stream));
+    dst->window_len = src->window_len;
+  });
+}
+
+int csb_series_shape(const csb_series* s, int* dim, int* max_order, int* block, uint64_t* wl) {
+  return guard([&] {
+    require(s != nullptr, "null series");
+    if (dim) *dim = s->n;
+    if (max_order) *max_order = s->d;
+    if (block) *block = s->b;
+    if (wl) *wl = s->window_len;
+  });
+}
+
+int csb_series_set_window_len(csb_series* s, uint64_t wl) {
+  return guard([&] {
+    require(s != nullptr, "null series");
+    s->window_len = wl;
+  });
+}
+
+int csb_series_stored(const csb_series* s, int order, uint64_t* stored) {
+  return guard([&] {
+    check_order(s, order);
+    *stored = s->lay[order - 1]->host.stored;
+  });
+}
+
+int csb_series_device_ptr(const csb_series* s, int order, double** dev) {
+  return guard([&] {
+    check_order(s, order);
+    *dev = s->data[order - 1].ptr;
+  });
+}
+
+int csb_series_upload(csb_series* s, int order, const double* host, uint64_t count) {
+  return guard([&] {
+    check_order(s, order);
+    require(count == s->lay[order - 1]->host.stored, "series_upload: size mismatch");
+    CSB_CUDA(cudaMemcpy(s->data[order - 1].ptr, host, count * sizeof(double), cudaMemcpyHostToDevice));
+  });
+}
+
+int csb_series_download(const csb_series* s, int order, double* host, uint64_t count) {
+  return guard([&] {
+    check_order(s, order);
+    require(count == s->lay[order - 1]->host.stored, "series_download: size mismatch");
+    CSB_CUDA(cudaStreamSynchronize(s->dev->stream));
+    CSB_CUDA(cudaMemcpy(host, s->data[order - 1].ptr, count * sizeof(double), cudaMemcpyDeviceToHost));
+  });
+}
+
+static void moment_series_impl(csb_series* out, const double* xd, uint64_t rows, uint64_t) {
+  RowSource src[2];
+  src[0].seg0 = xd;
+  src[0].len0 = static_cast<uint32_t>(rows);
+  run_moments(out, src, 1, rows, 0.0, out->dev->stream);
+  out->window_len = rows;
+  g_rows_read.fetch_add(rows, std::memory_order_relaxed);
+}
+
+int csb_moment_series(csb_series* out, const double* x, uint64_t rows, uint64_t cols) {
+  return guard([&] {
+    require(out != nullptr, "moment_series: null series");
+    check_batch(rows, cols, "moment_series");
+    require(cols == static_cast<uint64_t>(out->n), "moment_series: dimension mismatch");
+    DevBuf<double> xd(rows * cols);
+    CSB_CUDA(cudaMemcpyAsync(xd.ptr, x, xd.bytes(), cudaMemcpyHostToDevice, out->dev->stream));
+    moment_series_impl(out, xd.ptr, rows, cols);
+    CSB_CUDA(cudaStreamSynchronize(out->dev->stream));
+  });
+}
+
+int csb_moment_series_dev(csb_series* out, const double* x, uint64_t rows, uint64_t cols) {
+  return guard([&] {
+    require(out != nullptr, "moment_series: null series");
+    check_batch(rows, cols, "moment_series");
+    require(cols == static_cast<uint64_t>(out->n), "moment_series: dimension mismatch");
+    moment_series_impl(out, x, rows, cols);
+    CSB_CUDA(cudaStreamSynchronize(out->dev->stream));
+  });
+}
+
+int csb_moment_tensor(csb_series* out, int order, const double* x, uint64_t rows, uint64_t cols) {
+  return guard([&] {
+    check_order(out, order);
+    check_batch(rows, cols, "moment_tensor");
+    require(cols == static_cast<uint64_t>(out->n), "moment_tensor: dimension mismatch");
+    DevBuf<double> xd(rows * cols);
+    CSB_CUDA(cudaMemcpyAsync(xd.ptr, x, xd.bytes(), cudaMemcpyHostToDevice, out->dev->stream));
+    RowSource src[2];
+    src[0].seg0 = xd.ptr;
+    src[0].len0 = static_cast<uint32_t>(rows);
+    run_moments(out, src, 1, rows, 0.0, out->dev->stream, order);
+    g_rows_read.fetch_add(rows, std::memory_order_relaxed);
+    CSB_CUDA(cudaStreamSynchronize(out->dev->stream));
+  });
+}
+
+static void update_impl(csb_series* m, const double* in, const double* outg, uint64_t rows) {
+  RowSource src[2];
+  src[0].seg0 = in;
+  src[0].len0 = static_cast<uint32_t>(rows);
+  src[1].seg0 = outg;
+  src[1].len0 = static_cast<uint32_t>(rows);
+  run_moments(m, src, 2, rows, static_cast<double>(rows) / static_cast<double>(m->window_len),
+              m->dev->stream);
+  g_rows_read.fetch_add(2 * rows, std::memory_order_relaxed);
+}
+
+static void check_update(const csb_series* m, uint64_t rows, uint64_t cols) {
+  require(m != nullptr, "moments_update: null series");
+  check_batch(rows, cols, "moments_update");
+  if (rows > m->window_len) fail(CSB_EINVAL, "moments_update: batch longer than the window");
+  if (cols != static_cast<uint64_t>(m->n)) fail(CSB_EINVAL, "moments_update: dimension mismatch");
+}
+
+int csb_moments_update(csb_series* m, const double* in, const double* outg, uint64_t rows, uint64_t cols) {
+  return guard([&] {
+    check_update(m, rows, cols);
+    DevBuf<double> xd(2 * rows * cols);
+    const uint64_t nb = rows * cols * sizeof(double);
+    CSB_CUDA(cudaMemcpyAsync(xd.ptr, in, nb, cudaMemcpyHostToDevice, m->dev->stream));
+    CSB_CUDA(cudaMemcpyAsync(xd.ptr + rows * cols, outg, nb, cudaMemcpyHostToDevice, m->dev->stream));
+    update_impl(m, xd.ptr, xd.ptr + rows * cols, rows);
+    CSB_CUDA(cudaStreamSynchronize(m->dev->stream));
+  });
+}
+
+int csb_moments_update_dev(csb_series* m, const double* in, const double* outg, uint64_t rows, uint64_t cols) {
+  return guard([&] {
+    check_update(m, rows, cols);
+    update_impl(m, in, outg, rows);
+    CSB_CUDA(cudaStreamSynchronize(m->dev->stream));
+  });
+}
+
+int csb_moms2cums(const csb_series* m, csb_series* c) {
+  return guard([&] {
+    require(m && c, "moms2cums: null series");
+    require(m->d >= 1, "moms2cums: empty series");
+    require(m->n == c->n && m->d == c->d && m->b == c->b, "moms2cums: series tensors disagree on shape");
+    NormScratch ns;
+    run_moms2cums(m, c, ns, m->dev->stream);
+    CSB_CUDA(cudaStreamSynchronize(m->dev->stream));
+  });
+}
+
+int csb_combine(const csb_series* m1, uint64_t s1, const csb_series* m2, uint64_t s2, csb_series* out) {
+  return guard([&] {
+    require(m1 && m2 && out, "combine: null series");
+    if (m1->d != m2->d) fail(CSB_EINVAL, "combine: order mismatch");
+    if (s1 + s2 == 0) fail(CSB_EINVAL, "combine: empty combination");
+    if (m1->n != m2->n || m1->b != m2->b || out->n != m1->n || out->b != m1->b || out->d != m1->d)
+      fail(CSB_EINVAL, "combine: shape mismatch");
+    const double w1 = static_cast<double>(s1) / static_cast<double>(s1 + s2);
+    const double w2 = static_cast<double>(s2) / static_cast<double>(s1 + s2);
+    for (int k = 0; k < m1->d; ++k)
+      launch_combine(m1->data[k].ptr, m2->data[k].ptr, w1, w2, out->data[k].ptr, m1->data[k].count,
+                     m1->dev->stream);
+    out->window_len = s1 + s2;
+    CSB_CUDA(cudaStreamSynchronize(m1->dev->stream));
+  });
+}
+
+int csb_knorm(const csb_series* s, int order, double k, double* out) {
+  return guard([&] {
+    check_order(s, order);
+    *out = knorm_device(s, order, k, s->dev->stream);
+  });
+}
+
+int csb_nu(const csb_series* c, int d, double* out) {
+  return guard([&] {
+    require(c != nullptr, "nu: null series");
+    if (d < 3 || d > c->d) fail(CSB_EINVAL, "nu: order must be in [3, max_order]");
+    const double n2 = knorm_device(c, 2, 2.0, c->dev->stream);
+    if (n2 <= 0.0) fail(CSB_EDOMAIN, "nu: vanishing second-order cumulant norm");
+    *out = knorm_device(c, d, 2.0, c->dev->stream) / std::pow(n2, 0.5 * static_cast<double>(d));
+  });
+}
+
+int csb_window_report(const csb_series* c, uint64_t window, csb_report* out) {
+  return guard([&] {
+    require(c && out, "window_report: null argument");
+    if (c->d < 2) fail(CSB_EINVAL, "make_window_report: needs orders up to 2");
+    NormScratch ns;
+    for (int s = 1; s <= c->d; ++s) {
+      const auto& L = c->lay[s - 1];
+      ns.partial.emplace_back(L->host.nblocks);
+      launch_knorm_partials(c->data[s - 1].ptr, L->view(), L->host.nblocks, 2.0, ns.partial.back().ptr,
+                            c->dev->stream);
+    }
+    finalize_norms(c, ns, c->dev->stream);
+    build_report(c, ns, window, out);
+  });
+}
+
+int csb_stream_prime(const csb_stream_config* cfg, const double* first, uint64_t rows, uint64_t cols,
+                     csb_stream** out) {
+  return guard([&] {
+    require(cfg && out, "prime: null argument");
+    // StreamConfig::validate (stream.cpp:18-27)
+    if (cfg->dim < 1) fail(CSB_EINVAL, "StreamConfig: dim must be positive");
+    if (cfg->max_order < 2) fail(CSB_EINVAL, "StreamConfig: max_order must be >= 2");
+    if (cfg->window_len < 1) fail(CSB_EINVAL, "StreamConfig: window_len must be positive");
+    if (cfg->update_len < 1 || cfg->update_len > cfg->window_len)
+      fail(CSB_EINVAL, "StreamConfig: update_len must be in [1, window_len]");
+    if (cfg->block_size < 1 || cfg->block_size > cfg->dim)
+      fail(CSB_EINVAL, "StreamConfig: block_size must be in [1, dim]");
+    if (cfg->workers < 0) fail(CSB_EINVAL, "StreamConfig: workers must be >= 0");
+    if (rows != cfg->window_len || cols != static_cast<uint64_t>(cfg->dim))
+      fail(CSB_EINVAL, "prime: batch does not match the configured window");
+    auto s = std::make_unique<csb_stream>();
+    s->cfg = *cfg;
+    s->dev = &device();
+    s->st = s->dev->stream;
+    s->M = make_series(cfg->dim, cfg->max_order, cfg->block_size);
+    s->C = make_series(cfg->dim, cfg->max_order, cfg->block_size);
+    s->ring.alloc(rows * cols);
+    s->staging.alloc(cfg->update_len * cols);
+    for (auto& e : s->ev) CSB_CUDA(cudaEventCreate(&e));
+    CSB_CUDA(cudaMemcpyAsync(s->ring.ptr, first, s->ring.bytes(), cudaMemcpyHostToDevice, s->st));
+    s->head = 0;
+    moment_series_impl(s->M.get(), s->ring.ptr, rows, cols);
+    run_moms2cums(s->M.get(), s->C.get(), s->ns, s->st);
+    s->window = 1;
+    s->steps_since_resync = 0;
+    CSB_CUDA(cudaStreamSynchronize(s->st));
+    *out = s.release();
+  });
+}
+
+int csb_stream_destroy(csb_stream* st) {
+  return guard([&] { delete st; });
+}
+
+int csb_stream_step(csb_stream* s, const double* x, uint64_t rows, uint64_t cols, csb_step_timing* t,
+                    csb_report* r) {
+  return stream_step_impl(s, x, false, rows, cols, t, r);
+}
+
+int csb_stream_step_dev(csb_stream* s, const double* x, uint64_t rows, uint64_t cols, csb_step_timing* t,
+                        csb_report* r) {
+  return stream_step_impl(s, x, true, rows, cols, t, r);
+}
+
+int csb_stream_report(csb_stream* s, csb_report* r) {
+  return guard([&] {
+    require(s && r, "stream_report: null argument");
+    if (!s->norms_valid) {
+      finalize_norms(s->C.get(), s->ns, s->st);
+      s->norms_valid = true;
+    }
+    build_report(s->C.get(), s->ns, s->window, r);
+  });
+}
+
+int csb_stream_moments(csb_stream* s, const csb_series** m) {
+  return guard([&] {
+    require(s && m, "null argument");
+    CSB_CUDA(cudaStreamSynchronize(s->st));
+    *m = s->M.get();
+  });
+}
+
+int csb_stream_cumulants(csb_stream* s, const csb_series** c) {
+  return guard([&] {
+    require(s && c, "null argument");
+    CSB_CUDA(cudaStreamSynchronize(s->st));
+    *c = s->C.get();
+  });
+}
+
+int csb_stream_window(const csb_stream* s, uint64_t* w) {
+  return guard([&] {
+    require(s && w, "null argument");
+    *w = s->window;
+  });
+}
+
+int csb_stream_materialize(const csb_stream* s, double* host, uint64_t count) {
+  return guard([&] {
+    require(s && host, "null argument");
+    const uint64_t T = s->cfg.window_len, n = s->cfg.dim;
+    require(count == T * n, "materialize: size mismatch");
+    CSB_CUDA(cudaStreamSynchronize(s->st));
+    const uint64_t tail = T - s->head;
+    CSB_CUDA(cudaMemcpy(host, s->ring.ptr + s->head * n, tail * n * sizeof(double), cudaMemcpyDeviceToHost));
+    if (s->head)
+      CSB_CUDA(cudaMemcpy(host + tail * n, s->ring.ptr, s->head * n * sizeof(double), cudaMemcpyDeviceToHost));
+  });
+}
+
+int csb_stream_norm_partials(csb_stream* s, int order, double* host, uint64_t count, uint64_t* first_block) {
+  return guard([&] {
+    require(s && host, "null argument");
+    if (order < 1 || order > s->cfg.max_order) fail(CSB_ERANGE, "norm_partials: order out of range");
+    const auto& buf = s->ns.partial.at(order - 1);
+    require(count == buf.count, "norm_partials: size mismatch");
+    CSB_CUDA(cudaStreamSynchronize(s->st));
+    CSB_CUDA(cudaMemcpy(host, buf.ptr, buf.bytes(), cudaMemcpyDeviceToHost));
+    if (first_block) *first_block = 0;
+  });
+}
+
+uint64_t csb_launch_count(void) { return csb::launch_count(); }
+
+int csb_profile_enable(int on) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    g_prof.on = on != 0;
+  });
+}
+
+int csb_profile_read(const char* tag, double* total_ms, uint64_t* launches) {
+  return guard([&] {
+    require(tag && total_ms && launches, "profile_read: null argument");
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+    {
+      std::lock_guard<std::mutex> lk(g_prof.mu);
+      ev.swap(g_prof.recs[tag].ev);
+    }
+    double tot = 0.0;
+    for (auto& [a, b] : ev) {
+      CSB_CUDA(cudaEventSynchronize(b));
+      float ms = 0.f;
+      CSB_CUDA(cudaEventElapsedTime(&ms, a, b));
+      tot += ms;
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+    }
+    *total_ms = tot;
+    *launches = ev.size();
+  });
+}
+
+int csb_stream_cuda_stream(csb_stream* s, void** cs) {
+  return guard([&] {
+    require(s && cs, "null argument");
+    *cs = s->st;
+  });
+}
+
+}  // extern "C"
