@@ -72,5 +72,13 @@ constexpr int kMomThreads = 256;
 // Kernels this library has launched in this process (bench.py's
 // gpu_launches claim).
 uint64_t launch_count();
+void count_launch();
+
+// FP64 tensor-core (DMMA) kernel for the top pair of orders (moment_dmma.cu)
+bool dmma_supported(const MomParams& p);
+int dmma_rows_per_warp(int ncol_groups);
+int dmma_warps();
+size_t dmma_scratch_per_tile();
+void launch_moment_top_dmma(const MomParams& p, int ntiles, cudaStream_t st);
 
 }  // namespace csb

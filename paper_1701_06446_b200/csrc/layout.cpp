@@ -77,7 +77,8 @@ uint64_t block_multiplicity(const int* j, int d) {
   return num;
 }
 
-void MomentPlan::build(int S_, int n_, int b_, const Layout& top, const Layout* low, int threads) {
+std::vector<std::vector<PrefixRow>> MomentPlan::enumerate(int S_, int n_, int b_, const Layout& top,
+                                                          const Layout* low) {
   S = S_;
   L = S_ - 1;
   n = n_;
@@ -94,34 +95,78 @@ void MomentPlan::build(int S_, int n_, int b_, const Layout& top, const Layout* 
     r.vprime = 1;
     r.poff = 0;
     byJ[0].push_back(r);
-  } else {
-    int t[8] = {0};
-    int jj[8], full[8];
-    for (;;) {
-      PrefixRow r{};
-      uint32_t vprime = 1, poff = 0;
-      for (int k = 0; k < L; ++k) {
-        r.idx[k] = static_cast<uint16_t>(t[k]);
-        jj[k] = t[k] / b;
-        const int e = top.ext(jj[k]);
-        vprime *= static_cast<uint32_t>(e);
-        poff = poff * static_cast<uint32_t>(e) + static_cast<uint32_t>(t[k] - jj[k] * b);
+    return byJ;
+  }
+  int t[8] = {0};
+  int jj[8], full[8];
+  for (;;) {
+    PrefixRow r{};
+    uint32_t vprime = 1, poff = 0;
+    for (int k = 0; k < L; ++k) {
+      r.idx[k] = static_cast<uint16_t>(t[k]);
+      jj[k] = t[k] / b;
+      const int e = top.ext(jj[k]);
+      vprime *= static_cast<uint32_t>(e);
+      poff = poff * static_cast<uint32_t>(e) + static_cast<uint32_t>(t[k] - jj[k] * b);
+    }
+    const int J = jj[L - 1];
+    for (int k = 0; k < L; ++k) full[k] = jj[k];
+    full[L] = J;
+    r.top_base = top.offset[top.rank(full)];
+    r.low_off = low ? low->offset[low->rank(jj)] + poff : 0;
+    r.vprime = vprime;
+    r.poff = poff;
+    byJ[J].push_back(r);
+    int k = L - 1;
+    while (k >= 0 && t[k] == n - 1) --k;
+    if (k < 0) break;
+    const int v = t[k] + 1;
+    for (int l = k; l < L; ++l) t[l] = v;
+  }
+  return byJ;
+}
+
+void MomentPlan::build_dmma(int S_, int n_, int b_, const Layout& top, const Layout* low, int warps,
+                            int (*rows_per_warp)(int), uint64_t scratch) {
+  auto byJ = enumerate(S_, n_, b_, top, low);
+  dmma = true;
+  for (int J = 0; J < top.grid; ++J) {
+    const auto& R = byJ[J];
+    if (R.empty()) continue;
+    const uint32_t base = static_cast<uint32_t>(rows.size());
+    rows.insert(rows.end(), R.begin(), R.end());
+    const int ncols_all = n - J * b;
+    const int ncg_all = (ncols_all + 7) / 8;
+    const int nranges = (ncg_all + 11) / 12;
+    for (int q = 0; q < nranges; ++q) {
+      // balanced column ranges of whole 8-column groups
+      const int g0 = q * ncg_all / nranges, g1 = (q + 1) * ncg_all / nranges;
+      const uint32_t col0 = static_cast<uint32_t>(J * b + 8 * g0);
+      const uint32_t ncols = static_cast<uint32_t>(std::min(8 * g1, ncols_all) - 8 * g0);
+      const int ncg = g1 - g0;
+      const uint64_t cap = static_cast<uint64_t>(warps) * rows_per_warp(ncg);
+      for (uint64_t r0 = 0; r0 < R.size(); r0 += cap) {
+        MomTile t{};
+        t.row0 = base + static_cast<uint32_t>(r0);
+        t.nrows = static_cast<uint32_t>(std::min<uint64_t>(cap, R.size() - r0));
+        t.J = static_cast<uint32_t>(J);
+        t.col0 = col0;
+        t.ncols = ncols;
+        t.low = (q == 0 && low) ? 1u : 0u;
+        t.pad0 = static_cast<uint32_t>(ncg);
+        tiles.push_back(t);
       }
-      const int J = jj[L - 1];
-      for (int k = 0; k < L; ++k) full[k] = jj[k];
-      full[L] = J;
-      r.top_base = top.offset[top.rank(full)];
-      r.low_off = low ? low->offset[low->rank(jj)] + poff : 0;
-      r.vprime = vprime;
-      r.poff = poff;
-      byJ[J].push_back(r);
-      int k = L - 1;
-      while (k >= 0 && t[k] == n - 1) --k;
-      if (k < 0) break;
-      const int v = t[k] + 1;
-      for (int l = k; l < L; ++l) t[l] = v;
     }
   }
+  std::stable_sort(tiles.begin(), tiles.end(), [](const MomTile& a, const MomTile& c) {
+    return static_cast<uint64_t>(a.nrows) * a.ncols > static_cast<uint64_t>(c.nrows) * c.ncols;
+  });
+  scratch_per_tile = scratch;
+}
+
+void MomentPlan::build(int S_, int n_, int b_, const Layout& top, const Layout* low, int threads) {
+  auto byJ = enumerate(S_, n_, b_, top, low);
+  const int grid = top.grid;
   constexpr int kMaxTileRows = 1024;
   for (int J = 0; J < grid; ++J) {
     const auto& R = byJ[J];

@@ -66,8 +66,16 @@ struct MomentPlan {
   DevBuf<PrefixRow> d_rows;
   DevBuf<MomTile> d_tiles;
   uint64_t scratch_per_tile = 0;  // doubles
+  bool dmma = false;  // tiles are for moment_top_dmma_kernel (pad0 = column groups)
   void build(int S, int n, int b, const Layout& top, const Layout* low, int threads);
+  // Tiles for the DMMA kernel: rows grouped by J in runs of warps x
+  // rows_per_warp(ncg), column ranges of at most 12 groups of 8.
+  void build_dmma(int S, int n, int b, const Layout& top, const Layout* low, int warps,
+                  int (*rows_per_warp)(int), uint64_t scratch_per_tile);
   void upload();
+
+ private:
+  std::vector<std::vector<PrefixRow>> enumerate(int S, int n, int b, const Layout& top, const Layout* low);
 };
 
 }  // namespace csb

@@ -6,6 +6,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -47,7 +48,7 @@ struct Device {
   cudaStream_t stream = nullptr;
   std::mutex mu;
   std::map<std::tuple<int, int, int>, std::shared_ptr<DevLayout>> layouts;
-  std::map<std::tuple<int, int, int>, std::shared_ptr<MomentPlan>> plans;
+  std::map<std::tuple<int, int, int, int>, std::shared_ptr<MomentPlan>> plans;
 };
 
 std::mutex g_dev_mu;
@@ -98,14 +99,18 @@ std::shared_ptr<DevLayout> get_layout(Device& dev, int order, int n, int b) {
   return slot;
 }
 
-std::shared_ptr<MomentPlan> get_plan(Device& dev, int S, int n, int b) {
+std::shared_ptr<MomentPlan> get_plan(Device& dev, int S, int n, int b, bool dmma) {
   auto top = get_layout(dev, S, n, b);
   std::shared_ptr<DevLayout> low = S > 1 ? get_layout(dev, S - 1, n, b) : nullptr;
   std::lock_guard<std::mutex> lk(dev.mu);
-  auto& slot = dev.plans[{S, n, b}];
+  auto& slot = dev.plans[{S, n, b, dmma ? 1 : 0}];
   if (!slot) {
     auto p = std::make_shared<MomentPlan>();
-    p->build(S, n, b, top->host, low ? &low->host : nullptr, kMomThreads);
+    if (dmma)
+      p->build_dmma(S, n, b, top->host, low ? &low->host : nullptr, dmma_warps(), dmma_rows_per_warp,
+                    dmma_scratch_per_tile());
+    else
+      p->build(S, n, b, top->host, low ? &low->host : nullptr, kMomThreads);
     p->upload();
     slot = p;
   }
@@ -201,6 +206,11 @@ struct Scratch {
   }
 };
 thread_local std::map<int, Scratch> g_scratch;
+// CSB_NO_DMMA=1 forces the DFMA kernel for the top pair (A/B testing)
+const bool g_use_dmma = [] {
+  const char* e = std::getenv("CSB_NO_DMMA");
+  return !(e && e[0] == '1');
+}();
 
 // Orders are processed as pairs (S, S-1): (d, d-1), (d-2, d-3), ... with a
 // lone order 1 when d is odd.  Only the pair topped by d uses the fused
@@ -211,7 +221,7 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
   const int d = m->d;
   for (int S = d; S >= 1; S -= 2) {
     if (only_order && S != only_order) continue;
-    auto plan = get_plan(dev, S, m->n, m->b);
+    const bool top = S == (only_order ? only_order : d);
     MomParams p;
     p.src[0] = src[0];
     p.src[1] = src[1];
@@ -220,17 +230,23 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
     p.n = m->n;
     p.b = m->b;
     p.L = S - 1;
-    p.rows = plan->d_rows.ptr;
-    p.tiles = plan->d_tiles.ptr;
     p.top = m->data[S - 1].ptr;
     p.low = (S > 1 && !only_order) ? m->data[S - 2].ptr : nullptr;
     p.c = c;
     p.inv = 1.0 / static_cast<double>(K);
+    // the top pair runs on the FP64 tensor cores when the rows allow TMA
+    // bulk copies; lower pairs (unfused multiply-add) stay on DFMA/DMUL
+    const bool use_dmma = top && g_use_dmma && dmma_supported(p);
+    auto plan = get_plan(dev, S, m->n, m->b, use_dmma);
+    p.rows = plan->d_rows.ptr;
+    p.tiles = plan->d_tiles.ptr;
     const uint64_t ntiles = plan->tiles.size();
-    if (npass == 2) p.scratch = g_scratch[dev.id].get(ntiles * plan->scratch_per_tile);
-    const bool top = S == (only_order ? only_order : d);
+    if (npass == 2 || use_dmma) p.scratch = g_scratch[dev.id].get(ntiles * plan->scratch_per_tile);
     ProfScope ps(top ? "moment_top" : "moment_low", st);
-    launch_moment_pair(p, static_cast<int>(ntiles), top, st);
+    if (use_dmma)
+      launch_moment_top_dmma(p, static_cast<int>(ntiles), st);
+    else
+      launch_moment_pair(p, static_cast<int>(ntiles), top, st);
   }
 }
 

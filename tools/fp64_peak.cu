@@ -61,6 +61,36 @@ __global__ void dmma_kernel(double* out, int iters, double a, double b) {
   if (s == 12345.678) out[0] = s;
 }
 
+// DMMA and DFMA interleaved: does the FP64 tensor path overlap with the
+// FP64 FMA pipe?  Same DMMA count as dmma_kernel plus `nf` DFMA per DMMA.
+template <int NF>
+__global__ void mixed_kernel(double* out, int iters, double a, double b) {
+  double d[MMA_ACC][2];
+  double f[MMA_ACC][NF > 0 ? NF : 1];
+#pragma unroll
+  for (int c = 0; c < MMA_ACC; ++c) {
+    d[c][0] = d[c][1] = threadIdx.x * 1e-3 + c;
+#pragma unroll
+    for (int q = 0; q < (NF > 0 ? NF : 1); ++q) f[c][q] = c + q;
+  }
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < MMA_ACC; ++c) {
+      dmma(d[c][0], d[c][1], a, b);
+#pragma unroll
+      for (int q = 0; q < NF; ++q) f[c][q] = __fma_rn(f[c][q], a, b);
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int c = 0; c < MMA_ACC; ++c) {
+    s += d[c][0] + d[c][1];
+#pragma unroll
+    for (int q = 0; q < (NF > 0 ? NF : 1); ++q) s += f[c][q];
+  }
+  if (s == 12345.678) out[0] = s;
+}
+
 // One m8n8k4 on given A (8x4 row-major), B (4x8), C (8x8); writes D (8x8).
 __global__ void dmma_once(const double* A, const double* B, const double* Cm, double* D) {
   const int l = threadIdx.x;
@@ -108,6 +138,31 @@ int main() {
   run(dfma_kernel, sms * 8, 256, 20000, 2.0 * CHAINS, "dfma");
   // DMMA: per warp per mma 2*8*8*4 = 512 flops -> 16 per thread
   run(dmma_kernel, sms * 8, 256, 20000, 16.0 * MMA_ACC, "dmma");
+
+  // mixed: report the time ratio against DMMA alone (1.0 = DFMA fully hidden)
+  {
+    auto time_it = [&](auto kern) {
+      kern<<<sms * 8, 256>>>(out, 10, 1.0000001, 1e-9);
+      CK(cudaDeviceSynchronize());
+      float best = 1e30f;
+      for (int rep = 0; rep < 5; ++rep) {
+        CK(cudaEventRecord(e0));
+        kern<<<sms * 8, 256>>>(out, 20000, 1.0000001, 1e-9);
+        CK(cudaEventRecord(e1));
+        CK(cudaEventSynchronize(e1));
+        float ms;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        best = ms < best ? ms : best;
+      }
+      return best;
+    };
+    const float t0 = time_it(mixed_kernel<0>);
+    const float t1 = time_it(mixed_kernel<1>);
+    const float t2 = time_it(mixed_kernel<2>);
+    const float t4 = time_it(mixed_kernel<4>);
+    printf("  \"mixed_dmma_plus_1dfma_ratio\": %.3f,\n  \"mixed_dmma_plus_2dfma_ratio\": %.3f,\n"
+           "  \"mixed_dmma_plus_4dfma_ratio\": %.3f,\n", t1 / t0, t2 / t0, t4 / t0);
+  }
 
   // bitwise check of one DMMA against the sequential FMA chain
   std::mt19937_64 rng(7);
