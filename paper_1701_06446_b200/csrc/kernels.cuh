@@ -22,6 +22,7 @@ struct MomParams {
   int n = 0, b = 0, L = 0;
   const PrefixRow* rows = nullptr;
   const MomTile* tiles = nullptr;
+  const DmmaGroup* groups = nullptr;  // DMMA kernel only
   double* top = nullptr;      // M_S
   double* low = nullptr;      // M_{S-1} (nullptr: not written)
   double* scratch = nullptr;  // pass-0 stash, tiles x 64 x threads
@@ -76,7 +77,6 @@ void count_launch();
 
 // FP64 tensor-core (DMMA) kernel for the top pair of orders (moment_dmma.cu)
 bool dmma_supported(const MomParams& p);
-int dmma_rows_per_warp(int ncol_groups);
 int dmma_warps();
 size_t dmma_scratch_per_tile();
 void launch_moment_top_dmma(const MomParams& p, int ntiles, cudaStream_t st);

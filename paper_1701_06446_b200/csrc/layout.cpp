@@ -1,6 +1,7 @@
 #include "layout.hpp"
 
 #include <algorithm>
+#include <array>
 #include <numeric>
 
 namespace csb {
@@ -126,40 +127,102 @@ std::vector<std::vector<PrefixRow>> MomentPlan::enumerate(int S_, int n_, int b_
   return byJ;
 }
 
+PrefixRow MomentPlan::make_row(const int* t, const Layout& top, const Layout* low) const {
+  PrefixRow r{};
+  int jj[8], full[8];
+  uint32_t vprime = 1, poff = 0;
+  for (int k = 0; k < L; ++k) {
+    r.idx[k] = static_cast<uint16_t>(t[k]);
+    jj[k] = t[k] / b;
+    const int e = top.ext(jj[k]);
+    vprime *= static_cast<uint32_t>(e);
+    poff = poff * static_cast<uint32_t>(e) + static_cast<uint32_t>(t[k] - jj[k] * b);
+  }
+  for (int k = 0; k < L; ++k) full[k] = jj[k];
+  full[L] = jj[L - 1];
+  r.top_base = top.offset[top.rank(full)];
+  r.low_off = low ? low->offset[low->rank(jj)] + poff : 0;
+  r.vprime = vprime;
+  r.poff = poff;
+  return r;
+}
+
 void MomentPlan::build_dmma(int S_, int n_, int b_, const Layout& top, const Layout* low, int warps,
-                            int (*rows_per_warp)(int), uint64_t scratch) {
-  auto byJ = enumerate(S_, n_, b_, top, low);
+                            uint64_t scratch) {
+  S = S_;
+  L = S_ - 1;
+  n = n_;
+  b = b_;
+  rows.clear();
+  tiles.clear();
+  groups.clear();
   dmma = true;
-  for (int J = 0; J < top.grid; ++J) {
-    const auto& R = byJ[J];
-    if (R.empty()) continue;
-    const uint32_t base = static_cast<uint32_t>(rows.size());
-    rows.insert(rows.end(), R.begin(), R.end());
-    const int ncols_all = n - J * b;
-    const int ncg_all = (ncols_all + 7) / 8;
-    const int nranges = (ncg_all + 11) / 12;
+  require(L >= 1 && L <= 7, "build_dmma: order out of range");
+  const int LM1 = L - 1;
+  // all (L-1)-tuples pi in lexicographic order (one empty tuple when L == 1)
+  std::vector<std::array<uint16_t, 6>> pis;
+  {
+    int t[8] = {0};
+    if (LM1 == 0) {
+      pis.push_back({});
+    } else {
+      for (;;) {
+        std::array<uint16_t, 6> a{};
+        for (int k = 0; k < LM1; ++k) a[k] = static_cast<uint16_t>(t[k]);
+        pis.push_back(a);
+        int k = LM1 - 1;
+        while (k >= 0 && t[k] == n - 1) --k;
+        if (k < 0) break;
+        const int v = t[k] + 1;
+        for (int l = k; l < LM1; ++l) t[l] = v;
+      }
+    }
+  }
+  const int nh = (n + 7) / 8;
+  const int per_tile = warps * 8;  // groups per CTA
+  for (int h = 0; h < nh; ++h) {
+    const uint32_t g0 = static_cast<uint32_t>(groups.size());
+    for (const auto& pi : pis) {
+      const int last = LM1 > 0 ? pi[LM1 - 1] : 0;
+      if (last > 8 * h + 7) continue;  // every row of this group has i_L < i_{L-1}
+      DmmaGroup g{};
+      for (int k = 0; k < 6; ++k) g.pidx[k] = pi[k];
+      g.lo = static_cast<uint16_t>(std::max(0, last - 8 * h));
+      g.h = static_cast<uint16_t>(h);
+      groups.push_back(g);
+      int t[8];
+      for (int k = 0; k < LM1; ++k) t[k] = pi[k];
+      for (int r = 0; r < 8; ++r) {
+        const int iL = 8 * h + r;
+        if (r < g.lo || iL >= n) {
+          rows.push_back(PrefixRow{});
+          continue;
+        }
+        t[LM1] = iL;
+        rows.push_back(make_row(t, top, low));
+      }
+    }
+    const uint32_t ng = static_cast<uint32_t>(groups.size()) - g0;
+    if (!ng) continue;
+    const int ncg_all = (n - 8 * h + 7) / 8;
+    const int nranges = (ncg_all + 2) / 3;
     for (int q = 0; q < nranges; ++q) {
-      // balanced column ranges of whole 8-column groups
-      const int g0 = q * ncg_all / nranges, g1 = (q + 1) * ncg_all / nranges;
-      const uint32_t col0 = static_cast<uint32_t>(J * b + 8 * g0);
-      const uint32_t ncols = static_cast<uint32_t>(std::min(8 * g1, ncols_all) - 8 * g0);
-      const int ncg = g1 - g0;
-      const uint64_t cap = static_cast<uint64_t>(warps) * rows_per_warp(ncg);
-      for (uint64_t r0 = 0; r0 < R.size(); r0 += cap) {
+      const int c0 = q * ncg_all / nranges, c1 = (q + 1) * ncg_all / nranges;
+      for (uint32_t s0 = 0; s0 < ng; s0 += per_tile) {
         MomTile t{};
-        t.row0 = base + static_cast<uint32_t>(r0);
-        t.nrows = static_cast<uint32_t>(std::min<uint64_t>(cap, R.size() - r0));
-        t.J = static_cast<uint32_t>(J);
-        t.col0 = col0;
-        t.ncols = ncols;
+        t.row0 = g0 + s0;
+        t.nrows = std::min<uint32_t>(per_tile, ng - s0);
+        t.J = static_cast<uint32_t>(h);
+        t.col0 = static_cast<uint32_t>(8 * h + 8 * c0);
+        t.ncols = static_cast<uint32_t>(std::min(8 * c1, n - 8 * h) - 8 * c0);
         t.low = (q == 0 && low) ? 1u : 0u;
-        t.pad0 = static_cast<uint32_t>(ncg);
+        t.pad0 = static_cast<uint32_t>(c1 - c0);
         tiles.push_back(t);
       }
     }
   }
   std::stable_sort(tiles.begin(), tiles.end(), [](const MomTile& a, const MomTile& c) {
-    return static_cast<uint64_t>(a.nrows) * a.ncols > static_cast<uint64_t>(c.nrows) * c.ncols;
+    return static_cast<uint64_t>(a.nrows) * a.pad0 > static_cast<uint64_t>(c.nrows) * c.pad0;
   });
   scratch_per_tile = scratch;
 }
@@ -203,6 +266,9 @@ void MomentPlan::build(int S_, int n_, int b_, const Layout& top, const Layout* 
 void MomentPlan::upload() {
   d_rows.alloc(rows.size());
   d_tiles.alloc(tiles.size());
+  d_groups.alloc(groups.size());
+  if (!groups.empty())
+    CSB_CUDA(cudaMemcpy(d_groups.ptr, groups.data(), d_groups.bytes(), cudaMemcpyHostToDevice));
   if (!rows.empty())
     CSB_CUDA(cudaMemcpy(d_rows.ptr, rows.data(), d_rows.bytes(), cudaMemcpyHostToDevice));
   if (!tiles.empty())

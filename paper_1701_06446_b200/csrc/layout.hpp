@@ -51,6 +51,16 @@ struct alignas(16) PrefixRow {
 };
 static_assert(sizeof(PrefixRow) == 48, "PrefixRow layout");
 
+// One group of 8 prefix rows (pi, 8h + g), g = 0..7, for the DMMA kernel:
+// pi = (i_1..i_{L-1}); rows with g < lo (i_L < i_{L-1}) or 8h + g >= n are
+// not canonical and are masked.
+struct DmmaGroup {
+  uint16_t pidx[6];
+  uint16_t lo;
+  uint16_t h;
+};
+static_assert(sizeof(DmmaGroup) == 16, "DmmaGroup layout");
+
 struct MomTile {
   uint32_t row0, nrows;  // range in the row table
   uint32_t J;            // block of the last prefix index
@@ -67,15 +77,19 @@ struct MomentPlan {
   DevBuf<MomTile> d_tiles;
   uint64_t scratch_per_tile = 0;  // doubles
   bool dmma = false;  // tiles are for moment_top_dmma_kernel (pad0 = column groups)
+  std::vector<DmmaGroup> groups;
+  DevBuf<DmmaGroup> d_groups;
   void build(int S, int n, int b, const Layout& top, const Layout* low, int threads);
-  // Tiles for the DMMA kernel: rows grouped by J in runs of warps x
-  // rows_per_warp(ncg), column ranges of at most 12 groups of 8.
+  // Tiles for the DMMA kernel: groups (pi, h) of 8 prefix rows, 8 groups per
+  // warp; columns [8h, n) in ranges of at most 3 groups of 8; rows[8 g + r]
+  // is the PrefixRow of row r of group g (zero for masked rows).
   void build_dmma(int S, int n, int b, const Layout& top, const Layout* low, int warps,
-                  int (*rows_per_warp)(int), uint64_t scratch_per_tile);
+                  uint64_t scratch_per_tile);
   void upload();
 
  private:
   std::vector<std::vector<PrefixRow>> enumerate(int S, int n, int b, const Layout& top, const Layout* low);
+  PrefixRow make_row(const int* t, const Layout& top, const Layout* low) const;
 };
 
 }  // namespace csb

@@ -31,8 +31,7 @@ namespace {
 constexpr int WARPS = 8;
 constexpr int THREADS = WARPS * 32;
 constexpr int STAGES = 3;
-constexpr int MAX_MG = 8;
-constexpr int MAX_LOW_ROWS = WARPS * 8 * MAX_MG;
+
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -136,41 +135,98 @@ __device__ __noinline__ void store_copies(double* dst, int S, const int* jv, int
   }
 }
 
-template <int MG, int NC>
-__device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile, double* xs,
-                                         uint64_t* full, double* lowacc, int XS, int KC) {
-  const int n = P.n, b = P.b, L = P.L;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int ncg = static_cast<int>((tile.ncols + 7) / 8);
-  const int nr = static_cast<int>(tile.nrows);
-  const int wrow0 = warp * 8 * MG;  // first tile row of this warp
-  const bool do_low = (P.low != nullptr) && tile.low;
-
-  // prefix indices of my MG rows (row = wrow0 + 8g + lane/4), two uint16
-  // per register
-  uint32_t pidx[MG][4];
-  bool rvalid[MG];
+// Per-warp layout: lane = 4 r + q.  The warp owns 8 groups; group r is
+// (pi_r, h): the 8 prefix rows (pi_r, 8h + g), g = 0..7.  For MMA fragment
+// g, row m = r of A is the Khatri-Rao value of row (pi_r, 8h + g) at data
+// row k = q, so each thread forms P = x[pi_r] once per k and the 8 row values
+// as P * x[8h + g] (prefix sharing of moments.cpp:55,71).  B fragment c is
+// x[k = q][col0 + 8c + r].  Accumulator (g, c, e) is the element
+// (pi_r, 8h + g, col0 + 8c + 2q + e).
+template <int LM1, int NC, bool PARTIAL>
+__device__ __forceinline__ void k4_step(const double* __restrict__ xst, int XS, int kk, int kc, int q, int r,
+                                        int h8, int col0, const int* pidx, int lo, bool gvalid, double* lowbuf,
+                                        bool do_low, double (&lowacc)[2], double (&acc)[8][NC][2]) {
+  const int k = kk + q;
+  const bool kv = !PARTIAL || k < kc;
+  const double* xr = xst + k * XS;
+  double a[8];
+  {
+    double P = 1.0;
+    if (LM1 > 0) {
+      P = xr[pidx[0]];
 #pragma unroll
-  for (int g = 0; g < MG; ++g) {
-    const int r = wrow0 + 8 * g + (lane >> 2);
-    rvalid[g] = r < nr;
-    const PrefixRow& pr = P.rows[tile.row0 + (rvalid[g] ? r : 0)];
-    const uint32_t* w = reinterpret_cast<const uint32_t*>(pr.idx);
+      for (int t = 1; t < LM1; ++t) P = __dmul_rn(P, xr[pidx[t]]);
+    }
+    const double2* xa = reinterpret_cast<const double2*>(xr + h8);
 #pragma unroll
-    for (int h = 0; h < 4; ++h) pidx[g][h] = w[h];
+    for (int s = 0; s < 4; ++s) {
+      const double2 v = xa[s];
+      a[2 * s] = v.x;
+      a[2 * s + 1] = v.y;
+    }
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      if (LM1 > 0) a[g] = __dmul_rn(P, a[g]);  // 1.0 * x == x: no multiply for L == 1
+      if (!(kv && gvalid && g >= lo)) a[g] = 0.0;
+    }
   }
-  auto IDX = [&](int g, int q) -> int { return static_cast<int>((pidx[g][q >> 1] >> (16 * (q & 1))) & 0xffffu); };
-  double acc[MG][NC][2];
+  if (do_low) {
+    // transpose the 8 x 4 block (rows g, k) through shared memory so lane q
+    // owns rows 2q, 2q+1 and adds their four k values in row order
+    double2* wb = reinterpret_cast<double2*>(lowbuf + q * 66 + r * 8);
 #pragma unroll
-  for (int g = 0; g < MG; ++g)
+    for (int s = 0; s < 4; ++s) wb[s] = make_double2(a[2 * s], a[2 * s + 1]);
+    __syncwarp();
+#pragma unroll
+    for (int kp = 0; kp < 4; ++kp) {
+      const double2 v = *reinterpret_cast<const double2*>(lowbuf + kp * 66 + r * 8 + 2 * q);
+      if (!PARTIAL || kk + kp < kc) {
+        lowacc[0] = __dadd_rn(lowacc[0], v.x);
+        lowacc[1] = __dadd_rn(lowacc[1], v.y);
+      }
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    double bv = xr[col0 + 8 * c + r];
+    if (PARTIAL && !kv) bv = 0.0;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) dmma(acc[g][c][0], acc[g][c][1], a[g], bv);
+  }
+}
+
+template <int LM1, int NC>
+__device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile, double* xs,
+                                         uint64_t* full, double* lowbufs, int XS, int KC) {
+  constexpr int L = LM1 + 1;
+  const int n = P.n, b = P.b;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int q = lane & 3, r = lane >> 2;
+  const int h8 = static_cast<int>(tile.J) * 8;
+  const int col0 = static_cast<int>(tile.col0);
+  const bool do_low = (P.low != nullptr) && tile.low;
+  double* lowbuf = lowbufs + warp * (4 * 66);
+
+  const int gl = warp * 8 + r;  // group slot in the tile
+  const bool gvalid = gl < static_cast<int>(tile.nrows);
+  const uint32_t gi = tile.row0 + (gvalid ? gl : 0);
+  const DmmaGroup grp = P.groups[gi];
+  int pidx[LM1 > 0 ? LM1 : 1];
+#pragma unroll
+  for (int t = 0; t < LM1; ++t) pidx[t] = grp.pidx[t];
+  const int lo = grp.lo;
+
+  double acc[8][NC][2];
+#pragma unroll
+  for (int g = 0; g < 8; ++g)
 #pragma unroll
     for (int c = 0; c < NC; ++c) acc[g][c][0] = acc[g][c][1] = 0.0;
+  double lowacc[2] = {0.0, 0.0}, lowin[2] = {0.0, 0.0};
 
   const uint32_t nch = (P.K + KC - 1) / KC;  // chunks per pass
   const uint32_t total = nch * P.npass;
   const uint32_t rowbytes = static_cast<uint32_t>(n) * 8u;
-  const int kq = lane & 3;       // k offset of my A / B fragment
-  const int cl = lane >> 2;      // my B column within a group
   const size_t stage_elems = static_cast<size_t>(KC) * XS;
 
   auto issue = [&](uint32_t i) {
@@ -180,7 +236,8 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
     uint64_t* bar = full + (i % STAGES);
     double* dst = xs + (i % STAGES) * stage_elems;
     mbar_expect_tx(bar, kc * rowbytes);
-    for (uint32_t r = 0; r < kc; ++r) bulk_g2s(dst + r * XS, row_ptr(P.src[pass], k0 + r, n), rowbytes, bar);
+    for (uint32_t rr = 0; rr < kc; ++rr)
+      bulk_g2s(dst + rr * XS, row_ptr(P.src[pass], k0 + rr, n), rowbytes, bar);
   };
   if (threadIdx.x == 0)
     for (uint32_t i = 0; i < min(static_cast<uint32_t>(STAGES - 1), total); ++i) issue(i);
@@ -188,54 +245,15 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
   for (uint32_t i = 0; i < total; ++i) {
     if (threadIdx.x == 0 && i + STAGES - 1 < total) issue(i + STAGES - 1);
     mbar_wait(full + (i % STAGES), (i / STAGES) & 1u);
-    const int pass = static_cast<int>(i / nch);
     const uint32_t k0 = (i % nch) * KC;
     const int kc = static_cast<int>(min(static_cast<uint32_t>(KC), P.K - k0));
     const double* xst = xs + (i % STAGES) * stage_elems;
-
-    for (int kk = 0; kk < KC; kk += 4) {
-      if (kk >= kc) break;
-      const int k = kk + kq;
-      const bool kv = k < kc;
-      const double* xr = xst + k * XS;
-      double a[MG];
-#pragma unroll
-      for (int g = 0; g < MG; ++g) {
-        double v = 0.0;
-        if (kv && rvalid[g]) {
-          v = xr[IDX(g, 0)];
-#pragma unroll
-          for (int q = 1; q < kMaxOrder - 1; ++q)
-            if (q < L) v = __dmul_rn(v, xr[IDX(g, q)]);
-        }
-        a[g] = v;
-      }
-      if (do_low) {
-        // row sums of A in row order: lane kq==0 adds its own value then the
-        // three following k (moments.cpp:44, plain adds)
-#pragma unroll
-        for (int g = 0; g < MG; ++g) {
-          const double a1 = __shfl_down_sync(0xffffffffu, a[g], 1);
-          const double a2 = __shfl_down_sync(0xffffffffu, a[g], 2);
-          const double a3 = __shfl_down_sync(0xffffffffu, a[g], 3);
-          if (kq == 0 && rvalid[g]) {
-            double* s = lowacc + (pass * MAX_LOW_ROWS + wrow0 + 8 * g + cl);
-            double t = __dadd_rn(*s, a[g]);
-            if (kk + 1 < kc) t = __dadd_rn(t, a1);
-            if (kk + 2 < kc) t = __dadd_rn(t, a2);
-            if (kk + 3 < kc) t = __dadd_rn(t, a3);
-            *s = t;
-          }
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        if (c < ncg) {
-          const double bv = kv ? xr[tile.col0 + 8 * c + cl] : 0.0;
-#pragma unroll
-          for (int g = 0; g < MG; ++g) dmma(acc[g][c][0], acc[g][c][1], a[g], bv);
-        }
-      }
+    if (kc == KC) {
+      for (int kk = 0; kk < KC; kk += 4)
+        k4_step<LM1, NC, false>(xst, XS, kk, kc, q, r, h8, col0, pidx, lo, gvalid, lowbuf, do_low, lowacc, acc);
+    } else {
+      for (int kk = 0; kk < kc; kk += 4)
+        k4_step<LM1, NC, true>(xst, XS, kk, kc, q, r, h8, col0, pidx, lo, gvalid, lowbuf, do_low, lowacc, acc);
     }
     __syncthreads();  // stage (i % STAGES) is free for chunk i + STAGES
 
@@ -243,7 +261,7 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
       // end of the incoming pass: stash its means, restart the accumulators
       double* st = P.scratch + static_cast<size_t>(blockIdx.x) * (THREADS * 48);
 #pragma unroll
-      for (int g = 0; g < MG; ++g)
+      for (int g = 0; g < 8; ++g)
 #pragma unroll
         for (int c = 0; c < NC; ++c)
 #pragma unroll
@@ -251,58 +269,73 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
             st[static_cast<size_t>((g * NC + c) * 2 + e) * THREADS + threadIdx.x] = __dmul_rn(acc[g][c][e], P.inv);
             acc[g][c][e] = 0.0;
           }
+      lowin[0] = __dmul_rn(lowacc[0], P.inv);
+      lowin[1] = __dmul_rn(lowacc[1], P.inv);
+      lowacc[0] = lowacc[1] = 0.0;
     }
   }
 
-  // ---- epilogue: order d ----
+  // ---- epilogue ----
+  if (!gvalid) return;
   const double* st = P.scratch + static_cast<size_t>(blockIdx.x) * (THREADS * 48);
   const bool update = P.npass == 2;
 #pragma unroll
-  for (int g = 0; g < MG; ++g) {
-    if (!rvalid[g]) continue;
-    const int r = wrow0 + 8 * g + cl;
-    const PrefixRow& pr = P.rows[tile.row0 + r];
-    const int lastp = IDX(g, L - 1);
+  for (int g = 0; g < 8; ++g) {
+    const int iL = h8 + g;
+    if (g < lo || iL >= n) continue;
+    const PrefixRow& pr = P.rows[static_cast<size_t>(gi) * 8 + g];
+    int jv[kMaxOrder], ov[kMaxOrder], ev[kMaxOrder];
+    bool runs = false;
 #pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      if (c >= ncg) continue;
+    for (int t = 0; t <= LM1; ++t) {
+      const int iq = t < LM1 ? pidx[t] : iL;
+      jv[t] = iq / b;
+      ov[t] = iq - jv[t] * b;
+      ev[t] = ext_of(jv[t], n, b);
+      if (t > 0) runs |= jv[t] == jv[t - 1];
+    }
+    const int J = jv[LM1];
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int col = static_cast<int>(tile.col0) + 8 * c + 2 * kq + e;
-        if (col >= n || col < lastp) continue;
+        const int col = col0 + 8 * c + 2 * q + e;
+        if (col >= n || col < iL) continue;
         const double v = __dmul_rn(acc[g][c][e], P.inv);
-        const double delta = update ? __dsub_rn(st[static_cast<size_t>((g * NC + c) * 2 + e) * THREADS + threadIdx.x], v) : 0.0;
-        int jv[kMaxOrder], ov[kMaxOrder], ev[kMaxOrder];
-        for (int q = 0; q < L; ++q) {
-          const int iq = IDX(g, q);
-          jv[q] = iq / b;
-          ov[q] = iq - jv[q] * b;
-          ev[q] = ext_of(jv[q], n, b);
-        }
+        const double delta =
+            update ? __dsub_rn(st[static_cast<size_t>((g * NC + c) * 2 + e) * THREADS + threadIdx.x], v) : 0.0;
         const int jd = col / b;
-        jv[L] = jd;
-        ov[L] = col - jd * b;
-        ev[L] = ext_of(jd, n, b);
-        const uint64_t blk = pr.top_base + static_cast<uint64_t>(pr.vprime) * b * (jd - static_cast<int>(tile.J));
-        store_copies(P.top, L + 1, jv, ov, ev, blk, update, P.c, delta, v);
-      }
-    }
-  }
-  // ---- epilogue: order d-1 ----
-  if (do_low && kq == 0) {
+        const uint64_t blk = pr.top_base + static_cast<uint64_t>(pr.vprime) * b * (jd - J);
+        if (!runs && jd != J) {
+          // off-diagonal block: the canonical entry is the only stored copy
+          double* p = P.top + blk + static_cast<uint64_t>(pr.poff) * ext_of(jd, n, b) + (col - jd * b);
+          *p = update ? __fma_rn(P.c, delta, *p) : v;
+        } else {
+          jv[L] = jd;
+          ov[L] = col - jd * b;
+          ev[L] = ext_of(jd, n, b);
+          int o2[kMaxOrder];
 #pragma unroll
-    for (int g = 0; g < MG; ++g) {
-      if (!rvalid[g]) continue;
-      const int r = wrow0 + 8 * g + cl;
-      const PrefixRow& pr = P.rows[tile.row0 + r];
-      const double v = __dmul_rn(lowacc[(P.npass - 1) * MAX_LOW_ROWS + r], P.inv);
-      const double delta = update ? __dsub_rn(__dmul_rn(lowacc[r], P.inv), v) : 0.0;
+          for (int t = 0; t <= L; ++t) o2[t] = ov[t];
+          store_copies(P.top, L + 1, jv, o2, ev, blk, update, P.c, delta, v);
+        }
+      }
+  }
+  if (do_low) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int g = 2 * q + e;
+      const int iL = h8 + g;
+      if (g < lo || iL >= n) continue;
+      const PrefixRow& pr = P.rows[static_cast<size_t>(gi) * 8 + g];
+      const double v = __dmul_rn(lowacc[e], P.inv);
+      const double delta = update ? __dsub_rn(lowin[e], v) : 0.0;
       int jv[kMaxOrder], ov[kMaxOrder], ev[kMaxOrder];
-      for (int q = 0; q < L; ++q) {
-        const int iq = IDX(g, q);
-        jv[q] = iq / b;
-        ov[q] = iq - jv[q] * b;
-        ev[q] = ext_of(jv[q], n, b);
+      for (int t = 0; t <= LM1; ++t) {
+        const int iq = t < LM1 ? pidx[t] : iL;
+        jv[t] = iq / b;
+        ov[t] = iq - jv[t] * b;
+        ev[t] = ext_of(jv[t], n, b);
       }
       store_copies(P.low, L, jv, ov, ev, pr.low_off - pr.poff, update, P.c, delta, v);
     }
@@ -313,48 +346,42 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t full[STAGES];
   double* xs = smem;
-  double* lowacc = xs + static_cast<size_t>(STAGES) * KC * XS;  // 2 x MAX_LOW_ROWS
+  double* lowbufs = xs + static_cast<size_t>(STAGES) * KC * XS;  // WARPS x 4 x 66
   const MomTile tile = P.tiles[blockIdx.x];
   // zero the padding columns [n, XS) of the staging ring; bulk copies only
   // ever write [0, n), so the two proxies never touch the same bytes
   const int padw = XS - P.n;
   for (int e = threadIdx.x; e < STAGES * KC * padw; e += THREADS)
     xs[(e / padw) * XS + P.n + (e % padw)] = 0.0;
-  for (int e = threadIdx.x; e < 2 * MAX_LOW_ROWS; e += THREADS) lowacc[e] = 0.0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(full + s, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  switch (tile.pad0) {
-    case 1: run_tile<8, 1>(P, tile, xs, full, lowacc, XS, KC); break;
-    case 2: run_tile<8, 2>(P, tile, xs, full, lowacc, XS, KC); break;
-    case 3: run_tile<8, 3>(P, tile, xs, full, lowacc, XS, KC); break;
-    case 4: run_tile<6, 4>(P, tile, xs, full, lowacc, XS, KC); break;
-    case 5: run_tile<4, 5>(P, tile, xs, full, lowacc, XS, KC); break;
-    case 6: run_tile<4, 6>(P, tile, xs, full, lowacc, XS, KC); break;
-    case 7: run_tile<3, 7>(P, tile, xs, full, lowacc, XS, KC); break;
-    case 8: run_tile<3, 8>(P, tile, xs, full, lowacc, XS, KC); break;
-    case 9: run_tile<2, 9>(P, tile, xs, full, lowacc, XS, KC); break;
-    case 10: run_tile<2, 10>(P, tile, xs, full, lowacc, XS, KC); break;
-    case 11: run_tile<2, 11>(P, tile, xs, full, lowacc, XS, KC); break;
-    default: run_tile<2, 12>(P, tile, xs, full, lowacc, XS, KC); break;
+  const int nc = static_cast<int>(tile.pad0);
+  switch (P.L * 4 + nc) {
+#define CSB_CASE(LL, NCC) \
+  case (LL) * 4 + (NCC): run_tile<(LL) - 1, NCC>(P, tile, xs, full, lowbufs, XS, KC); break;
+    CSB_CASE(1, 1) CSB_CASE(1, 2) CSB_CASE(1, 3)
+    CSB_CASE(2, 1) CSB_CASE(2, 2) CSB_CASE(2, 3)
+    CSB_CASE(3, 1) CSB_CASE(3, 2) CSB_CASE(3, 3)
+    CSB_CASE(4, 1) CSB_CASE(4, 2) CSB_CASE(4, 3)
+    CSB_CASE(5, 1) CSB_CASE(5, 2) CSB_CASE(5, 3)
+    CSB_CASE(6, 1) CSB_CASE(6, 2) CSB_CASE(6, 3)
+    CSB_CASE(7, 1) CSB_CASE(7, 2) CSB_CASE(7, 3)
+#undef CSB_CASE
+    default: break;
   }
 }
 
 }  // namespace
-
-int dmma_rows_per_warp(int nc) {
-  const int mg = nc <= 3 ? 8 : nc == 4 ? 6 : nc <= 6 ? 4 : nc <= 8 ? 3 : 2;
-  return 8 * mg;
-}
 
 int dmma_warps() { return WARPS; }
 
 size_t dmma_scratch_per_tile() { return static_cast<size_t>(THREADS) * 48; }
 
 bool dmma_supported(const MomParams& p) {
-  if (p.n % 2 != 0 || p.L < 1 || p.L > kMaxOrder - 1) return false;
+  if (p.n % 2 != 0 || p.L < 1 || p.L > 7) return false;
   for (int s = 0; s < p.npass; ++s) {
     if (reinterpret_cast<uintptr_t>(p.src[s].seg0) % 16) return false;
     if (p.src[s].len1 && reinterpret_cast<uintptr_t>(p.src[s].seg1) % 16) return false;
@@ -364,11 +391,13 @@ bool dmma_supported(const MomParams& p) {
 
 void launch_moment_top_dmma(const MomParams& p, int ntiles, cudaStream_t st) {
   if (ntiles <= 0) return;
+  // row stride: >= n + 8 (zero padding for the last 8-column window) and
+  // = 4 (mod 16) doubles so the B-fragment loads are bank-conflict free
   int XS = p.n + 8;
-  while (XS % 16 != 8) ++XS;
+  while (XS % 16 != 4) ++XS;
   int KC = 32;
   while (KC > 8 && static_cast<size_t>(STAGES) * KC * XS * 8 > 160 * 1024) KC /= 2;
-  const size_t smem = sizeof(double) * (static_cast<size_t>(STAGES) * KC * XS + 2 * MAX_LOW_ROWS);
+  const size_t smem = sizeof(double) * (static_cast<size_t>(STAGES) * KC * XS + WARPS * 4 * 66);
   CSB_CUDA(cudaFuncSetAttribute(moment_top_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
   moment_top_dmma_kernel<<<ntiles, THREADS, smem, st>>>(p, XS, KC);

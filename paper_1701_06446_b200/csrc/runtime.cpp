@@ -107,8 +107,7 @@ std::shared_ptr<MomentPlan> get_plan(Device& dev, int S, int n, int b, bool dmma
   if (!slot) {
     auto p = std::make_shared<MomentPlan>();
     if (dmma)
-      p->build_dmma(S, n, b, top->host, low ? &low->host : nullptr, dmma_warps(), dmma_rows_per_warp,
-                    dmma_scratch_per_tile());
+      p->build_dmma(S, n, b, top->host, low ? &low->host : nullptr, dmma_warps(), dmma_scratch_per_tile());
     else
       p->build(S, n, b, top->host, low ? &low->host : nullptr, kMomThreads);
     p->upload();
@@ -240,6 +239,7 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
     auto plan = get_plan(dev, S, m->n, m->b, use_dmma);
     p.rows = plan->d_rows.ptr;
     p.tiles = plan->d_tiles.ptr;
+    p.groups = plan->d_groups.ptr;
     const uint64_t ntiles = plan->tiles.size();
     if (npass == 2 || use_dmma) p.scratch = g_scratch[dev.id].get(ntiles * plan->scratch_per_tile);
     ProfScope ps(top ? "moment_top" : "moment_low", st);
