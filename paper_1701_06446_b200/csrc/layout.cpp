@@ -205,7 +205,7 @@ void MomentPlan::build_dmma(int S_, int n_, int b_, const Layout& top, const Lay
     const uint32_t ng = static_cast<uint32_t>(groups.size()) - g0;
     if (!ng) continue;
     const int ncg_all = (n - 8 * h + 7) / 8;
-    const int nranges = (ncg_all + 2) / 3;
+    const int nranges = (ncg_all + 3) / 4;
     for (int q = 0; q < nranges; ++q) {
       const int c0 = q * ncg_all / nranges, c1 = (q + 1) * ncg_all / nranges;
       for (uint32_t s0 = 0; s0 < ng; s0 += per_tile) {

@@ -81,7 +81,7 @@ struct MomentPlan {
   DevBuf<DmmaGroup> d_groups;
   void build(int S, int n, int b, const Layout& top, const Layout* low, int threads);
   // Tiles for the DMMA kernel: groups (pi, h) of 8 prefix rows, 8 groups per
-  // warp; columns [8h, n) in ranges of at most 3 groups of 8; rows[8 g + r]
+  // warp; columns [8h, n) in ranges of at most 4 groups of 8; rows[8 g + r]
   // is the PrefixRow of row r of group g (zero for masked rows).
   void build_dmma(int S, int n, int b, const Layout& top, const Layout* low, int warps,
                   uint64_t scratch_per_tile);

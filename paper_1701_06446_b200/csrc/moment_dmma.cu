@@ -28,9 +28,9 @@ namespace csb {
 
 namespace {
 
-constexpr int WARPS = 8;
+constexpr int WARPS = 8;  // MMA warps; lane 0 of warp 0 also drives the TMA
 constexpr int THREADS = WARPS * 32;
-constexpr int STAGES = 3;
+constexpr int STAGES = 4;
 
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -135,6 +135,24 @@ __device__ __noinline__ void store_copies(double* dst, int S, const int* jv, int
   }
 }
 
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 // Per-warp layout: lane = 4 r + q.  The warp owns 8 groups; group r is
 // (pi_r, h): the 8 prefix rows (pi_r, 8h + g), g = 0..7.  For MMA fragment
 // g, row m = r of A is the Khatri-Rao value of row (pi_r, 8h + g) at data
@@ -142,63 +160,52 @@ __device__ __noinline__ void store_copies(double* dst, int S, const int* jv, int
 // as P * x[8h + g] (prefix sharing of moments.cpp:55,71).  B fragment c is
 // x[k = q][col0 + 8c + r].  Accumulator (g, c, e) is the element
 // (pi_r, 8h + g, col0 + 8c + 2q + e).
-template <int LM1, int NC, bool PARTIAL>
-__device__ __forceinline__ void k4_step(const double* __restrict__ xst, int XS, int kk, int kc, int q, int r,
-                                        int h8, int col0, const int* pidx, int lo, bool gvalid, double* lowbuf,
-                                        bool do_low, double (&lowacc)[2], double (&acc)[8][NC][2]) {
-  const int k = kk + q;
-  const bool kv = !PARTIAL || k < kc;
-  const double* xr = xst + k * XS;
-  double a[8];
-  {
-    double P = 1.0;
-    if (LM1 > 0) {
-      P = xr[pidx[0]];
+//
+// The k loop runs over "steps" of 4 data rows, flat across both passes and
+// all staged chunks, software-pipelined in registers: step s+1's operands
+// are loaded from shared memory and multiplied out while step s's DMMAs
+// occupy the FP64 tensor pipe.
+template <int LM1, int NC>
+struct Operands {
+  double a[8];   // A fragments (8 rows) of one step
+  double b[NC];  // B fragments
+};
+
+template <int LM1, int NC>
+__device__ __forceinline__ void load_ops(Operands<LM1, NC>& op, const double* __restrict__ xr, int h8, int col0,
+                                         int r, const int* pidx, bool zero) {
+  double P = 1.0;
+  if (LM1 > 0) {
+    P = xr[pidx[0]];
 #pragma unroll
-      for (int t = 1; t < LM1; ++t) P = __dmul_rn(P, xr[pidx[t]]);
-    }
-    const double2* xa = reinterpret_cast<const double2*>(xr + h8);
-#pragma unroll
-    for (int s = 0; s < 4; ++s) {
-      const double2 v = xa[s];
-      a[2 * s] = v.x;
-      a[2 * s + 1] = v.y;
-    }
-#pragma unroll
-    for (int g = 0; g < 8; ++g) {
-      if (LM1 > 0) a[g] = __dmul_rn(P, a[g]);  // 1.0 * x == x: no multiply for L == 1
-      if (!(kv && gvalid && g >= lo)) a[g] = 0.0;
-    }
+    for (int t = 1; t < LM1; ++t) P = __dmul_rn(P, xr[pidx[t]]);
   }
-  if (do_low) {
-    // transpose the 8 x 4 block (rows g, k) through shared memory so lane q
-    // owns rows 2q, 2q+1 and adds their four k values in row order
-    double2* wb = reinterpret_cast<double2*>(lowbuf + q * 66 + r * 8);
+  const double2* xa = reinterpret_cast<const double2*>(xr + h8);
 #pragma unroll
-    for (int s = 0; s < 4; ++s) wb[s] = make_double2(a[2 * s], a[2 * s + 1]);
-    __syncwarp();
-#pragma unroll
-    for (int kp = 0; kp < 4; ++kp) {
-      const double2 v = *reinterpret_cast<const double2*>(lowbuf + kp * 66 + r * 8 + 2 * q);
-      if (!PARTIAL || kk + kp < kc) {
-        lowacc[0] = __dadd_rn(lowacc[0], v.x);
-        lowacc[1] = __dadd_rn(lowacc[1], v.y);
-      }
-    }
-    __syncwarp();
+  for (int s = 0; s < 4; ++s) {
+    const double2 v = xa[s];
+    op.a[2 * s] = v.x;
+    op.a[2 * s + 1] = v.y;
   }
 #pragma unroll
-  for (int c = 0; c < NC; ++c) {
-    double bv = xr[col0 + 8 * c + r];
-    if (PARTIAL && !kv) bv = 0.0;
+  for (int c = 0; c < NC; ++c) op.b[c] = xr[col0 + 8 * c + r];
+  // Rows with g < lo (i_L < i_{L-1}) and padding groups are computed but
+  // never stored, so no masking is needed; only data rows past the end of
+  // a pass must contribute exact zeros.
 #pragma unroll
-    for (int g = 0; g < 8; ++g) dmma(acc[g][c][0], acc[g][c][1], a[g], bv);
+  for (int g = 0; g < 8; ++g) {
+    if (LM1 > 0) op.a[g] = __dmul_rn(P, op.a[g]);  // 1.0 * x == x: no multiply for L == 1
+    if (zero) op.a[g] = 0.0;
+  }
+  if (zero) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) op.b[c] = 0.0;
   }
 }
 
 template <int LM1, int NC>
 __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile, double* xs,
-                                         uint64_t* full, double* lowbufs, int XS, int KC) {
+                                         uint64_t* full, uint64_t* empty, double* lowbufs, int XS, int KC) {
   constexpr int L = LM1 + 1;
   const int n = P.n, b = P.b;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -207,6 +214,44 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
   const int col0 = static_cast<int>(tile.col0);
   const bool do_low = (P.low != nullptr) && tile.low;
   double* lowbuf = lowbufs + warp * (4 * 66);
+  const size_t stage_elems = static_cast<size_t>(KC) * XS;
+  const uint32_t K = P.K;
+  const uint32_t nch = (K + KC - 1) / KC;       // chunks per pass
+  const uint32_t spp = (K + 3) / 4;              // steps per pass
+  const uint32_t total = spp * P.npass;
+  const uint32_t spc = static_cast<uint32_t>(KC) / 4;  // steps per full chunk
+
+  // ---- TMA producer: lane 0 of warp 0 streams the rows in ----
+  // Chunk c goes into stage c % STAGES once every warp has released chunk
+  // c - STAGES (empty barrier).  The producer polls without blocking and
+  // blocks only for the chunk warp 0 itself needs next, so warp 0 never
+  // waits at a CTA-wide barrier.
+  const uint32_t chunks = nch * P.npass;
+  uint32_t next_issue = 0;
+  auto pump = [&](uint32_t needed) {
+    if (threadIdx.x != 0) return;
+    const uint32_t rowbytes = static_cast<uint32_t>(n) * 8u;
+    while (next_issue < chunks) {
+      const uint32_t i = next_issue;
+      const uint32_t st = i % STAGES;
+      if (i >= STAGES) {
+        const uint32_t par = ((i / STAGES) - 1) & 1u;
+        if (!mbar_test(empty + st, par)) {
+          if (i > needed) break;
+          mbar_wait(empty + st, par);
+        }
+      }
+      const int pass = static_cast<int>(i / nch);
+      const uint32_t k0 = (i % nch) * KC;
+      const uint32_t kc = min(static_cast<uint32_t>(KC), K - k0);
+      double* dst = xs + st * stage_elems;
+      mbar_expect_tx(full + st, kc * rowbytes);
+      for (uint32_t rr = 0; rr < kc; ++rr)
+        bulk_g2s(dst + rr * XS, row_ptr(P.src[pass], k0 + rr, n), rowbytes, full + st);
+      ++next_issue;
+    }
+  };
+  pump(0);
 
   const int gl = warp * 8 + r;  // group slot in the tile
   const bool gvalid = gl < static_cast<int>(tile.nrows);
@@ -224,60 +269,101 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
     for (int c = 0; c < NC; ++c) acc[g][c][0] = acc[g][c][1] = 0.0;
   double lowacc[2] = {0.0, 0.0}, lowin[2] = {0.0, 0.0};
 
-  const uint32_t nch = (P.K + KC - 1) / KC;  // chunks per pass
-  const uint32_t total = nch * P.npass;
-  const uint32_t rowbytes = static_cast<uint32_t>(n) * 8u;
-  const size_t stage_elems = static_cast<size_t>(KC) * XS;
-
-  auto issue = [&](uint32_t i) {
-    const int pass = static_cast<int>(i / nch);
-    const uint32_t k0 = (i % nch) * KC;
-    const uint32_t kc = min(static_cast<uint32_t>(KC), P.K - k0);
-    uint64_t* bar = full + (i % STAGES);
-    double* dst = xs + (i % STAGES) * stage_elems;
-    mbar_expect_tx(bar, kc * rowbytes);
-    for (uint32_t rr = 0; rr < kc; ++rr)
-      bulk_g2s(dst + rr * XS, row_ptr(P.src[pass], k0 + rr, n), rowbytes, bar);
+  // step s -> (pass, chunk, stage, row in stage)
+  auto step_row = [&](uint32_t s, bool& first_of_chunk, bool& last_of_chunk, bool& zero,
+                      uint32_t& chunk) -> const double* {
+    const uint32_t pass = s / spp, t = s % spp;
+    const uint32_t k0 = 4 * t;
+    chunk = pass * nch + k0 / KC;
+    const uint32_t in_chunk = (k0 % KC) / 4;
+    first_of_chunk = in_chunk == 0;
+    last_of_chunk = in_chunk + 1 == spc || t + 1 == spp;
+    zero = (k0 + q) >= K;
+    return xs + (chunk % STAGES) * stage_elems + static_cast<size_t>(k0 % KC + q) * XS;
   };
-  if (threadIdx.x == 0)
-    for (uint32_t i = 0; i < min(static_cast<uint32_t>(STAGES - 1), total); ++i) issue(i);
 
-  for (uint32_t i = 0; i < total; ++i) {
-    if (threadIdx.x == 0 && i + STAGES - 1 < total) issue(i + STAGES - 1);
-    mbar_wait(full + (i % STAGES), (i / STAGES) & 1u);
-    const uint32_t k0 = (i % nch) * KC;
-    const int kc = static_cast<int>(min(static_cast<uint32_t>(KC), P.K - k0));
-    const double* xst = xs + (i % STAGES) * stage_elems;
-    if (kc == KC) {
-      for (int kk = 0; kk < KC; kk += 4)
-        k4_step<LM1, NC, false>(xst, XS, kk, kc, q, r, h8, col0, pidx, lo, gvalid, lowbuf, do_low, lowacc, acc);
-    } else {
-      for (int kk = 0; kk < kc; kk += 4)
-        k4_step<LM1, NC, true>(xst, XS, kk, kc, q, r, h8, col0, pidx, lo, gvalid, lowbuf, do_low, lowacc, acc);
+  Operands<LM1, NC> cur, nxt;
+  bool cur_last, cur_first, zero;
+  uint32_t cur_chunk;
+  {
+    const double* xr = step_row(0, cur_first, cur_last, zero, cur_chunk);
+    mbar_wait(full + (cur_chunk % STAGES), (cur_chunk / STAGES) & 1u);
+    load_ops<LM1, NC>(cur, xr, h8, col0, r, pidx, zero);
+  }
+
+  for (uint32_t s = 0; s < total; ++s) {
+    // prefetch + multiply out step s+1 (overlaps the DMMAs below)
+    bool nfirst = false, nlast = false, nzero = false;
+    uint32_t nchunk = 0;
+    const bool has_next = s + 1 < total;
+    if (has_next) {
+      const double* xr = step_row(s + 1, nfirst, nlast, nzero, nchunk);
+      if (nfirst) {
+        if (warp == 0) pump(nchunk);
+        __syncwarp();
+        mbar_wait(full + (nchunk % STAGES), (nchunk / STAGES) & 1u);
+      }
+      load_ops<LM1, NC>(nxt, xr, h8, col0, r, pidx, nzero);
     }
-    __syncthreads();  // stage (i % STAGES) is free for chunk i + STAGES
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+      for (int g = 0; g < 8; ++g) dmma(acc[g][c][0], acc[g][c][1], cur.a[g], cur.b[c]);
 
-    if (P.npass == 2 && (i + 1) == nch) {
+    if (do_low) {
+      // order S-1 sums: transpose the 8 x 4 block (rows g, k) through shared
+      // memory so lane q owns rows 2q, 2q+1 and adds their four k values in
+      // row order (moments.cpp:44, plain adds)
+      const uint32_t t = s % spp;
+      double2* wb = reinterpret_cast<double2*>(lowbuf + q * 66 + r * 8);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) wb[u] = make_double2(cur.a[2 * u], cur.a[2 * u + 1]);
+      __syncwarp();
+#pragma unroll
+      for (int kp = 0; kp < 4; ++kp) {
+        const double2 v = *reinterpret_cast<const double2*>(lowbuf + kp * 66 + r * 8 + 2 * q);
+        if (4 * t + kp < K) {
+          lowacc[0] = __dadd_rn(lowacc[0], v.x);
+          lowacc[1] = __dadd_rn(lowacc[1], v.y);
+        }
+      }
+      __syncwarp();
+    }
+
+    if (cur_last) {
+      // every lane has consumed its rows of this stage
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + (cur_chunk % STAGES));
+      if (warp == 0) pump(0);  // refill without blocking
+    }
+
+    if (P.npass == 2 && s + 1 == spp) {
       // end of the incoming pass: stash its means, restart the accumulators
-      double* st = P.scratch + static_cast<size_t>(blockIdx.x) * (THREADS * 48);
+      double* stash = P.scratch + static_cast<size_t>(blockIdx.x) * (WARPS * 32 * 64);
+      const int tid = threadIdx.x;
 #pragma unroll
       for (int g = 0; g < 8; ++g)
 #pragma unroll
         for (int c = 0; c < NC; ++c)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            st[static_cast<size_t>((g * NC + c) * 2 + e) * THREADS + threadIdx.x] = __dmul_rn(acc[g][c][e], P.inv);
+            stash[static_cast<size_t>((g * NC + c) * 2 + e) * (WARPS * 32) + tid] = __dmul_rn(acc[g][c][e], P.inv);
             acc[g][c][e] = 0.0;
           }
       lowin[0] = __dmul_rn(lowacc[0], P.inv);
       lowin[1] = __dmul_rn(lowacc[1], P.inv);
       lowacc[0] = lowacc[1] = 0.0;
     }
+    if (has_next) {
+      cur = nxt;
+      cur_last = nlast;
+      cur_chunk = nchunk;
+    }
   }
 
   // ---- epilogue ----
   if (!gvalid) return;
-  const double* st = P.scratch + static_cast<size_t>(blockIdx.x) * (THREADS * 48);
+  const double* stash = P.scratch + static_cast<size_t>(blockIdx.x) * (WARPS * 32 * 64);
   const bool update = P.npass == 2;
 #pragma unroll
   for (int g = 0; g < 8; ++g) {
@@ -303,7 +389,8 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
         if (col >= n || col < iL) continue;
         const double v = __dmul_rn(acc[g][c][e], P.inv);
         const double delta =
-            update ? __dsub_rn(st[static_cast<size_t>((g * NC + c) * 2 + e) * THREADS + threadIdx.x], v) : 0.0;
+            update ? __dsub_rn(stash[static_cast<size_t>((g * NC + c) * 2 + e) * (WARPS * 32) + threadIdx.x], v)
+                   : 0.0;
         const int jd = col / b;
         const uint64_t blk = pr.top_base + static_cast<uint64_t>(pr.vprime) * b * (jd - J);
         if (!runs && jd != J) {
@@ -345,6 +432,7 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
 __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomParams P, int XS, int KC) {
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t full[STAGES];
+  __shared__ __align__(8) uint64_t empty[STAGES];
   double* xs = smem;
   double* lowbufs = xs + static_cast<size_t>(STAGES) * KC * XS;  // WARPS x 4 x 66
   const MomTile tile = P.tiles[blockIdx.x];
@@ -354,21 +442,20 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
   for (int e = threadIdx.x; e < STAGES * KC * padw; e += THREADS)
     xs[(e / padw) * XS + P.n + (e % padw)] = 0.0;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) mbar_init(full + s, 1);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, WARPS);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   const int nc = static_cast<int>(tile.pad0);
-  switch (P.L * 4 + nc) {
+  switch (P.L * 8 + nc) {
 #define CSB_CASE(LL, NCC) \
-  case (LL) * 4 + (NCC): run_tile<(LL) - 1, NCC>(P, tile, xs, full, lowbufs, XS, KC); break;
-    CSB_CASE(1, 1) CSB_CASE(1, 2) CSB_CASE(1, 3)
-    CSB_CASE(2, 1) CSB_CASE(2, 2) CSB_CASE(2, 3)
-    CSB_CASE(3, 1) CSB_CASE(3, 2) CSB_CASE(3, 3)
-    CSB_CASE(4, 1) CSB_CASE(4, 2) CSB_CASE(4, 3)
-    CSB_CASE(5, 1) CSB_CASE(5, 2) CSB_CASE(5, 3)
-    CSB_CASE(6, 1) CSB_CASE(6, 2) CSB_CASE(6, 3)
-    CSB_CASE(7, 1) CSB_CASE(7, 2) CSB_CASE(7, 3)
+  case (LL) * 8 + (NCC): run_tile<(LL) - 1, NCC>(P, tile, xs, full, empty, lowbufs, XS, KC); break;
+#define CSB_CASES(LL) CSB_CASE(LL, 1) CSB_CASE(LL, 2) CSB_CASE(LL, 3) CSB_CASE(LL, 4)
+    CSB_CASES(1) CSB_CASES(2) CSB_CASES(3) CSB_CASES(4) CSB_CASES(5) CSB_CASES(6) CSB_CASES(7)
+#undef CSB_CASES
 #undef CSB_CASE
     default: break;
   }
@@ -378,7 +465,7 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
 
 int dmma_warps() { return WARPS; }
 
-size_t dmma_scratch_per_tile() { return static_cast<size_t>(THREADS) * 48; }
+size_t dmma_scratch_per_tile() { return static_cast<size_t>(WARPS) * 32 * 64; }
 
 bool dmma_supported(const MomParams& p) {
   if (p.n % 2 != 0 || p.L < 1 || p.L > 7) return false;
@@ -396,7 +483,7 @@ void launch_moment_top_dmma(const MomParams& p, int ntiles, cudaStream_t st) {
   int XS = p.n + 8;
   while (XS % 16 != 4) ++XS;
   int KC = 32;
-  while (KC > 8 && static_cast<size_t>(STAGES) * KC * XS * 8 > 160 * 1024) KC /= 2;
+  while (KC > 8 && static_cast<size_t>(STAGES) * KC * XS * 8 > 190 * 1024) KC /= 2;
   const size_t smem = sizeof(double) * (static_cast<size_t>(STAGES) * KC * XS + WARPS * 4 * 66);
   CSB_CUDA(cudaFuncSetAttribute(moment_top_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));

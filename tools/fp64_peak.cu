@@ -139,6 +139,14 @@ int main() {
   // DMMA: per warp per mma 2*8*8*4 = 512 flops -> 16 per thread
   run(dmma_kernel, sms * 8, 256, 20000, 16.0 * MMA_ACC, "dmma");
 
+  // DMMA issue rate vs warps per SMSP: 148*m CTAs of 128 threads (m warps
+  // per SMSP when spread evenly), 8 independent accumulators per warp
+  for (int m : {1, 2, 3, 4, 8}) {
+    char name[64];
+    snprintf(name, sizeof name, "dmma_%dwarp_per_smsp", m);
+    run(dmma_kernel, sms * m, 128, 20000, 16.0 * MMA_ACC, name);
+  }
+
   // mixed: report the time ratio against DMMA alone (1.0 = DFMA fully hidden)
   {
     auto time_it = [&](auto kern) {
