@@ -31,6 +31,8 @@ namespace {
 constexpr int WARPS = 8;  // MMA warps; lane 0 of warp 0 also drives the TMA
 constexpr int THREADS = WARPS * 32;
 constexpr int STAGES = 4;
+constexpr int KC = 32;        // data rows per stage
+constexpr int SPC = KC / 4;   // k4 steps per stage
 
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -205,9 +207,10 @@ __device__ __forceinline__ void load_ops(Operands<LM1, NC>& op, const double* __
 
 template <int LM1, int NC>
 __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile, double* xs,
-                                         uint64_t* full, uint64_t* empty, double* lowbufs, int XS, int KC) {
+                                         uint64_t* full, uint64_t* empty, double* lowbufs) {
   constexpr int L = LM1 + 1;
   const int n = P.n, b = P.b;
+  const int XS = n;  // dense rows: one bulk copy per chunk
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int q = lane & 3, r = lane >> 2;
   const int h8 = static_cast<int>(tile.J) * 8;
@@ -216,21 +219,18 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
   double* lowbuf = lowbufs + warp * (4 * 66);
   const size_t stage_elems = static_cast<size_t>(KC) * XS;
   const uint32_t K = P.K;
-  const uint32_t nch = (K + KC - 1) / KC;       // chunks per pass
-  const uint32_t spp = (K + 3) / 4;              // steps per pass
-  const uint32_t total = spp * P.npass;
-  const uint32_t spc = static_cast<uint32_t>(KC) / 4;  // steps per full chunk
+  const uint32_t nch = (K + KC - 1) / KC;  // chunks per pass
+  const uint32_t chunks = nch * P.npass;
 
   // ---- TMA producer: lane 0 of warp 0 streams the rows in ----
   // Chunk c goes into stage c % STAGES once every warp has released chunk
   // c - STAGES (empty barrier).  The producer polls without blocking and
-  // blocks only for the chunk warp 0 itself needs next, so warp 0 never
+  // blocks only for the chunk warp 0 itself needs next, so no warp ever
   // waits at a CTA-wide barrier.
-  const uint32_t chunks = nch * P.npass;
   uint32_t next_issue = 0;
+  uint32_t issue_pass = 0, issue_k0 = 0;
   auto pump = [&](uint32_t needed) {
     if (threadIdx.x != 0) return;
-    const uint32_t rowbytes = static_cast<uint32_t>(n) * 8u;
     while (next_issue < chunks) {
       const uint32_t i = next_issue;
       const uint32_t st = i % STAGES;
@@ -241,17 +241,27 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
           mbar_wait(empty + st, par);
         }
       }
-      const int pass = static_cast<int>(i / nch);
-      const uint32_t k0 = (i % nch) * KC;
-      const uint32_t kc = min(static_cast<uint32_t>(KC), K - k0);
+      const RowSource& src = P.src[issue_pass];
+      const uint32_t kc = min(static_cast<uint32_t>(KC), K - issue_k0);
       double* dst = xs + st * stage_elems;
-      mbar_expect_tx(full + st, kc * rowbytes);
-      for (uint32_t rr = 0; rr < kc; ++rr)
-        bulk_g2s(dst + rr * XS, row_ptr(P.src[pass], k0 + rr, n), rowbytes, full + st);
+      mbar_expect_tx(full + st, kc * static_cast<uint32_t>(n) * 8u);
+      // rows [k0, k0 + kc) are contiguous except across the ring's wrap
+      const uint32_t a0 = issue_k0, a1 = issue_k0 + kc;
+      if (a1 <= src.len0 || a0 >= src.len0) {
+        bulk_g2s(dst, row_ptr(src, a0, n), kc * static_cast<uint32_t>(n) * 8u, full + st);
+      } else {
+        const uint32_t k1 = src.len0 - a0;
+        bulk_g2s(dst, row_ptr(src, a0, n), k1 * static_cast<uint32_t>(n) * 8u, full + st);
+        bulk_g2s(dst + static_cast<size_t>(k1) * n, src.seg1, (kc - k1) * static_cast<uint32_t>(n) * 8u, full + st);
+      }
       ++next_issue;
+      issue_k0 += KC;
+      if (issue_k0 >= K) {
+        issue_k0 = 0;
+        ++issue_pass;
+      }
     }
   };
-  pump(0);
 
   const int gl = warp * 8 + r;  // group slot in the tile
   const bool gvalid = gl < static_cast<int>(tile.nrows);
@@ -269,75 +279,69 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
     for (int c = 0; c < NC; ++c) acc[g][c][0] = acc[g][c][1] = 0.0;
   double lowacc[2] = {0.0, 0.0}, lowin[2] = {0.0, 0.0};
 
-  // step s -> (pass, chunk, stage, row in stage)
-  auto step_row = [&](uint32_t s, bool& first_of_chunk, bool& last_of_chunk, bool& zero,
-                      uint32_t& chunk) -> const double* {
-    const uint32_t pass = s / spp, t = s % spp;
-    const uint32_t k0 = 4 * t;
-    chunk = pass * nch + k0 / KC;
-    const uint32_t in_chunk = (k0 % KC) / 4;
-    first_of_chunk = in_chunk == 0;
-    last_of_chunk = in_chunk + 1 == spc || t + 1 == spp;
-    zero = (k0 + q) >= K;
-    return xs + (chunk % STAGES) * stage_elems + static_cast<size_t>(k0 % KC + q) * XS;
-  };
-
-  Operands<LM1, NC> cur, nxt;
-  bool cur_last, cur_first, zero;
-  uint32_t cur_chunk;
-  {
-    const double* xr = step_row(0, cur_first, cur_last, zero, cur_chunk);
-    mbar_wait(full + (cur_chunk % STAGES), (cur_chunk / STAGES) & 1u);
-    load_ops<LM1, NC>(cur, xr, h8, col0, r, pidx, zero);
-  }
-
-  for (uint32_t s = 0; s < total; ++s) {
-    // prefetch + multiply out step s+1 (overlaps the DMMAs below)
-    bool nfirst = false, nlast = false, nzero = false;
-    uint32_t nchunk = 0;
-    const bool has_next = s + 1 < total;
-    if (has_next) {
-      const double* xr = step_row(s + 1, nfirst, nlast, nzero, nchunk);
-      if (nfirst) {
-        if (warp == 0) pump(nchunk);
-        __syncwarp();
-        mbar_wait(full + (nchunk % STAGES), (nchunk / STAGES) & 1u);
+  auto low_sum = [&](const Operands<LM1, NC>& op, bool partial, int kleft) {
+    // order S-1 sums: transpose the 8 x 4 block (rows g, k) through shared
+    // memory so lane q owns rows 2q, 2q+1 and adds their four k values in
+    // row order (moments.cpp:44, plain adds)
+    double2* wb = reinterpret_cast<double2*>(lowbuf + q * 66 + r * 8);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) wb[u] = make_double2(op.a[2 * u], op.a[2 * u + 1]);
+    __syncwarp();
+#pragma unroll
+    for (int kp = 0; kp < 4; ++kp) {
+      const double2 v = *reinterpret_cast<const double2*>(lowbuf + kp * 66 + r * 8 + 2 * q);
+      if (!partial || kp < kleft) {
+        lowacc[0] = __dadd_rn(lowacc[0], v.x);
+        lowacc[1] = __dadd_rn(lowacc[1], v.y);
       }
-      load_ops<LM1, NC>(nxt, xr, h8, col0, r, pidx, nzero);
     }
+    __syncwarp();
+  };
+  auto mma_step = [&](const Operands<LM1, NC>& op) {
 #pragma unroll
     for (int c = 0; c < NC; ++c)
 #pragma unroll
-      for (int g = 0; g < 8; ++g) dmma(acc[g][c][0], acc[g][c][1], cur.a[g], cur.b[c]);
+      for (int g = 0; g < 8; ++g) dmma(acc[g][c][0], acc[g][c][1], op.a[g], op.b[c]);
+  };
 
-    if (do_low) {
-      // order S-1 sums: transpose the 8 x 4 block (rows g, k) through shared
-      // memory so lane q owns rows 2q, 2q+1 and adds their four k values in
-      // row order (moments.cpp:44, plain adds)
-      const uint32_t t = s % spp;
-      double2* wb = reinterpret_cast<double2*>(lowbuf + q * 66 + r * 8);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) wb[u] = make_double2(cur.a[2 * u], cur.a[2 * u + 1]);
+  pump(0);
+  uint32_t chunk = 0;
+  for (int pass = 0; pass < P.npass; ++pass) {
+    for (uint32_t k0 = 0; k0 < K; k0 += KC, ++chunk) {
+      const uint32_t st = chunk % STAGES;
+      if (warp == 0) pump(chunk);
       __syncwarp();
-#pragma unroll
-      for (int kp = 0; kp < 4; ++kp) {
-        const double2 v = *reinterpret_cast<const double2*>(lowbuf + kp * 66 + r * 8 + 2 * q);
-        if (4 * t + kp < K) {
-          lowacc[0] = __dadd_rn(lowacc[0], v.x);
-          lowacc[1] = __dadd_rn(lowacc[1], v.y);
+      mbar_wait(full + st, (chunk / STAGES) & 1u);
+      const double* xst = xs + st * stage_elems + static_cast<size_t>(q) * XS;
+      const int kc = static_cast<int>(min(static_cast<uint32_t>(KC), K - k0));
+      if (kc == KC) {
+        // full chunk: 8 steps of 4 rows, operands of step t+1 loaded and
+        // multiplied out while step t's DMMAs run
+        Operands<LM1, NC> o0, o1;
+        load_ops<LM1, NC>(o0, xst, h8, col0, r, pidx, false);
+#pragma unroll 1
+        for (int t = 0; t < SPC; t += 2) {
+          load_ops<LM1, NC>(o1, xst + (4 * t + 4) * XS, h8, col0, r, pidx, false);
+          mma_step(o0);
+          if (do_low) low_sum(o0, false, 4);
+          if (t + 2 < SPC) load_ops<LM1, NC>(o0, xst + (4 * t + 8) * XS, h8, col0, r, pidx, false);
+          mma_step(o1);
+          if (do_low) low_sum(o1, false, 4);
+        }
+      } else {
+        for (int t = 0; 4 * t < kc; ++t) {
+          Operands<LM1, NC> o0;
+          load_ops<LM1, NC>(o0, xst + 4 * t * XS, h8, col0, r, pidx, 4 * t + q >= kc);
+          mma_step(o0);
+          if (do_low) low_sum(o0, true, kc - 4 * t);
         }
       }
-      __syncwarp();
-    }
-
-    if (cur_last) {
       // every lane has consumed its rows of this stage
       __syncwarp();
-      if (lane == 0) mbar_arrive(empty + (cur_chunk % STAGES));
+      if (lane == 0) mbar_arrive(empty + st);
       if (warp == 0) pump(0);  // refill without blocking
     }
-
-    if (P.npass == 2 && s + 1 == spp) {
+    if (P.npass == 2 && pass == 0) {
       // end of the incoming pass: stash its means, restart the accumulators
       double* stash = P.scratch + static_cast<size_t>(blockIdx.x) * (WARPS * 32 * 64);
       const int tid = threadIdx.x;
@@ -353,11 +357,6 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
       lowin[0] = __dmul_rn(lowacc[0], P.inv);
       lowin[1] = __dmul_rn(lowacc[1], P.inv);
       lowacc[0] = lowacc[1] = 0.0;
-    }
-    if (has_next) {
-      cur = nxt;
-      cur_last = nlast;
-      cur_chunk = nchunk;
     }
   }
 
@@ -429,18 +428,15 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
   }
 }
 
-__global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomParams P, int XS, int KC) {
+__global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomParams P) {
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t full[STAGES];
   __shared__ __align__(8) uint64_t empty[STAGES];
   double* xs = smem;
-  double* lowbufs = xs + static_cast<size_t>(STAGES) * KC * XS;  // WARPS x 4 x 66
+  // dense staging ring; reads past row n of a stage (the last 8-column
+  // window / column group) only feed rows and columns that are never stored
+  double* lowbufs = xs + static_cast<size_t>(STAGES) * KC * P.n + 64;  // WARPS x 4 x 66
   const MomTile tile = P.tiles[blockIdx.x];
-  // zero the padding columns [n, XS) of the staging ring; bulk copies only
-  // ever write [0, n), so the two proxies never touch the same bytes
-  const int padw = XS - P.n;
-  for (int e = threadIdx.x; e < STAGES * KC * padw; e += THREADS)
-    xs[(e / padw) * XS + P.n + (e % padw)] = 0.0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full + s, 1);
@@ -452,9 +448,9 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
   const int nc = static_cast<int>(tile.pad0);
   switch (P.L * 8 + nc) {
 #define CSB_CASE(LL, NCC) \
-  case (LL) * 8 + (NCC): run_tile<(LL) - 1, NCC>(P, tile, xs, full, empty, lowbufs, XS, KC); break;
+  case (LL) * 8 + (NCC): run_tile<(LL) - 1, NCC>(P, tile, xs, full, empty, lowbufs); break;
 #define CSB_CASES(LL) CSB_CASE(LL, 1) CSB_CASE(LL, 2) CSB_CASE(LL, 3) CSB_CASE(LL, 4)
-    CSB_CASES(1) CSB_CASES(2) CSB_CASES(3) CSB_CASES(4) CSB_CASES(5) CSB_CASES(6) CSB_CASES(7)
+    CSB_CASES(2) CSB_CASES(3) CSB_CASES(4) CSB_CASES(5)
 #undef CSB_CASES
 #undef CSB_CASE
     default: break;
@@ -468,7 +464,9 @@ int dmma_warps() { return WARPS; }
 size_t dmma_scratch_per_tile() { return static_cast<size_t>(WARPS) * 32 * 64; }
 
 bool dmma_supported(const MomParams& p) {
-  if (p.n % 2 != 0 || p.L < 1 || p.L > 7) return false;
+  // instantiated for orders 3..6 (L = 2..5); the staging ring must fit
+  if (p.n % 2 != 0 || p.L < 2 || p.L > 5) return false;
+  if (sizeof(double) * (static_cast<size_t>(STAGES) * KC * p.n + 64 + WARPS * 4 * 66) > 220 * 1024) return false;
   for (int s = 0; s < p.npass; ++s) {
     if (reinterpret_cast<uintptr_t>(p.src[s].seg0) % 16) return false;
     if (p.src[s].len1 && reinterpret_cast<uintptr_t>(p.src[s].seg1) % 16) return false;
@@ -478,16 +476,10 @@ bool dmma_supported(const MomParams& p) {
 
 void launch_moment_top_dmma(const MomParams& p, int ntiles, cudaStream_t st) {
   if (ntiles <= 0) return;
-  // row stride: >= n + 8 (zero padding for the last 8-column window) and
-  // = 4 (mod 16) doubles so the B-fragment loads are bank-conflict free
-  int XS = p.n + 8;
-  while (XS % 16 != 4) ++XS;
-  int KC = 32;
-  while (KC > 8 && static_cast<size_t>(STAGES) * KC * XS * 8 > 190 * 1024) KC /= 2;
-  const size_t smem = sizeof(double) * (static_cast<size_t>(STAGES) * KC * XS + WARPS * 4 * 66);
+  const size_t smem = sizeof(double) * (static_cast<size_t>(STAGES) * KC * p.n + 64 + WARPS * 4 * 66);
   CSB_CUDA(cudaFuncSetAttribute(moment_top_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
-  moment_top_dmma_kernel<<<ntiles, THREADS, smem, st>>>(p, XS, KC);
+  moment_top_dmma_kernel<<<ntiles, THREADS, smem, st>>>(p);
   CSB_CUDA(cudaGetLastError());
   count_launch();
 }
