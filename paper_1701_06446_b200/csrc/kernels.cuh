@@ -25,7 +25,8 @@ struct MomParams {
   const DmmaGroup* groups = nullptr;  // DMMA kernel only
   double* top = nullptr;      // M_S
   double* low = nullptr;      // M_{S-1} (nullptr: not written)
-  double* scratch = nullptr;  // pass-0 stash, tiles x 64 x threads
+  double* scratch = nullptr;  // pass-0 stash (DMMA: per tile pair, both passes)
+  uint32_t* flags = nullptr;  // DMMA: per tile pair arrival counters (self-resetting)
   double c = 0.0;             // p / T        (moments.cpp:287)
   double inv = 1.0;           // 1.0 / rows   (moments.cpp:148)
 };

@@ -224,6 +224,7 @@ void MomentPlan::build_dmma(int S_, int n_, int b_, const Layout& top, const Lay
   std::stable_sort(tiles.begin(), tiles.end(), [](const MomTile& a, const MomTile& c) {
     return static_cast<uint64_t>(a.nrows) * a.pad0 > static_cast<uint64_t>(c.nrows) * c.pad0;
   });
+  for (size_t i = 0; i < tiles.size(); ++i) tiles[i].pad1 = static_cast<uint32_t>(i);  // pair slot
   scratch_per_tile = scratch;
 }
 

@@ -10,14 +10,20 @@
 // chaining the MMAs over k in row order therefore reproduces the
 // reference's row-ordered fma(A, x, acc) (moments.cpp:47) bit for bit.
 //
-// Data flow per CTA (8 warps): rows of the window stream through a 3-stage
-// shared-memory ring filled by cp.async.bulk (TMA bulk copies, one per row,
-// completion on an mbarrier); every warp owns MG x 8 prefix rows and NC x 8
-// columns of the tile, computes its Khatri-Rao operand fragments in
-// registers straight from the staged rows, and keeps its accumulators in
-// registers across both passes (incoming rows, then outgoing rows).  The
-// M_{d-1} sums are formed from the same fragments (warp shuffles put the
-// four k values of a row in order) and kept in shared memory.
+// Work unit: a tile = 32 groups (pi, h) of 8 prefix rows (pi, 8h + g) x up
+// to 4 column groups of 8, for ONE pass (incoming or outgoing rows).  The
+// two passes of a tile pair run as independent CTAs; whichever finishes
+// second reads its partner's means from scratch and performs the fused
+// update M = fma(p/T, a - b, M) (moments.cpp:297) -- the result does not
+// depend on the order they finish.
+//
+// Per CTA (4 warps): rows of the batch stream through a 4-stage shared
+// memory ring filled by cp.async.bulk (one TMA bulk copy per 32-row chunk,
+// mbarrier completion; lane 0 of warp 0 is the producer and refills a stage
+// once all warps released it -- no CTA-wide barrier in the loop).  Each warp
+// builds its Khatri-Rao fragments in registers straight from the staged
+// rows, software-pipelined so the next step's loads and products overlap
+// the current step's DMMAs.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -28,11 +34,10 @@ namespace csb {
 
 namespace {
 
-constexpr int WARPS = 8;  // MMA warps; lane 0 of warp 0 also drives the TMA
+constexpr int WARPS = 4;  // MMA warps; lane 0 of warp 0 also drives the TMA
 constexpr int THREADS = WARPS * 32;
 constexpr int STAGES = 4;
 constexpr int KC = 32;        // data rows per stage
-constexpr int SPC = KC / 4;   // k4 steps per stage
 
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -167,68 +172,72 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // all staged chunks, software-pipelined in registers: step s+1's operands
 // are loaded from shared memory and multiplied out while step s's DMMAs
 // occupy the FP64 tensor pipe.
+
 template <int LM1, int NC>
-struct Operands {
-  double a[8];   // A fragments (8 rows) of one step
-  double b[NC];  // B fragments
+struct Raw {
+  double p[LM1 > 0 ? LM1 : 1];  // x[pi_t] of this lane's group
+  double a[8];                  // x[8h + g]
+  double b[NC];                 // x[col0 + 8c + r]
 };
 
 template <int LM1, int NC>
-__device__ __forceinline__ void load_ops(Operands<LM1, NC>& op, const double* __restrict__ xr, int h8, int col0,
-                                         int r, const int* pidx, bool zero) {
-  double P = 1.0;
-  if (LM1 > 0) {
-    P = xr[pidx[0]];
+__device__ __forceinline__ void load_raw(Raw<LM1, NC>& w, const double* __restrict__ xr, int h8, int col0,
+                                         int r, const int* pidx) {
 #pragma unroll
-    for (int t = 1; t < LM1; ++t) P = __dmul_rn(P, xr[pidx[t]]);
-  }
+  for (int t = 0; t < LM1; ++t) w.p[t] = xr[pidx[t]];
   const double2* xa = reinterpret_cast<const double2*>(xr + h8);
 #pragma unroll
   for (int s = 0; s < 4; ++s) {
     const double2 v = xa[s];
-    op.a[2 * s] = v.x;
-    op.a[2 * s + 1] = v.y;
+    w.a[2 * s] = v.x;
+    w.a[2 * s + 1] = v.y;
   }
 #pragma unroll
-  for (int c = 0; c < NC; ++c) op.b[c] = xr[col0 + 8 * c + r];
-  // Rows with g < lo (i_L < i_{L-1}) and padding groups are computed but
-  // never stored, so no masking is needed; only data rows past the end of
-  // a pass must contribute exact zeros.
+  for (int c = 0; c < NC; ++c) w.b[c] = xr[col0 + 8 * c + r];
+}
+
+// A = x[pi_1] * ... * x[pi_{L-1}] * x[8h + g] in the reference's order.
+// Rows with g < lo (i_L < i_{L-1}) and padding groups are computed but never
+// stored, so no masking is needed; data rows past the end of the pass are
+// zeroed (zero == true) so they contribute exact zeros.
+template <int LM1, int NC>
+__device__ __forceinline__ void finish(Raw<LM1, NC>& w, bool zero) {
+  if (LM1 > 0) {
+    double P = w.p[0];
 #pragma unroll
-  for (int g = 0; g < 8; ++g) {
-    if (LM1 > 0) op.a[g] = __dmul_rn(P, op.a[g]);  // 1.0 * x == x: no multiply for L == 1
-    if (zero) op.a[g] = 0.0;
+    for (int t = 1; t < LM1; ++t) P = __dmul_rn(P, w.p[t]);
+#pragma unroll
+    for (int g = 0; g < 8; ++g) w.a[g] = __dmul_rn(P, w.a[g]);  // 1.0 * x == x: none for L == 1
   }
   if (zero) {
 #pragma unroll
-    for (int c = 0; c < NC; ++c) op.b[c] = 0.0;
+    for (int g = 0; g < 8; ++g) w.a[g] = 0.0;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) w.b[c] = 0.0;
   }
 }
 
 template <int LM1, int NC>
-__device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile, double* xs,
-                                         uint64_t* full, uint64_t* empty, double* lowbufs) {
+__device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile, int pass, double* xs,
+                                         uint64_t* full, uint64_t* empty, double* lowbufs, uint32_t* flag_smem) {
   constexpr int L = LM1 + 1;
   const int n = P.n, b = P.b;
-  const int XS = n;  // dense rows: one bulk copy per chunk
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int q = lane & 3, r = lane >> 2;
   const int h8 = static_cast<int>(tile.J) * 8;
   const int col0 = static_cast<int>(tile.col0);
   const bool do_low = (P.low != nullptr) && tile.low;
-  double* lowbuf = lowbufs + warp * (4 * 66);
-  const size_t stage_elems = static_cast<size_t>(KC) * XS;
+  double* lowbuf = lowbufs + warp * (2 * 4 * 66);  // double-buffered 4 x 66
+  const size_t stage_elems = static_cast<size_t>(KC) * n;
   const uint32_t K = P.K;
-  const uint32_t nch = (K + KC - 1) / KC;  // chunks per pass
-  const uint32_t chunks = nch * P.npass;
+  const uint32_t chunks = (K + KC - 1) / KC;
+  const RowSource& src = P.src[pass];
 
-  // ---- TMA producer: lane 0 of warp 0 streams the rows in ----
+  // ---- TMA producer: lane 0 of warp 0 ----
   // Chunk c goes into stage c % STAGES once every warp has released chunk
-  // c - STAGES (empty barrier).  The producer polls without blocking and
-  // blocks only for the chunk warp 0 itself needs next, so no warp ever
-  // waits at a CTA-wide barrier.
+  // c - STAGES.  The producer polls without blocking and blocks only for the
+  // chunk warp 0 itself needs next.
   uint32_t next_issue = 0;
-  uint32_t issue_pass = 0, issue_k0 = 0;
   auto pump = [&](uint32_t needed) {
     if (threadIdx.x != 0) return;
     while (next_issue < chunks) {
@@ -241,25 +250,20 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
           mbar_wait(empty + st, par);
         }
       }
-      const RowSource& src = P.src[issue_pass];
-      const uint32_t kc = min(static_cast<uint32_t>(KC), K - issue_k0);
+      const uint32_t a0 = i * KC;
+      const uint32_t kc = min(static_cast<uint32_t>(KC), K - a0);
       double* dst = xs + st * stage_elems;
-      mbar_expect_tx(full + st, kc * static_cast<uint32_t>(n) * 8u);
-      // rows [k0, k0 + kc) are contiguous except across the ring's wrap
-      const uint32_t a0 = issue_k0, a1 = issue_k0 + kc;
-      if (a1 <= src.len0 || a0 >= src.len0) {
-        bulk_g2s(dst, row_ptr(src, a0, n), kc * static_cast<uint32_t>(n) * 8u, full + st);
+      const uint32_t rb = static_cast<uint32_t>(n) * 8u;
+      mbar_expect_tx(full + st, kc * rb);
+      // rows [a0, a0 + kc) are contiguous except across the ring's wrap
+      if (a0 + kc <= src.len0 || a0 >= src.len0) {
+        bulk_g2s(dst, row_ptr(src, a0, n), kc * rb, full + st);
       } else {
         const uint32_t k1 = src.len0 - a0;
-        bulk_g2s(dst, row_ptr(src, a0, n), k1 * static_cast<uint32_t>(n) * 8u, full + st);
-        bulk_g2s(dst + static_cast<size_t>(k1) * n, src.seg1, (kc - k1) * static_cast<uint32_t>(n) * 8u, full + st);
+        bulk_g2s(dst, row_ptr(src, a0, n), k1 * rb, full + st);
+        bulk_g2s(dst + static_cast<size_t>(k1) * n, src.seg1, (kc - k1) * rb, full + st);
       }
       ++next_issue;
-      issue_k0 += KC;
-      if (issue_k0 >= K) {
-        issue_k0 = 0;
-        ++issue_pass;
-      }
     }
   };
 
@@ -277,93 +281,117 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
   for (int g = 0; g < 8; ++g)
 #pragma unroll
     for (int c = 0; c < NC; ++c) acc[g][c][0] = acc[g][c][1] = 0.0;
-  double lowacc[2] = {0.0, 0.0}, lowin[2] = {0.0, 0.0};
+  double lowacc[2] = {0.0, 0.0};
 
-  auto low_sum = [&](const Operands<LM1, NC>& op, bool partial, int kleft) {
-    // order S-1 sums: transpose the 8 x 4 block (rows g, k) through shared
-    // memory so lane q owns rows 2q, 2q+1 and adds their four k values in
-    // row order (moments.cpp:44, plain adds)
-    double2* wb = reinterpret_cast<double2*>(lowbuf + q * 66 + r * 8);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) wb[u] = make_double2(op.a[2 * u], op.a[2 * u + 1]);
-    __syncwarp();
-#pragma unroll
-    for (int kp = 0; kp < 4; ++kp) {
-      const double2 v = *reinterpret_cast<const double2*>(lowbuf + kp * 66 + r * 8 + 2 * q);
-      if (!partial || kp < kleft) {
-        lowacc[0] = __dadd_rn(lowacc[0], v.x);
-        lowacc[1] = __dadd_rn(lowacc[1], v.y);
-      }
-    }
-    __syncwarp();
-  };
-  auto mma_step = [&](const Operands<LM1, NC>& op) {
+  auto mma_step = [&](const Raw<LM1, NC>& op) {
 #pragma unroll
     for (int c = 0; c < NC; ++c)
 #pragma unroll
       for (int g = 0; g < 8; ++g) dmma(acc[g][c][0], acc[g][c][1], op.a[g], op.b[c]);
   };
+  // order L sums: the 8 x 4 block (rows g, k) of a step is transposed
+  // through shared memory so lane q owns rows 2q, 2q+1 and adds their four
+  // k values in row order (moments.cpp:44, plain adds).  Written at step t,
+  // read (after the next __syncwarp) at step t + 1.
+  auto low_put = [&](const Raw<LM1, NC>& op, int buf) {
+    double2* wb = reinterpret_cast<double2*>(lowbuf + buf * 264 + q * 66 + r * 8);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) wb[u] = make_double2(op.a[2 * u], op.a[2 * u + 1]);
+  };
+  auto low_get = [&](double2 (&v)[4], int buf) {
+#pragma unroll
+    for (int kp = 0; kp < 4; ++kp) v[kp] = *reinterpret_cast<const double2*>(lowbuf + buf * 264 + kp * 66 + r * 8 + 2 * q);
+  };
+  auto low_add = [&](const double2 (&v)[4], int kleft) {
+#pragma unroll
+    for (int kp = 0; kp < 4; ++kp)
+      if (kp < kleft) {
+        lowacc[0] = __dadd_rn(lowacc[0], v[kp].x);
+        lowacc[1] = __dadd_rn(lowacc[1], v[kp].y);
+      }
+  };
 
   pump(0);
-  uint32_t chunk = 0;
-  for (int pass = 0; pass < P.npass; ++pass) {
-    for (uint32_t k0 = 0; k0 < K; k0 += KC, ++chunk) {
-      const uint32_t st = chunk % STAGES;
-      if (warp == 0) pump(chunk);
-      __syncwarp();
-      mbar_wait(full + st, (chunk / STAGES) & 1u);
-      const double* xst = xs + st * stage_elems + static_cast<size_t>(q) * XS;
-      const int kc = static_cast<int>(min(static_cast<uint32_t>(KC), K - k0));
-      if (kc == KC) {
-        // full chunk: 8 steps of 4 rows, operands of step t+1 loaded and
-        // multiplied out while step t's DMMAs run
-        Operands<LM1, NC> o0, o1;
-        load_ops<LM1, NC>(o0, xst, h8, col0, r, pidx, false);
-#pragma unroll 1
-        for (int t = 0; t < SPC; t += 2) {
-          load_ops<LM1, NC>(o1, xst + (4 * t + 4) * XS, h8, col0, r, pidx, false);
-          mma_step(o0);
-          if (do_low) low_sum(o0, false, 4);
-          if (t + 2 < SPC) load_ops<LM1, NC>(o0, xst + (4 * t + 8) * XS, h8, col0, r, pidx, false);
-          mma_step(o1);
-          if (do_low) low_sum(o1, false, 4);
-        }
-      } else {
-        for (int t = 0; 4 * t < kc; ++t) {
-          Operands<LM1, NC> o0;
-          load_ops<LM1, NC>(o0, xst + 4 * t * XS, h8, col0, r, pidx, 4 * t + q >= kc);
-          mma_step(o0);
-          if (do_low) low_sum(o0, true, kc - 4 * t);
-        }
+  int lowpend = 0;     // rows pending in the low buffer (0: none)
+  int lowbuf_cur = 0;
+  for (uint32_t c = 0; c < chunks; ++c) {
+    const uint32_t st = c % STAGES;
+    if (warp == 0) pump(c);
+    __syncwarp();
+    mbar_wait(full + st, (c / STAGES) & 1u);
+    const double* xst = xs + st * stage_elems + static_cast<size_t>(q) * n;
+    const int kc = static_cast<int>(min(static_cast<uint32_t>(KC), K - c * KC));
+    const int steps = (kc + 3) / 4;
+    Raw<LM1, NC> cur, nxt;
+    load_raw<LM1, NC>(cur, xst, h8, col0, r, pidx);
+    finish<LM1, NC>(cur, q >= kc);
+#pragma unroll 2
+    for (int t = 0; t < steps; ++t) {
+      // (1) issue the next step's shared-memory loads
+      if (t + 1 < steps) load_raw<LM1, NC>(nxt, xst + (4 * t + 4) * n, h8, col0, r, pidx);
+      // (2) previous step's transposed row values
+      double2 lv[4];
+      if (do_low && lowpend) {
+        __syncwarp();
+        low_get(lv, lowbuf_cur ^ 1);
       }
-      // every lane has consumed its rows of this stage
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty + st);
-      if (warp == 0) pump(0);  // refill without blocking
+      // (3) this step's DMMAs keep the FP64 tensor pipe busy meanwhile
+      mma_step(cur);
+      // (4) hand this step's A values to the row owners, fold the previous
+      if (do_low) {
+        low_put(cur, lowbuf_cur);
+        if (lowpend) low_add(lv, lowpend);
+        lowpend = min(4, kc - 4 * t);
+        lowbuf_cur ^= 1;
+      }
+      // (5) products of the next step
+      if (t + 1 < steps) {
+        finish<LM1, NC>(nxt, 4 * t + 4 + q >= kc);
+        cur = nxt;
+      }
     }
-    if (P.npass == 2 && pass == 0) {
-      // end of the incoming pass: stash its means, restart the accumulators
-      double* stash = P.scratch + static_cast<size_t>(blockIdx.x) * (WARPS * 32 * 64);
-      const int tid = threadIdx.x;
+    // every lane has consumed its rows of this stage
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + st);
+    if (warp == 0) pump(0);  // refill without blocking
+  }
+  if (do_low && lowpend) {
+    __syncwarp();
+    double2 lv[4];
+    low_get(lv, lowbuf_cur ^ 1);
+    low_add(lv, lowpend);
+  }
+
+  // ---- pair fixup: the second of (incoming, outgoing) does the update ----
+  const bool update = P.npass == 2;
+  const size_t pair = tile.pad1;
+  const int tid = threadIdx.x;
+  double* mine = nullptr;
+  const double* other = nullptr;
+  if (update) {
+    double* base = P.scratch + pair * (2 * (THREADS * 64 + THREADS * 2));
+    mine = base + pass * (THREADS * 64 + THREADS * 2);
+    other = base + (pass ^ 1) * (THREADS * 64 + THREADS * 2);
 #pragma unroll
-      for (int g = 0; g < 8; ++g)
+    for (int g = 0; g < 8; ++g)
 #pragma unroll
-        for (int c = 0; c < NC; ++c)
+      for (int c = 0; c < NC; ++c)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            stash[static_cast<size_t>((g * NC + c) * 2 + e) * (WARPS * 32) + tid] = __dmul_rn(acc[g][c][e], P.inv);
-            acc[g][c][e] = 0.0;
-          }
-      lowin[0] = __dmul_rn(lowacc[0], P.inv);
-      lowin[1] = __dmul_rn(lowacc[1], P.inv);
-      lowacc[0] = lowacc[1] = 0.0;
-    }
+        for (int e = 0; e < 2; ++e)
+          mine[static_cast<size_t>((g * NC + c) * 2 + e) * THREADS + tid] = __dmul_rn(acc[g][c][e], P.inv);
+    mine[THREADS * 64 + tid] = __dmul_rn(lowacc[0], P.inv);
+    mine[THREADS * 64 + THREADS + tid] = __dmul_rn(lowacc[1], P.inv);
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) *flag_smem = atomicAdd(P.flags + pair, 1u);
+    __syncthreads();
+    if (*flag_smem == 0) return;  // partner still running: it finishes the pair
+    __threadfence();
+    if (tid == 0) P.flags[pair] = 0;  // self-resetting for the next launch
   }
 
   // ---- epilogue ----
   if (!gvalid) return;
-  const double* stash = P.scratch + static_cast<size_t>(blockIdx.x) * (WARPS * 32 * 64);
-  const bool update = P.npass == 2;
 #pragma unroll
   for (int g = 0; g < 8; ++g) {
     const int iL = h8 + g;
@@ -386,10 +414,16 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
       for (int e = 0; e < 2; ++e) {
         const int col = col0 + 8 * c + 2 * q + e;
         if (col >= n || col < iL) continue;
-        const double v = __dmul_rn(acc[g][c][e], P.inv);
-        const double delta =
-            update ? __dsub_rn(stash[static_cast<size_t>((g * NC + c) * 2 + e) * (WARPS * 32) + threadIdx.x], v)
-                   : 0.0;
+        double v, delta = 0.0;
+        if (update) {
+          const size_t ix = static_cast<size_t>((g * NC + c) * 2 + e) * THREADS + tid;
+          const double a = pass == 0 ? mine[ix] : __ldcg(other + ix);
+          const double bb = pass == 1 ? mine[ix] : __ldcg(other + ix);
+          delta = __dsub_rn(a, bb);
+          v = 0.0;
+        } else {
+          v = __dmul_rn(acc[g][c][e], P.inv);
+        }
         const int jd = col / b;
         const uint64_t blk = pr.top_base + static_cast<uint64_t>(pr.vprime) * b * (jd - J);
         if (!runs && jd != J) {
@@ -414,8 +448,15 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
       const int iL = h8 + g;
       if (g < lo || iL >= n) continue;
       const PrefixRow& pr = P.rows[static_cast<size_t>(gi) * 8 + g];
-      const double v = __dmul_rn(lowacc[e], P.inv);
-      const double delta = update ? __dsub_rn(lowin[e], v) : 0.0;
+      double v = 0.0, delta = 0.0;
+      if (update) {
+        const size_t ix = THREADS * 64 + static_cast<size_t>(e) * THREADS + tid;
+        const double a = pass == 0 ? mine[ix] : __ldcg(other + ix);
+        const double bb = pass == 1 ? mine[ix] : __ldcg(other + ix);
+        delta = __dsub_rn(a, bb);
+      } else {
+        v = __dmul_rn(lowacc[e], P.inv);
+      }
       int jv[kMaxOrder], ov[kMaxOrder], ev[kMaxOrder];
       for (int t = 0; t <= LM1; ++t) {
         const int iq = t < LM1 ? pidx[t] : iL;
@@ -428,15 +469,17 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
   }
 }
 
-__global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomParams P) {
+__global__ void __launch_bounds__(THREADS, 2) moment_top_dmma_kernel(const MomParams P) {
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t full[STAGES];
   __shared__ __align__(8) uint64_t empty[STAGES];
+  __shared__ uint32_t flag_smem;
   double* xs = smem;
   // dense staging ring; reads past row n of a stage (the last 8-column
   // window / column group) only feed rows and columns that are never stored
-  double* lowbufs = xs + static_cast<size_t>(STAGES) * KC * P.n + 64;  // WARPS x 4 x 66
-  const MomTile tile = P.tiles[blockIdx.x];
+  double* lowbufs = xs + static_cast<size_t>(STAGES) * KC * P.n + 64;  // WARPS x 2 x 4 x 66
+  const int pass = static_cast<int>(blockIdx.x % P.npass);
+  const MomTile tile = P.tiles[blockIdx.x / P.npass];
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full + s, 1);
@@ -448,7 +491,7 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
   const int nc = static_cast<int>(tile.pad0);
   switch (P.L * 8 + nc) {
 #define CSB_CASE(LL, NCC) \
-  case (LL) * 8 + (NCC): run_tile<(LL) - 1, NCC>(P, tile, xs, full, empty, lowbufs); break;
+  case (LL) * 8 + (NCC): run_tile<(LL) - 1, NCC>(P, tile, pass, xs, full, empty, lowbufs, &flag_smem); break;
 #define CSB_CASES(LL) CSB_CASE(LL, 1) CSB_CASE(LL, 2) CSB_CASE(LL, 3) CSB_CASE(LL, 4)
     CSB_CASES(2) CSB_CASES(3) CSB_CASES(4) CSB_CASES(5)
 #undef CSB_CASES
@@ -457,29 +500,30 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
   }
 }
 
+size_t smem_bytes(int n) {
+  return sizeof(double) * (static_cast<size_t>(STAGES) * KC * n + 64 + WARPS * 2 * 4 * 66);
+}
+
 }  // namespace
 
 int dmma_warps() { return WARPS; }
 
-size_t dmma_scratch_per_tile() { return static_cast<size_t>(WARPS) * 32 * 64; }
+// per tile pair: both passes' stashes (64 values + 2 low sums per thread)
+size_t dmma_scratch_per_tile() { return static_cast<size_t>(2) * (THREADS * 64 + THREADS * 2); }
 
 bool dmma_supported(const MomParams& p) {
   // instantiated for orders 3..6 (L = 2..5); the staging ring must fit
   if (p.n % 2 != 0 || p.L < 2 || p.L > 5) return false;
-  if (sizeof(double) * (static_cast<size_t>(STAGES) * KC * p.n + 64 + WARPS * 4 * 66) > 220 * 1024) return false;
-  for (int s = 0; s < p.npass; ++s) {
-    if (reinterpret_cast<uintptr_t>(p.src[s].seg0) % 16) return false;
-    if (p.src[s].len1 && reinterpret_cast<uintptr_t>(p.src[s].seg1) % 16) return false;
-  }
+  if (smem_bytes(p.n) > 220 * 1024) return false;
   return true;
 }
 
 void launch_moment_top_dmma(const MomParams& p, int ntiles, cudaStream_t st) {
   if (ntiles <= 0) return;
-  const size_t smem = sizeof(double) * (static_cast<size_t>(STAGES) * KC * p.n + 64 + WARPS * 4 * 66);
+  const size_t smem = smem_bytes(p.n);
   CSB_CUDA(cudaFuncSetAttribute(moment_top_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
-  moment_top_dmma_kernel<<<ntiles, THREADS, smem, st>>>(p);
+  moment_top_dmma_kernel<<<ntiles * p.npass, THREADS, smem, st>>>(p);
   CSB_CUDA(cudaGetLastError());
   count_launch();
 }

@@ -199,9 +199,17 @@ void check_order(const csb_series* s, int order) {
 // Scratch buffer for the pass-0 stash of the update kernel (per device).
 struct Scratch {
   DevBuf<double> buf;
+  DevBuf<uint32_t> flags;
   double* get(uint64_t count) {
     if (buf.count < count) buf.alloc(count);
     return buf.ptr;
+  }
+  uint32_t* get_flags(uint64_t count) {
+    if (flags.count < count) {
+      flags.alloc(count);
+      CSB_CUDA(cudaMemset(flags.ptr, 0, flags.bytes()));
+    }
+    return flags.ptr;
   }
 };
 thread_local std::map<int, Scratch> g_scratch;
@@ -242,6 +250,7 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
     p.groups = plan->d_groups.ptr;
     const uint64_t ntiles = plan->tiles.size();
     if (npass == 2 || use_dmma) p.scratch = g_scratch[dev.id].get(ntiles * plan->scratch_per_tile);
+    if (use_dmma) p.flags = g_scratch[dev.id].get_flags(ntiles);
     ProfScope ps(top ? "moment_top" : "moment_low", st);
     if (use_dmma)
       launch_moment_top_dmma(p, static_cast<int>(ntiles), st);
