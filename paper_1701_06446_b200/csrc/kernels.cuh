@@ -27,6 +27,7 @@ struct MomParams {
   double* low = nullptr;      // M_{S-1} (nullptr: not written)
   double* scratch = nullptr;  // pass-0 stash (DMMA: per tile pair, both passes)
   uint32_t* flags = nullptr;  // DMMA: per tile pair arrival counters (self-resetting)
+  const double* zeros = nullptr;  // DMMA: >= 32 x n zero doubles (tail rows of a pass)
   double c = 0.0;             // p / T        (moments.cpp:287)
   double inv = 1.0;           // 1.0 / rows   (moments.cpp:148)
 };

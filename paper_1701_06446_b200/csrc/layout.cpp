@@ -144,6 +144,11 @@ PrefixRow MomentPlan::make_row(const int* t, const Layout& top, const Layout* lo
   r.low_off = low ? low->offset[low->rank(jj)] + poff : 0;
   r.vprime = vprime;
   r.poff = poff;
+  // bit 0 of the spare idx slot: equal neighbouring block coordinates among
+  // (j_1..j_L), i.e. the prefix block has internal symmetry copies
+  uint16_t runs = 0;
+  for (int k = 1; k < L; ++k) runs |= jj[k] == jj[k - 1];
+  r.idx[7] = runs;
   return r;
 }
 

@@ -36,7 +36,7 @@ namespace {
 
 constexpr int WARPS = 4;  // MMA warps; lane 0 of warp 0 also drives the TMA
 constexpr int THREADS = WARPS * 32;
-constexpr int STAGES = 4;
+constexpr int STAGES = 3;
 constexpr int KC = 32;        // data rows per stage
 
 
@@ -254,7 +254,11 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
       const uint32_t kc = min(static_cast<uint32_t>(KC), K - a0);
       double* dst = xs + st * stage_elems;
       const uint32_t rb = static_cast<uint32_t>(n) * 8u;
-      mbar_expect_tx(full + st, kc * rb);
+      mbar_expect_tx(full + st, static_cast<uint32_t>(KC) * rb);
+      // rows past the end of the pass are zero rows: A = B = 0 adds exact
+      // zeros, so the k loop never needs masking
+      if (kc < static_cast<uint32_t>(KC))
+        bulk_g2s(dst + static_cast<size_t>(kc) * n, P.zeros, (KC - kc) * rb, full + st);
       // rows [a0, a0 + kc) are contiguous except across the ring's wrap
       if (a0 + kc <= src.len0 || a0 >= src.len0) {
         bulk_g2s(dst, row_ptr(src, a0, n), kc * rb, full + st);
@@ -312,43 +316,38 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
   };
 
   pump(0);
-  int lowpend = 0;     // rows pending in the low buffer (0: none)
-  int lowbuf_cur = 0;
+  bool lowpend = false;  // previous step's A values wait in lowbuf[1 - cur]
+  int lb = 0;
+  // one step: loads of the next step, DMMAs of this one, row sums, products
+  auto step = [&](const Raw<LM1, NC>& cur, Raw<LM1, NC>& nxt, const double* xnext, bool has_next) {
+    if (has_next) load_raw<LM1, NC>(nxt, xnext, h8, col0, r, pidx);
+    double2 lv[4];
+    if (do_low && lowpend) {
+      __syncwarp();
+      low_get(lv, lb ^ 1);
+    }
+    mma_step(cur);
+    if (do_low) {
+      low_put(cur, lb);
+      if (lowpend) low_add(lv, 4);
+      lowpend = true;
+      lb ^= 1;
+    }
+    if (has_next) finish<LM1, NC>(nxt, false);
+  };
   for (uint32_t c = 0; c < chunks; ++c) {
     const uint32_t st = c % STAGES;
     if (warp == 0) pump(c);
     __syncwarp();
     mbar_wait(full + st, (c / STAGES) & 1u);
     const double* xst = xs + st * stage_elems + static_cast<size_t>(q) * n;
-    const int kc = static_cast<int>(min(static_cast<uint32_t>(KC), K - c * KC));
-    const int steps = (kc + 3) / 4;
-    Raw<LM1, NC> cur, nxt;
-    load_raw<LM1, NC>(cur, xst, h8, col0, r, pidx);
-    finish<LM1, NC>(cur, q >= kc);
-#pragma unroll 2
-    for (int t = 0; t < steps; ++t) {
-      // (1) issue the next step's shared-memory loads
-      if (t + 1 < steps) load_raw<LM1, NC>(nxt, xst + (4 * t + 4) * n, h8, col0, r, pidx);
-      // (2) previous step's transposed row values
-      double2 lv[4];
-      if (do_low && lowpend) {
-        __syncwarp();
-        low_get(lv, lowbuf_cur ^ 1);
-      }
-      // (3) this step's DMMAs keep the FP64 tensor pipe busy meanwhile
-      mma_step(cur);
-      // (4) hand this step's A values to the row owners, fold the previous
-      if (do_low) {
-        low_put(cur, lowbuf_cur);
-        if (lowpend) low_add(lv, lowpend);
-        lowpend = min(4, kc - 4 * t);
-        lowbuf_cur ^= 1;
-      }
-      // (5) products of the next step
-      if (t + 1 < steps) {
-        finish<LM1, NC>(nxt, 4 * t + 4 + q >= kc);
-        cur = nxt;
-      }
+    Raw<LM1, NC> o0, o1;
+    load_raw<LM1, NC>(o0, xst, h8, col0, r, pidx);
+    finish<LM1, NC>(o0, false);
+#pragma unroll 1
+    for (int t = 0; t < KC / 4; t += 2) {
+      step(o0, o1, xst + (4 * t + 4) * n, true);
+      step(o1, o0, xst + (4 * t + 8) * n, t + 2 < KC / 4);
     }
     // every lane has consumed its rows of this stage
     __syncwarp();
@@ -358,8 +357,8 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
   if (do_low && lowpend) {
     __syncwarp();
     double2 lv[4];
-    low_get(lv, lowbuf_cur ^ 1);
-    low_add(lv, lowpend);
+    low_get(lv, lb ^ 1);
+    low_add(lv, 4);
   }
 
   // ---- pair fixup: the second of (incoming, outgoing) does the update ----
@@ -392,53 +391,73 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
 
   // ---- epilogue ----
   if (!gvalid) return;
+  const double cc = P.c;
 #pragma unroll
   for (int g = 0; g < 8; ++g) {
     const int iL = h8 + g;
     if (g < lo || iL >= n) continue;
     const PrefixRow& pr = P.rows[static_cast<size_t>(gi) * 8 + g];
-    int jv[kMaxOrder], ov[kMaxOrder], ev[kMaxOrder];
-    bool runs = false;
-#pragma unroll
-    for (int t = 0; t <= LM1; ++t) {
-      const int iq = t < LM1 ? pidx[t] : iL;
-      jv[t] = iq / b;
-      ov[t] = iq - jv[t] * b;
-      ev[t] = ext_of(jv[t], n, b);
-      if (t > 0) runs |= jv[t] == jv[t - 1];
-    }
-    const int J = jv[LM1];
+    const bool row_runs = (pr.idx[7] & 1u) != 0;  // runs among (j_1..j_L)
+    const int J = iL / b;
+    // fast path (block (j_1..j_L, jd) with distinct coordinates: the
+    // canonical entry is the only stored copy): batch the loads
+    double* addr[NC][2];
+    double val[NC][2];
+    bool fast[NC][2];
 #pragma unroll
     for (int c = 0; c < NC; ++c)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int col = col0 + 8 * c + 2 * q + e;
-        if (col >= n || col < iL) continue;
-        double v, delta = 0.0;
+        const int jd = col / b;
+        const bool ok = col < n && col >= iL;
+        fast[c][e] = ok && !row_runs && jd != J;
+        addr[c][e] = P.top + pr.top_base + static_cast<uint64_t>(pr.vprime) * b * (jd - J) +
+                     static_cast<uint64_t>(pr.poff) * ext_of(jd, n, b) + (col - jd * b);
         if (update) {
           const size_t ix = static_cast<size_t>((g * NC + c) * 2 + e) * THREADS + tid;
-          const double a = pass == 0 ? mine[ix] : __ldcg(other + ix);
-          const double bb = pass == 1 ? mine[ix] : __ldcg(other + ix);
-          delta = __dsub_rn(a, bb);
-          v = 0.0;
+          const double mv = mine[ix];
+          const double ov = ok ? __ldcg(other + ix) : 0.0;
+          val[c][e] = pass == 0 ? __dsub_rn(mv, ov) : __dsub_rn(ov, mv);  // a - b
         } else {
-          v = __dmul_rn(acc[g][c][e], P.inv);
+          val[c][e] = __dmul_rn(acc[g][c][e], P.inv);
+        }
+      }
+    if (update) {
+      double old[NC][2];
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) old[c][e] = fast[c][e] ? *addr[c][e] : 0.0;
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          if (fast[c][e]) *addr[c][e] = __fma_rn(cc, val[c][e], old[c][e]);
+    } else {
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          if (fast[c][e]) *addr[c][e] = val[c][e];
+    }
+    // diagonal blocks: every stored copy (permutations within runs)
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = col0 + 8 * c + 2 * q + e;
+        if (col >= n || col < iL || fast[c][e]) continue;
+        int jv[kMaxOrder], ov[kMaxOrder], ev[kMaxOrder];
+        for (int t = 0; t <= L; ++t) {
+          const int iq = t < LM1 ? pidx[t] : (t == LM1 ? iL : col);
+          jv[t] = iq / b;
+          ov[t] = iq - jv[t] * b;
+          ev[t] = ext_of(jv[t], n, b);
         }
         const int jd = col / b;
         const uint64_t blk = pr.top_base + static_cast<uint64_t>(pr.vprime) * b * (jd - J);
-        if (!runs && jd != J) {
-          // off-diagonal block: the canonical entry is the only stored copy
-          double* p = P.top + blk + static_cast<uint64_t>(pr.poff) * ext_of(jd, n, b) + (col - jd * b);
-          *p = update ? __fma_rn(P.c, delta, *p) : v;
-        } else {
-          jv[L] = jd;
-          ov[L] = col - jd * b;
-          ev[L] = ext_of(jd, n, b);
-          int o2[kMaxOrder];
-#pragma unroll
-          for (int t = 0; t <= L; ++t) o2[t] = ov[t];
-          store_copies(P.top, L + 1, jv, o2, ev, blk, update, P.c, delta, v);
-        }
+        store_copies(P.top, L + 1, jv, ov, ev, blk, update, cc, val[c][e], val[c][e]);
       }
   }
   if (do_low) {
@@ -451,9 +470,8 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
       double v = 0.0, delta = 0.0;
       if (update) {
         const size_t ix = THREADS * 64 + static_cast<size_t>(e) * THREADS + tid;
-        const double a = pass == 0 ? mine[ix] : __ldcg(other + ix);
-        const double bb = pass == 1 ? mine[ix] : __ldcg(other + ix);
-        delta = __dsub_rn(a, bb);
+        const double mv = mine[ix], ov2 = __ldcg(other + ix);
+        delta = pass == 0 ? __dsub_rn(mv, ov2) : __dsub_rn(ov2, mv);
       } else {
         v = __dmul_rn(lowacc[e], P.inv);
       }
@@ -514,7 +532,7 @@ size_t dmma_scratch_per_tile() { return static_cast<size_t>(2) * (THREADS * 64 +
 bool dmma_supported(const MomParams& p) {
   // instantiated for orders 3..6 (L = 2..5); the staging ring must fit
   if (p.n % 2 != 0 || p.L < 2 || p.L > 5) return false;
-  if (smem_bytes(p.n) > 220 * 1024) return false;
+  if (smem_bytes(p.n) > 110 * 1024) return false;  // two CTAs per SM
   return true;
 }
 

@@ -204,6 +204,14 @@ struct Scratch {
     if (buf.count < count) buf.alloc(count);
     return buf.ptr;
   }
+  DevBuf<double> zeros;
+  const double* get_zeros(uint64_t count) {
+    if (zeros.count < count) {
+      zeros.alloc(count);
+      CSB_CUDA(cudaMemset(zeros.ptr, 0, zeros.bytes()));
+    }
+    return zeros.ptr;
+  }
   uint32_t* get_flags(uint64_t count) {
     if (flags.count < count) {
       flags.alloc(count);
@@ -250,7 +258,10 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
     p.groups = plan->d_groups.ptr;
     const uint64_t ntiles = plan->tiles.size();
     if (npass == 2 || use_dmma) p.scratch = g_scratch[dev.id].get(ntiles * plan->scratch_per_tile);
-    if (use_dmma) p.flags = g_scratch[dev.id].get_flags(ntiles);
+    if (use_dmma) {
+      p.flags = g_scratch[dev.id].get_flags(ntiles);
+      p.zeros = g_scratch[dev.id].get_zeros(32ull * m->n);
+    }
     ProfScope ps(top ? "moment_top" : "moment_low", st);
     if (use_dmma)
       launch_moment_top_dmma(p, static_cast<int>(ntiles), st);
