@@ -28,6 +28,8 @@ struct MomParams {
   double* scratch = nullptr;  // pass-0 stash (DMMA: per tile pair, both passes)
   uint32_t* flags = nullptr;  // DMMA: per tile pair arrival counters (self-resetting)
   const double* zeros = nullptr;  // DMMA: >= 32 x n zero doubles (tail rows of a pass)
+  double* dtop = nullptr;         // DMMA update: canonical deltas of M_S (diagonal blocks)
+  double* dlow = nullptr;         // DMMA update: canonical deltas of M_{S-1}
   double c = 0.0;             // p / T        (moments.cpp:287)
   double inv = 1.0;           // 1.0 / rows   (moments.cpp:148)
 };
@@ -82,5 +84,8 @@ bool dmma_supported(const MomParams& p);
 int dmma_warps();
 size_t dmma_scratch_per_tile();
 void launch_moment_top_dmma(const MomParams& p, int ntiles, cudaStream_t st);
+// copies of canonical entries in blocks with runs (after the DMMA kernel)
+void launch_mirror(int S, double* m, const double* delta, const LayoutDev& lay, const uint32_t* blocks,
+                   uint32_t nblocks, int n, int b, bool update, double c, cudaStream_t st);
 
 }  // namespace csb

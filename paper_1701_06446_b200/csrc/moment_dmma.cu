@@ -87,61 +87,6 @@ __device__ __forceinline__ const double* row_ptr(const RowSource& s, uint32_t k,
 
 __device__ __forceinline__ int ext_of(int j, int n, int b) { return b < n - j * b ? b : n - j * b; }
 
-__device__ __forceinline__ bool next_perm(int* a, int len) {
-  if (len < 2) return false;
-  int i = len - 2;
-  while (i >= 0 && a[i] >= a[i + 1]) --i;
-  if (i < 0) {
-    for (int l = 0, r = len - 1; l < r; ++l, --r) {
-      const int t = a[l];
-      a[l] = a[r];
-      a[r] = t;
-    }
-    return false;
-  }
-  int j = len - 1;
-  while (a[j] <= a[i]) --j;
-  int t = a[i];
-  a[i] = a[j];
-  a[j] = t;
-  for (int l = i + 1, r = len - 1; l < r; ++l, --r) {
-    t = a[l];
-    a[l] = a[r];
-    a[r] = t;
-  }
-  return true;
-}
-
-// RMW (update) or assign every stored copy of one canonical element
-// (distinct permutations of the in-block offsets within runs of equal block
-// coordinate, symten.cpp:195-220).
-__device__ __noinline__ void store_copies(double* dst, int S, const int* jv, int* ov, const int* ev,
-                                          uint64_t blk, bool update, double c, double delta, double v) {
-  bool runs = false;
-  for (int k = 1; k < S; ++k) runs |= (jv[k] == jv[k - 1]);
-  int rs[kMaxOrder], re[kMaxOrder], nr = 0;
-  if (runs) {
-    for (int s = 0; s < S;) {
-      int t = s + 1;
-      while (t < S && jv[t] == jv[s]) ++t;
-      rs[nr] = s;
-      re[nr] = t;
-      ++nr;
-      s = t;
-    }
-  }
-  for (;;) {
-    uint64_t off = 0;
-    for (int k = 0; k < S; ++k) off = off * static_cast<uint64_t>(ev[k]) + static_cast<uint64_t>(ov[k]);
-    double* p = dst + blk + off;
-    *p = update ? __fma_rn(c, delta, *p) : v;
-    if (!runs) break;
-    int q = nr - 1;
-    while (q >= 0 && !next_perm(ov + rs[q], re[q] - rs[q])) --q;
-    if (q < 0) break;
-  }
-}
-
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -389,7 +334,11 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
     if (tid == 0) P.flags[pair] = 0;  // self-resetting for the next launch
   }
 
-  // ---- epilogue ----
+  // ---- epilogue: canonical entries only ----
+  // Entries of blocks with equal neighbouring coordinates have symmetric
+  // copies; for those the update's delta is also written to the delta
+  // buffer at the canonical position and mirror_kernel applies it to every
+  // other stored copy (or copies the value, for an assignment).
   if (!gvalid) return;
   const double cc = P.c;
 #pragma unroll
@@ -399,25 +348,23 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
     const PrefixRow& pr = P.rows[static_cast<size_t>(gi) * 8 + g];
     const bool row_runs = (pr.idx[7] & 1u) != 0;  // runs among (j_1..j_L)
     const int J = iL / b;
-    // fast path (block (j_1..j_L, jd) with distinct coordinates: the
-    // canonical entry is the only stored copy): batch the loads
-    double* addr[NC][2];
+    size_t off[NC][2];
     double val[NC][2];
-    bool fast[NC][2];
+    bool ok[NC][2], diag[NC][2];
 #pragma unroll
     for (int c = 0; c < NC; ++c)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int col = col0 + 8 * c + 2 * q + e;
         const int jd = col / b;
-        const bool ok = col < n && col >= iL;
-        fast[c][e] = ok && !row_runs && jd != J;
-        addr[c][e] = P.top + pr.top_base + static_cast<uint64_t>(pr.vprime) * b * (jd - J) +
-                     static_cast<uint64_t>(pr.poff) * ext_of(jd, n, b) + (col - jd * b);
+        ok[c][e] = col < n && col >= iL;
+        diag[c][e] = row_runs || jd == J;
+        off[c][e] = pr.top_base + static_cast<uint64_t>(pr.vprime) * b * (jd - J) +
+                    static_cast<uint64_t>(pr.poff) * ext_of(jd, n, b) + (col - jd * b);
         if (update) {
           const size_t ix = static_cast<size_t>((g * NC + c) * 2 + e) * THREADS + tid;
           const double mv = mine[ix];
-          const double ov = ok ? __ldcg(other + ix) : 0.0;
+          const double ov = ok[c][e] ? __ldcg(other + ix) : 0.0;
           val[c][e] = pass == 0 ? __dsub_rn(mv, ov) : __dsub_rn(ov, mv);  // a - b
         } else {
           val[c][e] = __dmul_rn(acc[g][c][e], P.inv);
@@ -428,37 +375,22 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
 #pragma unroll
       for (int c = 0; c < NC; ++c)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) old[c][e] = fast[c][e] ? *addr[c][e] : 0.0;
+        for (int e = 0; e < 2; ++e) old[c][e] = ok[c][e] ? P.top[off[c][e]] : 0.0;
 #pragma unroll
       for (int c = 0; c < NC; ++c)
 #pragma unroll
         for (int e = 0; e < 2; ++e)
-          if (fast[c][e]) *addr[c][e] = __fma_rn(cc, val[c][e], old[c][e]);
+          if (ok[c][e]) {
+            P.top[off[c][e]] = __fma_rn(cc, val[c][e], old[c][e]);
+            if (diag[c][e]) P.dtop[off[c][e]] = val[c][e];
+          }
     } else {
 #pragma unroll
       for (int c = 0; c < NC; ++c)
 #pragma unroll
         for (int e = 0; e < 2; ++e)
-          if (fast[c][e]) *addr[c][e] = val[c][e];
+          if (ok[c][e]) P.top[off[c][e]] = val[c][e];
     }
-    // diagonal blocks: every stored copy (permutations within runs)
-#pragma unroll
-    for (int c = 0; c < NC; ++c)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int col = col0 + 8 * c + 2 * q + e;
-        if (col >= n || col < iL || fast[c][e]) continue;
-        int jv[kMaxOrder], ov[kMaxOrder], ev[kMaxOrder];
-        for (int t = 0; t <= L; ++t) {
-          const int iq = t < LM1 ? pidx[t] : (t == LM1 ? iL : col);
-          jv[t] = iq / b;
-          ov[t] = iq - jv[t] * b;
-          ev[t] = ext_of(jv[t], n, b);
-        }
-        const int jd = col / b;
-        const uint64_t blk = pr.top_base + static_cast<uint64_t>(pr.vprime) * b * (jd - J);
-        store_copies(P.top, L + 1, jv, ov, ev, blk, update, cc, val[c][e], val[c][e]);
-      }
   }
   if (do_low) {
 #pragma unroll
@@ -467,22 +399,15 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
       const int iL = h8 + g;
       if (g < lo || iL >= n) continue;
       const PrefixRow& pr = P.rows[static_cast<size_t>(gi) * 8 + g];
-      double v = 0.0, delta = 0.0;
       if (update) {
         const size_t ix = THREADS * 64 + static_cast<size_t>(e) * THREADS + tid;
         const double mv = mine[ix], ov2 = __ldcg(other + ix);
-        delta = pass == 0 ? __dsub_rn(mv, ov2) : __dsub_rn(ov2, mv);
+        const double delta = pass == 0 ? __dsub_rn(mv, ov2) : __dsub_rn(ov2, mv);
+        P.low[pr.low_off] = __fma_rn(cc, delta, P.low[pr.low_off]);
+        if (pr.idx[7] & 1u) P.dlow[pr.low_off] = delta;
       } else {
-        v = __dmul_rn(lowacc[e], P.inv);
+        P.low[pr.low_off] = __dmul_rn(lowacc[e], P.inv);
       }
-      int jv[kMaxOrder], ov[kMaxOrder], ev[kMaxOrder];
-      for (int t = 0; t <= LM1; ++t) {
-        const int iq = t < LM1 ? pidx[t] : iL;
-        jv[t] = iq / b;
-        ov[t] = iq - jv[t] * b;
-        ev[t] = ext_of(jv[t], n, b);
-      }
-      store_copies(P.low, L, jv, ov, ev, pr.low_off - pr.poff, update, P.c, delta, v);
     }
   }
 }
@@ -518,6 +443,55 @@ __global__ void __launch_bounds__(THREADS, 2) moment_top_dmma_kernel(const MomPa
   }
 }
 
+// Symmetric copies of the canonical entries written above, one CTA per
+// stored block with equal neighbouring coordinates (symten.cpp:195-220):
+// entry o of block j is a copy of the entry with o sorted within each run
+// of equal j; an update applies the canonical delta to the copy's own old
+// value (moments.cpp:294-299 RMWs every stored entry), an assignment copies.
+template <int S>
+__global__ void __launch_bounds__(256) mirror_kernel(double* __restrict__ m, const double* __restrict__ delta,
+                                                     LayoutDev lay, const uint32_t* __restrict__ blocks, int n,
+                                                     int b, bool update, double c) {
+  const uint32_t blk = blocks[blockIdx.x];
+  int j[S], e[S];
+#pragma unroll
+  for (int k = 0; k < S; ++k) {
+    j[k] = lay.index[static_cast<size_t>(blk) * S + k];
+    e[k] = ext_of(j[k], n, b);
+  }
+  const uint64_t base = lay.offset[blk];
+  const uint64_t vol = lay.offset[blk + 1] - base;
+  for (uint64_t pos = threadIdx.x; pos < vol; pos += blockDim.x) {
+    int o[S];
+    uint64_t rem = pos;
+#pragma unroll
+    for (int k = S - 1; k >= 0; --k) {
+      o[k] = static_cast<int>(rem % e[k]);
+      rem /= e[k];
+    }
+    // sort within runs (bubble passes over a tiny array, fully unrolled)
+    bool canonical = true;
+#pragma unroll
+    for (int k = 1; k < S; ++k)
+      if (j[k] == j[k - 1] && o[k] < o[k - 1]) canonical = false;
+    if (canonical) continue;
+#pragma unroll
+    for (int pass = 0; pass < S - 1; ++pass)
+#pragma unroll
+      for (int k = 1; k < S; ++k)
+        if (j[k] == j[k - 1] && o[k] < o[k - 1]) {
+          const int t = o[k];
+          o[k] = o[k - 1];
+          o[k - 1] = t;
+        }
+    uint64_t src = 0;
+#pragma unroll
+    for (int k = 0; k < S; ++k) src = src * e[k] + o[k];
+    double* p = m + base + pos;
+    *p = update ? __fma_rn(c, delta[base + src], *p) : m[base + src];
+  }
+}
+
 size_t smem_bytes(int n) {
   return sizeof(double) * (static_cast<size_t>(STAGES) * KC * n + 64 + WARPS * 2 * 4 * 66);
 }
@@ -534,6 +508,20 @@ bool dmma_supported(const MomParams& p) {
   if (p.n % 2 != 0 || p.L < 2 || p.L > 5) return false;
   if (smem_bytes(p.n) > 110 * 1024) return false;  // two CTAs per SM
   return true;
+}
+
+void launch_mirror(int S, double* m, const double* delta, const LayoutDev& lay, const uint32_t* blocks,
+                   uint32_t nblocks, int n, int b, bool update, double c, cudaStream_t st) {
+  if (!nblocks) return;
+  switch (S) {
+#define CSB_MIRROR(SS) \
+  case SS: mirror_kernel<SS><<<nblocks, 256, 0, st>>>(m, delta, lay, blocks, n, b, update, c); break;
+    CSB_MIRROR(2) CSB_MIRROR(3) CSB_MIRROR(4) CSB_MIRROR(5) CSB_MIRROR(6) CSB_MIRROR(7) CSB_MIRROR(8)
+#undef CSB_MIRROR
+    default: fail(CSB_EINVAL, "mirror: order out of range");
+  }
+  CSB_CUDA(cudaGetLastError());
+  count_launch();
 }
 
 void launch_moment_top_dmma(const MomParams& p, int ntiles, cudaStream_t st) {

@@ -32,6 +32,8 @@ struct DevLayout {
   DevBuf<uint16_t> index;
   DevBuf<uint64_t> prefix;
   DevBuf<double> mult;
+  DevBuf<uint32_t> diag;  // blocks with equal neighbouring coordinates
+  uint32_t ndiag = 0;
   LayoutDev view() const {
     LayoutDev v;
     v.offset = offset.ptr;
@@ -94,6 +96,16 @@ std::shared_ptr<DevLayout> get_layout(Device& dev, int order, int n, int b) {
     CSB_CUDA(cudaMemcpy(L->index.ptr, h.index.data(), L->index.bytes(), cudaMemcpyHostToDevice));
     CSB_CUDA(cudaMemcpy(L->prefix.ptr, h.prefix.data(), L->prefix.bytes(), cudaMemcpyHostToDevice));
     CSB_CUDA(cudaMemcpy(L->mult.ptr, mult.data(), L->mult.bytes(), cudaMemcpyHostToDevice));
+    std::vector<uint32_t> diag;
+    for (uint64_t r = 0; r < h.nblocks; ++r) {
+      bool runs = false;
+      for (int k = 1; k < order; ++k) runs |= h.index[r * order + k] == h.index[r * order + k - 1];
+      if (runs) diag.push_back(static_cast<uint32_t>(r));
+    }
+    L->ndiag = static_cast<uint32_t>(diag.size());
+    L->diag.alloc(diag.size());
+    if (!diag.empty())
+      CSB_CUDA(cudaMemcpy(L->diag.ptr, diag.data(), L->diag.bytes(), cudaMemcpyHostToDevice));
     slot = L;
   }
   return slot;
@@ -205,6 +217,11 @@ struct Scratch {
     return buf.ptr;
   }
   DevBuf<double> zeros;
+  DevBuf<double> dtop, dlow;
+  double* get_delta(DevBuf<double>& d, uint64_t count) {
+    if (d.count < count) d.alloc(count);
+    return d.ptr;
+  }
   const double* get_zeros(uint64_t count) {
     if (zeros.count < count) {
       zeros.alloc(count);
@@ -258,14 +275,25 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
     p.groups = plan->d_groups.ptr;
     const uint64_t ntiles = plan->tiles.size();
     if (npass == 2 || use_dmma) p.scratch = g_scratch[dev.id].get(ntiles * plan->scratch_per_tile);
+    Scratch& sc = g_scratch[dev.id];
     if (use_dmma) {
-      p.flags = g_scratch[dev.id].get_flags(ntiles);
-      p.zeros = g_scratch[dev.id].get_zeros(32ull * m->n);
+      p.flags = sc.get_flags(ntiles);
+      p.zeros = sc.get_zeros(32ull * m->n);
+      if (npass == 2) {
+        p.dtop = sc.get_delta(sc.dtop, m->lay[S - 1]->host.stored);
+        if (p.low) p.dlow = sc.get_delta(sc.dlow, m->lay[S - 2]->host.stored);
+      }
     }
     ProfScope ps(top ? "moment_top" : "moment_low", st);
-    if (use_dmma)
+    if (use_dmma) {
       launch_moment_top_dmma(p, static_cast<int>(ntiles), st);
-    else
+      const auto& LT = m->lay[S - 1];
+      launch_mirror(S, p.top, p.dtop, LT->view(), LT->diag.ptr, LT->ndiag, m->n, m->b, npass == 2, c, st);
+      if (p.low) {
+        const auto& LL = m->lay[S - 2];
+        launch_mirror(S - 1, p.low, p.dlow, LL->view(), LL->diag.ptr, LL->ndiag, m->n, m->b, npass == 2, c, st);
+      }
+    } else
       launch_moment_pair(p, static_cast<int>(ntiles), top, st);
   }
 }
