@@ -1,0 +1,347 @@
+// moms2cums and the low-order moment kernel (sm_100a).
+//
+// moms2cums_v2 (cumulants.cpp:128-196): one CTA per stored block of C_S.
+//   * the 2^S - 2 lower-order sub-blocks the block's corrections read
+//     (one per proper subset of index positions) are staged in shared
+//     memory when they fit, so every factor C_|P|[i_P] is an LDS;
+//   * phase 1: each canonical entry (offsets non-decreasing within runs of
+//     equal block coordinate) is M - partition_correction<S>(f), with the
+//     partitions in the reference's RGS order and no FMA contraction, so the
+//     result is bit-identical to the reference;
+//   * phase 2: every stored entry is written from its canonical source
+//     (non-canonical entries copy, cumulants.cpp:172-185) coalesced, and the
+//     block's sum of squares (knorm, symten.cpp:257-276) is reduced in a
+//     fixed order for the norm/nu report.
+//
+// moment_lower_kernel: orders S <= d-2 of a window update / prime, one
+// thread per canonical element, rows in order: acc = acc + round(product)
+// exactly as the reference's upper levels (moments.cpp:55-57).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.cuh"
+#include "partitions_gen.cuh"
+
+namespace csb {
+
+namespace {
+
+__device__ __forceinline__ int ext_of(int j, int n, int b) { return b < n - j * b ? b : n - j * b; }
+
+__device__ __forceinline__ uint64_t rank_dev(const LayoutDev& L, const int* j, int order) {
+  uint64_t acc = 0;
+  int lo = 0;
+  for (int i = 0; i < order; ++i) {
+    const int rem = order - 1 - i;
+    acc += L.prefix[static_cast<size_t>(rem) * (L.grid + 1) + j[i]] -
+           L.prefix[static_cast<size_t>(rem) * (L.grid + 1) + lo];
+    lo = j[i];
+  }
+  return acc;
+}
+
+constexpr int popcount_c(int m) { return m == 0 ? 0 : (m & 1) + popcount_c(m >> 1); }
+
+template <int S>
+__device__ __forceinline__ void decode(uint32_t pos, const int (&e)[S], int (&o)[S]) {
+#pragma unroll
+  for (int k = S - 1; k >= 0; --k) {
+    o[k] = static_cast<int>(pos % static_cast<uint32_t>(e[k]));
+    pos /= static_cast<uint32_t>(e[k]);
+  }
+}
+
+template <int S>
+__device__ __forceinline__ bool canonical(const int (&j)[S], const int (&o)[S]) {
+  bool c = true;
+#pragma unroll
+  for (int k = 1; k < S; ++k)
+    if (j[k] == j[k - 1] && o[k] < o[k - 1]) c = false;
+  return c;
+}
+
+// In-block offset of the canonical source of entry o: o sorted within runs.
+template <int S>
+__device__ __forceinline__ uint32_t source_of(const int (&j)[S], int (&o)[S], const int (&e)[S]) {
+#pragma unroll
+  for (int pass = 0; pass < S - 1; ++pass)
+#pragma unroll
+    for (int k = 1; k < S; ++k)
+      if (j[k] == j[k - 1] && o[k] < o[k - 1]) {
+        const int t = o[k];
+        o[k] = o[k - 1];
+        o[k - 1] = t;
+      }
+  uint32_t src = 0;
+#pragma unroll
+  for (int k = 0; k < S; ++k) src = src * static_cast<uint32_t>(e[k]) + static_cast<uint32_t>(o[k]);
+  return src;
+}
+
+template <int S, bool STAGED>
+__global__ void __launch_bounds__(256) moms2cums_v2(const M2CParams P) {
+  constexpr int NM = (1 << S) - 1;  // masks 1..NM-1: proper non-empty subsets
+  extern __shared__ __align__(16) double sfac[];  // staged sub-blocks (STAGED)
+  __shared__ uint64_t sbase[NM];                  // global (or smem) base per subset
+  __shared__ uint32_t sstride[NM][S];
+  __shared__ double red[8];
+  const uint64_t blk = P.blk0 + blockIdx.x;
+  const LayoutDev& LS = P.lay[S - 1];
+  const int n = P.n, b = P.b;
+  int j[S], e[S];
+#pragma unroll
+  for (int k = 0; k < S; ++k) {
+    j[k] = LS.index[blk * S + k];
+    e[k] = ext_of(j[k], n, b);
+  }
+  const uint64_t boff = LS.offset[blk];
+  const uint32_t vol = static_cast<uint32_t>(LS.offset[blk + 1] - boff);
+
+  if (threadIdx.x == 0) {
+    uint32_t soff = 0;
+    for (int m = 1; m < NM; ++m) {
+      int sub[S], cnt = 0;
+      uint32_t svol = 1;
+      for (int k = 0; k < S; ++k)
+        if (m >> k & 1) {
+          sub[cnt++] = j[k];
+          svol *= static_cast<uint32_t>(e[k]);
+        }
+      const LayoutDev& Lq = P.lay[cnt - 1];
+      const uint64_t g = Lq.offset[rank_dev(Lq, sub, cnt)];
+      uint32_t stride = 1;
+      for (int k = S - 1; k >= 0; --k) {
+        if (m >> k & 1) {
+          sstride[m][k] = stride;
+          stride *= static_cast<uint32_t>(e[k]);
+        } else {
+          sstride[m][k] = 0;
+        }
+      }
+      if (STAGED) {
+        sbase[m] = soff;  // offset of the staged copy in shared memory
+        soff += svol;
+      } else {
+        sbase[m] = g;     // offset in C_|m|
+      }
+    }
+  }
+  __syncthreads();
+  if (STAGED) {
+    // copy every needed sub-block into shared memory (coalesced per subset)
+    uint32_t soff = 0;
+    for (int m = 1; m < NM; ++m) {
+      int sub[S], cnt = 0;
+      uint32_t svol = 1;
+#pragma unroll
+      for (int k = 0; k < S; ++k)
+        if (m >> k & 1) {
+          sub[cnt++] = j[k];
+          svol *= static_cast<uint32_t>(e[k]);
+        }
+      const LayoutDev& Lq = P.lay[cnt - 1];
+      const double* src = P.lower[cnt - 1] + Lq.offset[rank_dev(Lq, sub, cnt)];
+      for (uint32_t t = threadIdx.x; t < svol; t += blockDim.x) sfac[soff + t] = src[t];
+      soff += svol;
+    }
+    __syncthreads();
+  }
+
+  // phase 1: canonical entries
+  for (uint32_t pos = threadIdx.x; pos < vol; pos += blockDim.x) {
+    int o[S];
+    decode<S>(pos, e, o);
+    if (!canonical<S>(j, o)) continue;
+    double f[NM];
+#pragma unroll
+    for (int m = 1; m < NM; ++m) {
+      uint32_t a = 0;
+#pragma unroll
+      for (int k = 0; k < S; ++k)
+        if (m >> k & 1) a += static_cast<uint32_t>(o[k]) * sstride[m][k];
+      if (STAGED)
+        f[m] = sfac[sbase[m] + a];
+      else
+        f[m] = P.lower[popcount_c(m) - 1][sbase[m] + a];
+    }
+    const double corr = partition_correction<S>(f);
+    P.c[boff + pos] = __dsub_rn(P.m[boff + pos], corr);
+  }
+  __syncthreads();  // canonical entries of this block are visible to the CTA
+
+  // phase 2: copies + the block's sum of squares (fixed order)
+  double part = 0.0;
+  for (uint32_t pos = threadIdx.x; pos < vol; pos += blockDim.x) {
+    int o[S];
+    decode<S>(pos, e, o);
+    double v;
+    if (canonical<S>(j, o)) {
+      v = P.c[boff + pos];
+    } else {
+      v = P.c[boff + source_of<S>(j, o, e)];
+      P.c[boff + pos] = v;
+    }
+    part = __fma_rn(v, v, part);
+  }
+  for (int s = 16; s > 0; s >>= 1) part = __dadd_rn(part, __shfl_down_sync(0xffffffffu, part, s));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) s = __dadd_rn(s, red[w]);
+    P.partial[blockIdx.x] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+template <int S>
+__global__ void __launch_bounds__(128) moment_lower_kernel(const LowerParams P) {
+  const uint64_t el = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (el >= P.count) return;
+  const LowerElem E = P.elems[el];
+  const int n = P.n;
+  int idx[S];
+#pragma unroll
+  for (int k = 0; k < S; ++k) idx[k] = E.idx[k];
+  double res[2] = {0.0, 0.0};
+  for (int pass = 0; pass < P.npass; ++pass) {
+    const RowSource src = P.src[pass];
+    double acc = 0.0;
+    // rows in order; the two segments of the ring in arrival order
+    for (int seg = 0; seg < 2; ++seg) {
+      const double* base = seg == 0 ? src.seg0 : src.seg1;
+      const uint32_t len = seg == 0 ? src.len0 : src.len1;
+      uint32_t k = 0;
+      for (; k + 4 <= len; k += 4) {
+        double p[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double* row = base + static_cast<size_t>(k + u) * n;
+          double v = __ldg(row + idx[0]);
+#pragma unroll
+          for (int t = 1; t < S; ++t) v = __dmul_rn(v, __ldg(row + idx[t]));
+          p[u] = v;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc = __dadd_rn(acc, p[u]);
+      }
+      for (; k < len; ++k) {
+        const double* row = base + static_cast<size_t>(k) * n;
+        double v = __ldg(row + idx[0]);
+#pragma unroll
+        for (int t = 1; t < S; ++t) v = __dmul_rn(v, __ldg(row + idx[t]));
+        acc = __dadd_rn(acc, v);
+      }
+    }
+    res[pass] = __dmul_rn(acc, P.inv);
+  }
+  // every stored copy: distinct permutations of the offsets within runs
+  const int b = P.b;
+  int j[S], o[S], e[S];
+#pragma unroll
+  for (int k = 0; k < S; ++k) {
+    j[k] = idx[k] / b;
+    o[k] = idx[k] - j[k] * b;
+    e[k] = ext_of(j[k], n, b);
+  }
+  const bool update = P.npass == 2;
+  const double delta = update ? __dsub_rn(res[0], res[1]) : 0.0;
+  double* m = P.m;
+  bool runs = false;
+#pragma unroll
+  for (int k = 1; k < S; ++k) runs |= j[k] == j[k - 1];
+  for (;;) {
+    uint32_t off = 0;
+#pragma unroll
+    for (int k = 0; k < S; ++k) off = off * static_cast<uint32_t>(e[k]) + static_cast<uint32_t>(o[k]);
+    double* p = m + E.blk_off + off;
+    *p = update ? __fma_rn(P.c, delta, *p) : res[0];
+    if (!runs) break;
+    // next distinct permutation within runs (odometer over runs, from the last)
+    int k = S - 1;
+    bool advanced = false;
+    while (k >= 0 && !advanced) {
+      int s0 = k;
+      while (s0 > 0 && j[s0 - 1] == j[k]) --s0;  // run [s0, k]
+      // std::next_permutation on o[s0..k]
+      int i = k - 1;
+      while (i >= s0 && o[i] >= o[i + 1]) --i;
+      if (i >= s0) {
+        int t = k;
+        while (o[t] <= o[i]) --t;
+        int tmp = o[i];
+        o[i] = o[t];
+        o[t] = tmp;
+        for (int l = i + 1, r = k; l < r; ++l, --r) {
+          tmp = o[l];
+          o[l] = o[r];
+          o[r] = tmp;
+        }
+        advanced = true;
+      } else {
+        for (int l = s0, r = k; l < r; ++l, --r) {
+          const int tmp = o[l];
+          o[l] = o[r];
+          o[r] = tmp;
+        }
+        k = s0 - 1;
+      }
+    }
+    if (!advanced) break;
+  }
+}
+
+}  // namespace
+
+size_t moms2cums_stage_bytes(int S, int n, int b) {
+  // upper bound: all sub-blocks full (b^|m| doubles per subset)
+  size_t tot = 0;
+  for (int m = 1; m < (1 << S) - 1; ++m) {
+    size_t v = 1;
+    for (int k = 0; k < S; ++k)
+      if (m >> k & 1) v *= static_cast<size_t>(b < n ? b : n);
+    tot += v;
+  }
+  return tot * sizeof(double);
+}
+
+void launch_moms2cums_v2(int S, const M2CParams& p, uint64_t nblocks, cudaStream_t st) {
+  if (nblocks == 0) return;
+  const unsigned g = static_cast<unsigned>(nblocks);
+  const size_t sm = moms2cums_stage_bytes(S, p.n, p.b);
+  const bool staged = sm <= 160 * 1024;
+  switch (S) {
+#define CSB_M2C(SS)                                                                                   \
+  case SS:                                                                                            \
+    if (staged) {                                                                                     \
+      CSB_CUDA(cudaFuncSetAttribute(moms2cums_v2<SS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                    static_cast<int>(sm)));                                           \
+      moms2cums_v2<SS, true><<<g, 256, sm, st>>>(p);                                                  \
+    } else {                                                                                          \
+      moms2cums_v2<SS, false><<<g, 256, 0, st>>>(p);                                                  \
+    }                                                                                                 \
+    break;
+    CSB_M2C(2) CSB_M2C(3) CSB_M2C(4) CSB_M2C(5) CSB_M2C(6)
+#undef CSB_M2C
+    default: fail(CSB_EINVAL, "moms2cums: device path supports orders <= 6");
+  }
+  CSB_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+void launch_moment_lower(int S, const LowerParams& p, cudaStream_t st) {
+  if (!p.count) return;
+  const unsigned g = static_cast<unsigned>((p.count + 127) / 128);
+  switch (S) {
+#define CSB_LOW(SS) \
+  case SS: moment_lower_kernel<SS><<<g, 128, 0, st>>>(p); break;
+    CSB_LOW(1) CSB_LOW(2) CSB_LOW(3) CSB_LOW(4) CSB_LOW(5) CSB_LOW(6)
+#undef CSB_LOW
+    default: fail(CSB_EINVAL, "moment_lower: order out of range");
+  }
+  CSB_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+}  // namespace csb

@@ -51,6 +51,23 @@ struct M2CParams {
   double* partial = nullptr;        // per block: sum over stored entries of v*v
 };
 
+// One canonical element of a low order (S <= d-2): indices and the offset
+// of its block in M_S.
+struct LowerElem {
+  uint16_t idx[8];
+  uint64_t blk_off;
+};
+
+struct LowerParams {
+  RowSource src[2];
+  int npass = 1;
+  int n = 0, b = 0;
+  const LowerElem* elems = nullptr;
+  uint64_t count = 0;
+  double* m = nullptr;
+  double c = 0.0, inv = 1.0;
+};
+
 struct NormParams {
   const double* partial[kMaxOrder];  // per order, nblocks each
   const double* mult[kMaxOrder];     // per order block multiplicities (as double)
@@ -64,6 +81,8 @@ struct NormParams {
 
 void launch_moment_pair(const MomParams& p, int ntiles, bool top_fma, cudaStream_t st);
 void launch_moms2cums(int S, const M2CParams& p, uint64_t nblocks, cudaStream_t st);
+void launch_moms2cums_v2(int S, const M2CParams& p, uint64_t nblocks, cudaStream_t st);
+void launch_moment_lower(int S, const LowerParams& p, cudaStream_t st);
 void launch_copy_c1(const double* m1, double* c1, double* partial, const LayoutDev& lay,
                     uint64_t nblocks, uint64_t stored, cudaStream_t st);
 void launch_norm_finalize(const NormParams& p, cudaStream_t st);

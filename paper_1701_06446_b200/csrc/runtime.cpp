@@ -51,6 +51,7 @@ struct Device {
   std::mutex mu;
   std::map<std::tuple<int, int, int>, std::shared_ptr<DevLayout>> layouts;
   std::map<std::tuple<int, int, int, int>, std::shared_ptr<MomentPlan>> plans;
+  std::map<std::tuple<int, int, int>, std::shared_ptr<DevBuf<LowerElem>>> lower;
 };
 
 std::mutex g_dev_mu;
@@ -157,6 +158,36 @@ struct ProfScope {
   }
 };
 
+// Canonical elements of order s (lexicographic) with the offset of their
+// block in M_s, for the low-order kernel.
+std::shared_ptr<DevBuf<LowerElem>> get_lower_elems(Device& dev, int s, int n, int b, const Layout& L) {
+  std::lock_guard<std::mutex> lk(dev.mu);
+  auto& slot = dev.lower[{s, n, b}];
+  if (!slot) {
+    std::vector<LowerElem> v;
+    v.reserve(multiset_count(n, s));
+    int t[8] = {0}, j[8];
+    for (;;) {
+      LowerElem e{};
+      for (int k = 0; k < s; ++k) {
+        e.idx[k] = static_cast<uint16_t>(t[k]);
+        j[k] = t[k] / b;
+      }
+      e.blk_off = L.offset[L.rank(j)];
+      v.push_back(e);
+      int k = s - 1;
+      while (k >= 0 && t[k] == n - 1) --k;
+      if (k < 0) break;
+      const int val = t[k] + 1;
+      for (int l = k; l < s; ++l) t[l] = val;
+    }
+    auto buf = std::make_shared<DevBuf<LowerElem>>(v.size());
+    CSB_CUDA(cudaMemcpy(buf->ptr, v.data(), buf->bytes(), cudaMemcpyHostToDevice));
+    slot = buf;
+  }
+  return slot;
+}
+
 }  // namespace
 
 void ensure_device() {
@@ -247,13 +278,17 @@ const bool g_use_dmma = [] {
 // Orders are processed as pairs (S, S-1): (d, d-1), (d-2, d-3), ... with a
 // lone order 1 when d is odd.  Only the pair topped by d uses the fused
 // multiply-add of the reference's deepest loop (moments.cpp:47).
+// Orders are processed as: the top pair (S, S-1) with S = d -- the fused
+// multiply-add of the reference's deepest loop (moments.cpp:47) on the
+// FP64 tensor cores when possible -- and every order <= d-2 by the
+// element-parallel low-order kernel (plain product + add, moments.cpp:55-57).
 void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, double c,
                  cudaStream_t st, int only_order = 0) {
   Device& dev = *m->dev;
   const int d = m->d;
-  for (int S = d; S >= 1; S -= 2) {
-    if (only_order && S != only_order) continue;
-    const bool top = S == (only_order ? only_order : d);
+  const int S = only_order ? only_order : d;
+  Scratch& sc = g_scratch[dev.id];
+  {
     MomParams p;
     p.src[0] = src[0];
     p.src[1] = src[1];
@@ -267,15 +302,15 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
     p.c = c;
     p.inv = 1.0 / static_cast<double>(K);
     // the top pair runs on the FP64 tensor cores when the rows allow TMA
-    // bulk copies; lower pairs (unfused multiply-add) stay on DFMA/DMUL
-    const bool use_dmma = top && g_use_dmma && dmma_supported(p);
+    // bulk copies; otherwise on the DFMA kernel
+    const bool use_dmma = g_use_dmma && dmma_supported(p);
     auto plan = get_plan(dev, S, m->n, m->b, use_dmma);
     p.rows = plan->d_rows.ptr;
     p.tiles = plan->d_tiles.ptr;
     p.groups = plan->d_groups.ptr;
     const uint64_t ntiles = plan->tiles.size();
-    if (npass == 2 || use_dmma) p.scratch = g_scratch[dev.id].get(ntiles * plan->scratch_per_tile);
-    Scratch& sc = g_scratch[dev.id];
+    if (npass == 2 || use_dmma) p.scratch = sc.get(ntiles * plan->scratch_per_tile);
+    ProfScope ps("moment_top", st);
     if (use_dmma) {
       p.flags = sc.get_flags(ntiles);
       p.zeros = sc.get_zeros(32ull * m->n);
@@ -283,9 +318,6 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
         p.dtop = sc.get_delta(sc.dtop, m->lay[S - 1]->host.stored);
         if (p.low) p.dlow = sc.get_delta(sc.dlow, m->lay[S - 2]->host.stored);
       }
-    }
-    ProfScope ps(top ? "moment_top" : "moment_low", st);
-    if (use_dmma) {
       launch_moment_top_dmma(p, static_cast<int>(ntiles), st);
       const auto& LT = m->lay[S - 1];
       launch_mirror(S, p.top, p.dtop, LT->view(), LT->diag.ptr, LT->ndiag, m->n, m->b, npass == 2, c, st);
@@ -293,8 +325,26 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
         const auto& LL = m->lay[S - 2];
         launch_mirror(S - 1, p.low, p.dlow, LL->view(), LL->diag.ptr, LL->ndiag, m->n, m->b, npass == 2, c, st);
       }
-    } else
-      launch_moment_pair(p, static_cast<int>(ntiles), top, st);
+    } else {
+      launch_moment_pair(p, static_cast<int>(ntiles), true, st);
+    }
+  }
+  if (only_order) return;
+  ProfScope ps("moment_low", st);
+  for (int s = 1; s <= d - 2; ++s) {
+    auto el = get_lower_elems(dev, s, m->n, m->b, m->lay[s - 1]->host);
+    LowerParams lp;
+    lp.src[0] = src[0];
+    lp.src[1] = src[1];
+    lp.npass = npass;
+    lp.n = m->n;
+    lp.b = m->b;
+    lp.elems = el->ptr;
+    lp.count = el->count;
+    lp.m = m->data[s - 1].ptr;
+    lp.c = c;
+    lp.inv = 1.0 / static_cast<double>(K);
+    launch_moment_lower(s, lp, st);
   }
 }
 
@@ -331,7 +381,7 @@ void run_moms2cums(const csb_series* m, csb_series* c, NormScratch& ns, cudaStre
     p.b = m->b;
     p.blk0 = 0;
     p.partial = ns.partial[s - 1].ptr;
-    launch_moms2cums(s, p, m->lay[s - 1]->host.nblocks, st);
+    launch_moms2cums_v2(s, p, m->lay[s - 1]->host.nblocks, st);
   }
   c->window_len = m->window_len;
 }
