@@ -195,11 +195,14 @@ __global__ void __launch_bounds__(256) moms2cums_v2(const M2CParams P) {
 }
 
 // ---------------------------------------------------------------------------
+constexpr int LOW_ROWS = 32;  // rows per shared-memory chunk
+
 template <int S>
 __global__ void __launch_bounds__(128) moment_lower_kernel(const LowerParams P) {
+  extern __shared__ __align__(16) double xrows[];  // LOW_ROWS x n
   const uint64_t el = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  if (el >= P.count) return;
-  const LowerElem E = P.elems[el];
+  const bool live = el < P.count;
+  const LowerElem E = P.elems[live ? el : 0];
   const int n = P.n;
   int idx[S];
 #pragma unroll
@@ -207,35 +210,32 @@ __global__ void __launch_bounds__(128) moment_lower_kernel(const LowerParams P) 
   double res[2] = {0.0, 0.0};
   for (int pass = 0; pass < P.npass; ++pass) {
     const RowSource src = P.src[pass];
+    const uint32_t K = src.len0 + src.len1;
     double acc = 0.0;
-    // rows in order; the two segments of the ring in arrival order
-    for (int seg = 0; seg < 2; ++seg) {
-      const double* base = seg == 0 ? src.seg0 : src.seg1;
-      const uint32_t len = seg == 0 ? src.len0 : src.len1;
-      uint32_t k = 0;
-      for (; k + 4 <= len; k += 4) {
-        double p[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const double* row = base + static_cast<size_t>(k + u) * n;
-          double v = __ldg(row + idx[0]);
-#pragma unroll
-          for (int t = 1; t < S; ++t) v = __dmul_rn(v, __ldg(row + idx[t]));
-          p[u] = v;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) acc = __dadd_rn(acc, p[u]);
+    // rows stream through shared memory in chunks (coalesced loads), each
+    // thread folds its element's products in row order
+    for (uint32_t k0 = 0; k0 < K; k0 += LOW_ROWS) {
+      const uint32_t kc = min(static_cast<uint32_t>(LOW_ROWS), K - k0);
+      __syncthreads();
+      for (uint32_t t = threadIdx.x; t < kc * static_cast<uint32_t>(n); t += blockDim.x) {
+        const uint32_t r = t / n, c = t - r * n;
+        const uint32_t k = k0 + r;
+        const double* row = k < src.len0 ? src.seg0 + static_cast<size_t>(k) * n
+                                         : src.seg1 + static_cast<size_t>(k - src.len0) * n;
+        xrows[t] = __ldg(row + c);
       }
-      for (; k < len; ++k) {
-        const double* row = base + static_cast<size_t>(k) * n;
-        double v = __ldg(row + idx[0]);
+      __syncthreads();
+      for (uint32_t r = 0; r < kc; ++r) {
+        const double* row = xrows + r * n;
+        double v = row[idx[0]];
 #pragma unroll
-        for (int t = 1; t < S; ++t) v = __dmul_rn(v, __ldg(row + idx[t]));
+        for (int t = 1; t < S; ++t) v = __dmul_rn(v, row[idx[t]]);
         acc = __dadd_rn(acc, v);
       }
     }
     res[pass] = __dmul_rn(acc, P.inv);
   }
+  if (!live) return;
   // every stored copy: distinct permutations of the offsets within runs
   const int b = P.b;
   int j[S], o[S], e[S];
@@ -333,9 +333,14 @@ void launch_moms2cums_v2(int S, const M2CParams& p, uint64_t nblocks, cudaStream
 void launch_moment_lower(int S, const LowerParams& p, cudaStream_t st) {
   if (!p.count) return;
   const unsigned g = static_cast<unsigned>((p.count + 127) / 128);
+  const size_t sm = sizeof(double) * LOW_ROWS * p.n;
   switch (S) {
-#define CSB_LOW(SS) \
-  case SS: moment_lower_kernel<SS><<<g, 128, 0, st>>>(p); break;
+#define CSB_LOW(SS)                                                                                     \
+  case SS:                                                                                              \
+    CSB_CUDA(cudaFuncSetAttribute(moment_lower_kernel<SS>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                  static_cast<int>(sm)));                                               \
+    moment_lower_kernel<SS><<<g, 128, sm, st>>>(p);                                                     \
+    break;
     CSB_LOW(1) CSB_LOW(2) CSB_LOW(3) CSB_LOW(4) CSB_LOW(5) CSB_LOW(6)
 #undef CSB_LOW
     default: fail(CSB_EINVAL, "moment_lower: order out of range");

@@ -48,6 +48,8 @@ struct DevLayout {
 struct Device {
   int id = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;  // low-order moments overlap the top kernel
+  cudaEvent_t fork = nullptr, join = nullptr;
   std::mutex mu;
   std::map<std::tuple<int, int, int>, std::shared_ptr<DevLayout>> layouts;
   std::map<std::tuple<int, int, int, int>, std::shared_ptr<MomentPlan>> plans;
@@ -72,6 +74,9 @@ Device& device() {
     slot = std::make_unique<Device>();
     slot->id = id;
     CSB_CUDA(cudaStreamCreateWithFlags(&slot->stream, cudaStreamNonBlocking));
+    CSB_CUDA(cudaStreamCreateWithFlags(&slot->side, cudaStreamNonBlocking));
+    CSB_CUDA(cudaEventCreateWithFlags(&slot->fork, cudaEventDisableTiming));
+    CSB_CUDA(cudaEventCreateWithFlags(&slot->join, cudaEventDisableTiming));
   }
   return *slot;
 }
@@ -288,6 +293,29 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
   const int d = m->d;
   const int S = only_order ? only_order : d;
   Scratch& sc = g_scratch[dev.id];
+  const bool lower = !only_order && d > 2;
+  if (lower) {
+    // orders <= d-2 on the side stream, concurrently with the top pair
+    CSB_CUDA(cudaEventRecord(dev.fork, st));
+    CSB_CUDA(cudaStreamWaitEvent(dev.side, dev.fork, 0));
+    ProfScope ps("moment_low", dev.side);
+    for (int s = 1; s <= d - 2; ++s) {
+      auto el = get_lower_elems(dev, s, m->n, m->b, m->lay[s - 1]->host);
+      LowerParams lp;
+      lp.src[0] = src[0];
+      lp.src[1] = src[1];
+      lp.npass = npass;
+      lp.n = m->n;
+      lp.b = m->b;
+      lp.elems = el->ptr;
+      lp.count = el->count;
+      lp.m = m->data[s - 1].ptr;
+      lp.c = c;
+      lp.inv = 1.0 / static_cast<double>(K);
+      launch_moment_lower(s, lp, dev.side);
+    }
+    CSB_CUDA(cudaEventRecord(dev.join, dev.side));
+  }
   {
     MomParams p;
     p.src[0] = src[0];
@@ -329,23 +357,7 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
       launch_moment_pair(p, static_cast<int>(ntiles), true, st);
     }
   }
-  if (only_order) return;
-  ProfScope ps("moment_low", st);
-  for (int s = 1; s <= d - 2; ++s) {
-    auto el = get_lower_elems(dev, s, m->n, m->b, m->lay[s - 1]->host);
-    LowerParams lp;
-    lp.src[0] = src[0];
-    lp.src[1] = src[1];
-    lp.npass = npass;
-    lp.n = m->n;
-    lp.b = m->b;
-    lp.elems = el->ptr;
-    lp.count = el->count;
-    lp.m = m->data[s - 1].ptr;
-    lp.c = c;
-    lp.inv = 1.0 / static_cast<double>(K);
-    launch_moment_lower(s, lp, st);
-  }
+  if (lower) CSB_CUDA(cudaStreamWaitEvent(st, dev.join, 0));
 }
 
 void check_batch(uint64_t rows, uint64_t cols, const char* what) {
