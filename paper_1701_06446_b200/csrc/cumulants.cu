@@ -195,11 +195,27 @@ __global__ void __launch_bounds__(256) moms2cums_v2(const M2CParams P) {
 }
 
 // ---------------------------------------------------------------------------
-constexpr int LOW_ROWS = 32;  // rows per shared-memory chunk
+
+// rows in flight per thread (register double buffer)
+template <int S>
+constexpr int low_unroll() { return S <= 2 ? 16 : S == 3 ? 8 : 4; }
+
+template <int S, int LOW_UNROLL = low_unroll<S>()>
+__device__ __forceinline__ void low_load(const RowSource& src, uint32_t k0, uint32_t K, int n, const int (&idx)[S],
+                                         double (&v)[LOW_UNROLL][S]) {
+#pragma unroll
+  for (int u = 0; u < LOW_UNROLL; ++u) {
+    const uint32_t k = min(k0 + u, K - 1);
+    const double* row = k < src.len0 ? src.seg0 + static_cast<size_t>(k) * n
+                                     : src.seg1 + static_cast<size_t>(k - src.len0) * n;
+#pragma unroll
+    for (int t = 0; t < S; ++t) v[u][t] = __ldg(row + idx[t]);
+  }
+}
 
 template <int S>
 __global__ void __launch_bounds__(128) moment_lower_kernel(const LowerParams P) {
-  extern __shared__ __align__(16) double xrows[];  // LOW_ROWS x n
+  constexpr int LOW_UNROLL = low_unroll<S>();
   const uint64_t el = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   const bool live = el < P.count;
   const LowerElem E = P.elems[live ? el : 0];
@@ -212,26 +228,23 @@ __global__ void __launch_bounds__(128) moment_lower_kernel(const LowerParams P) 
     const RowSource src = P.src[pass];
     const uint32_t K = src.len0 + src.len1;
     double acc = 0.0;
-    // rows stream through shared memory in chunks (coalesced loads), each
-    // thread folds its element's products in row order
-    for (uint32_t k0 = 0; k0 < K; k0 += LOW_ROWS) {
-      const uint32_t kc = min(static_cast<uint32_t>(LOW_ROWS), K - k0);
-      __syncthreads();
-      for (uint32_t t = threadIdx.x; t < kc * static_cast<uint32_t>(n); t += blockDim.x) {
-        const uint32_t r = t / n, c = t - r * n;
-        const uint32_t k = k0 + r;
-        const double* row = k < src.len0 ? src.seg0 + static_cast<size_t>(k) * n
-                                         : src.seg1 + static_cast<size_t>(k - src.len0) * n;
-        xrows[t] = __ldg(row + c);
-      }
-      __syncthreads();
-      for (uint32_t r = 0; r < kc; ++r) {
-        const double* row = xrows + r * n;
-        double v = row[idx[0]];
+    // rows in order; the next LOW_UNROLL rows are loaded while the current
+    // ones are folded (plain product, then add: moments.cpp:55-57)
+    double cur[LOW_UNROLL][S], nxt[LOW_UNROLL][S];
+    low_load<S>(src, 0, K, n, idx, cur);
+    for (uint32_t k0 = 0; k0 < K; k0 += LOW_UNROLL) {
+      if (k0 + LOW_UNROLL < K) low_load<S>(src, k0 + LOW_UNROLL, K, n, idx, nxt);
 #pragma unroll
-        for (int t = 1; t < S; ++t) v = __dmul_rn(v, row[idx[t]]);
-        acc = __dadd_rn(acc, v);
+      for (int u = 0; u < LOW_UNROLL; ++u) {
+        double v = cur[u][0];
+#pragma unroll
+        for (int t = 1; t < S; ++t) v = __dmul_rn(v, cur[u][t]);
+        if (k0 + u < K) acc = __dadd_rn(acc, v);
       }
+#pragma unroll
+      for (int u = 0; u < LOW_UNROLL; ++u)
+#pragma unroll
+        for (int t = 0; t < S; ++t) cur[u][t] = nxt[u][t];
     }
     res[pass] = __dmul_rn(acc, P.inv);
   }
@@ -333,14 +346,9 @@ void launch_moms2cums_v2(int S, const M2CParams& p, uint64_t nblocks, cudaStream
 void launch_moment_lower(int S, const LowerParams& p, cudaStream_t st) {
   if (!p.count) return;
   const unsigned g = static_cast<unsigned>((p.count + 127) / 128);
-  const size_t sm = sizeof(double) * LOW_ROWS * p.n;
   switch (S) {
-#define CSB_LOW(SS)                                                                                     \
-  case SS:                                                                                              \
-    CSB_CUDA(cudaFuncSetAttribute(moment_lower_kernel<SS>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                  static_cast<int>(sm)));                                               \
-    moment_lower_kernel<SS><<<g, 128, sm, st>>>(p);                                                     \
-    break;
+#define CSB_LOW(SS) \
+  case SS: moment_lower_kernel<SS><<<g, 128, 0, st>>>(p); break;
     CSB_LOW(1) CSB_LOW(2) CSB_LOW(3) CSB_LOW(4) CSB_LOW(5) CSB_LOW(6)
 #undef CSB_LOW
     default: fail(CSB_EINVAL, "moment_lower: order out of range");
