@@ -260,7 +260,6 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
       }
   };
 
-  pump(0);
   bool lowpend = false;  // previous step's A values wait in lowbuf[1 - cur]
   int lb = 0;
   // one step: loads of the next step, DMMAs of this one, row sums, products
@@ -280,23 +279,35 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
     }
     if (has_next) finish<LM1, NC>(nxt, false);
   };
+  // The step stream is continuous across chunks: the last step of chunk c
+  // loads the first operands of chunk c + 1, so the pipeline never drains.
+  auto stage_ptr = [&](uint32_t c) {
+    return xs + (c % STAGES) * stage_elems + static_cast<size_t>(q) * n;
+  };
+  Raw<LM1, NC> o0, o1;
+  if (warp == 0) pump(0);
+  __syncwarp();
+  mbar_wait(full + 0, 0u);
+  load_raw<LM1, NC>(o0, stage_ptr(0), h8, col0, r, pidx);
+  finish<LM1, NC>(o0, false);
   for (uint32_t c = 0; c < chunks; ++c) {
-    const uint32_t st = c % STAGES;
-    if (warp == 0) pump(c);
-    __syncwarp();
-    mbar_wait(full + st, (c / STAGES) & 1u);
-    const double* xst = xs + st * stage_elems + static_cast<size_t>(q) * n;
-    Raw<LM1, NC> o0, o1;
-    load_raw<LM1, NC>(o0, xst, h8, col0, r, pidx);
-    finish<LM1, NC>(o0, false);
+    const double* xst = stage_ptr(c);
 #pragma unroll 1
-    for (int t = 0; t < KC / 4; t += 2) {
+    for (int t = 0; t < KC / 4 - 2; t += 2) {
       step(o0, o1, xst + (4 * t + 4) * n, true);
-      step(o1, o0, xst + (4 * t + 8) * n, t + 2 < KC / 4);
+      step(o1, o0, xst + (4 * t + 8) * n, true);
     }
-    // every lane has consumed its rows of this stage
+    step(o0, o1, xst + (KC - 4) * n, true);
+    // every lane has loaded its rows of this stage: release it
     __syncwarp();
-    if (lane == 0) mbar_arrive(empty + st);
+    if (lane == 0) mbar_arrive(empty + (c % STAGES));
+    const bool more = c + 1 < chunks;
+    if (more) {
+      if (warp == 0) pump(c + 1);
+      __syncwarp();
+      mbar_wait(full + ((c + 1) % STAGES), ((c + 1) / STAGES) & 1u);
+    }
+    step(o1, o0, more ? stage_ptr(c + 1) : xst, more);
     if (warp == 0) pump(0);  // refill without blocking
   }
   if (do_low && lowpend) {
