@@ -34,8 +34,12 @@ namespace csb {
 
 namespace {
 
-constexpr int WARPS = 4;  // MMA warps; lane 0 of warp 0 also drives the TMA
+constexpr int CWARPS = 4;           // DMMA consumer warps
+constexpr int WARPS = 2 * CWARPS;   // + one producer warp per consumer
 constexpr int THREADS = WARPS * 32;
+constexpr int HSTEPS = 4;           // k4 steps per A-ring slot (16 rows)
+constexpr int ASTRIDE = 10;         // doubles per (r, q) entry: 8 used, bank-conflict free
+constexpr int ASLOT = HSTEPS * 32 * ASTRIDE;
 constexpr int STAGES = 3;
 constexpr int KC = 32;        // data rows per stage
 
@@ -118,231 +122,223 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // are loaded from shared memory and multiplied out while step s's DMMAs
 // occupy the FP64 tensor pipe.
 
-template <int LM1, int NC>
-struct Raw {
-  double p[LM1 > 0 ? LM1 : 1];  // x[pi_t] of this lane's group
-  double a[8];                  // x[8h + g]
-  double b[NC];                 // x[col0 + 8c + r]
-};
-
-template <int LM1, int NC>
-__device__ __forceinline__ void load_raw(Raw<LM1, NC>& w, const double* __restrict__ xr, int h8, int col0,
-                                         int r, const int* pidx) {
-#pragma unroll
-  for (int t = 0; t < LM1; ++t) w.p[t] = xr[pidx[t]];
-  const double2* xa = reinterpret_cast<const double2*>(xr + h8);
-#pragma unroll
-  for (int s = 0; s < 4; ++s) {
-    const double2 v = xa[s];
-    w.a[2 * s] = v.x;
-    w.a[2 * s + 1] = v.y;
-  }
-#pragma unroll
-  for (int c = 0; c < NC; ++c) w.b[c] = xr[col0 + 8 * c + r];
-}
-
-// A = x[pi_1] * ... * x[pi_{L-1}] * x[8h + g] in the reference's order.
-// Rows with g < lo (i_L < i_{L-1}) and padding groups are computed but never
-// stored, so no masking is needed; data rows past the end of the pass are
-// zeroed (zero == true) so they contribute exact zeros.
-template <int LM1, int NC>
-__device__ __forceinline__ void finish(Raw<LM1, NC>& w, bool zero) {
-  if (LM1 > 0) {
-    double P = w.p[0];
-#pragma unroll
-    for (int t = 1; t < LM1; ++t) P = __dmul_rn(P, w.p[t]);
-#pragma unroll
-    for (int g = 0; g < 8; ++g) w.a[g] = __dmul_rn(P, w.a[g]);  // 1.0 * x == x: none for L == 1
-  }
-  if (zero) {
-#pragma unroll
-    for (int g = 0; g < 8; ++g) w.a[g] = 0.0;
-#pragma unroll
-    for (int c = 0; c < NC; ++c) w.b[c] = 0.0;
-  }
-}
-
+// Warp-specialized tile: warps 0..CWARPS-1 are DMMA consumers, warps
+// CWARPS..2*CWARPS-1 their producers.  A DMMA stalls its warp for 15 cycles
+// (SASS control bits), so a warp cannot overlap its own FP64 products and
+// row sums with its DMMAs; split across warps, the products, the order-L
+// row sums and the DMMAs share the FP64 pipe of the SM sub-partition.
+//
+// Producer lane (r, gp) of producer warp w: rows (pi_r, 8h + 2gp + e),
+// e = 0, 1, of the consumer warp's group r.  Per data row k it forms
+// P = x[pi_1] ... x[pi_{L-1}] and the two products P * x[8h + 2gp + e]
+// (moments.cpp:55,71), adds them to its row sums in row order, and stores
+// them to the A ring in fragment order:
+//   aring[w][slot][t][(r * 4 + q) * ASTRIDE + g],  k = 16 half + 4 t + q.
+// Consumer lane (r, q): fragment g of step t is aring[...][t][(r*4+q)*10+g]
+// (4 x LDS.128), B fragment c is x[k = 4 t + q][col0 + 8c + r].
 template <int LM1, int NC>
 __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile, int pass, double* xs,
-                                         uint64_t* full, uint64_t* empty, double* lowbufs, uint32_t* flag_smem) {
+                                         double* arings, uint64_t* xfull, uint64_t* xempty, uint64_t* afull,
+                                         uint64_t* aempty, uint32_t* flag_smem) {
   constexpr int L = LM1 + 1;
   const int n = P.n, b = P.b;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int q = lane & 3, r = lane >> 2;
+  const bool producer = warp >= CWARPS;
+  const int pw = producer ? warp - CWARPS : warp;  // pair index
+  const int r = lane >> 2, q4 = lane & 3;          // (r, q) consumer / (r, gp) producer
   const int h8 = static_cast<int>(tile.J) * 8;
   const int col0 = static_cast<int>(tile.col0);
   const bool do_low = (P.low != nullptr) && tile.low;
-  double* lowbuf = lowbufs + warp * (2 * 4 * 66);  // double-buffered 4 x 66
   const size_t stage_elems = static_cast<size_t>(KC) * n;
   const uint32_t K = P.K;
   const uint32_t chunks = (K + KC - 1) / KC;
   const RowSource& src = P.src[pass];
+  double* aring = arings + static_cast<size_t>(pw) * 2 * ASLOT;
 
-  // ---- TMA producer: lane 0 of warp 0 ----
-  // Chunk c goes into stage c % STAGES once every warp has released chunk
-  // c - STAGES.  The producer polls without blocking and blocks only for the
-  // chunk warp 0 itself needs next.
+  // ---- TMA producer: lane 0 of the first producer warp ----
   uint32_t next_issue = 0;
   auto pump = [&](uint32_t needed) {
-    if (threadIdx.x != 0) return;
+    if (threadIdx.x != CWARPS * 32) return;
     while (next_issue < chunks) {
       const uint32_t i = next_issue;
       const uint32_t st = i % STAGES;
       if (i >= STAGES) {
         const uint32_t par = ((i / STAGES) - 1) & 1u;
-        if (!mbar_test(empty + st, par)) {
+        if (!mbar_test(xempty + st, par)) {
           if (i > needed) break;
-          mbar_wait(empty + st, par);
+          mbar_wait(xempty + st, par);
         }
       }
       const uint32_t a0 = i * KC;
       const uint32_t kc = min(static_cast<uint32_t>(KC), K - a0);
       double* dst = xs + st * stage_elems;
       const uint32_t rb = static_cast<uint32_t>(n) * 8u;
-      mbar_expect_tx(full + st, static_cast<uint32_t>(KC) * rb);
-      // rows past the end of the pass are zero rows: A = B = 0 adds exact
-      // zeros, so the k loop never needs masking
+      mbar_expect_tx(xfull + st, static_cast<uint32_t>(KC) * rb);
+      // rows past the end of the pass are zero rows: they add exact zeros
       if (kc < static_cast<uint32_t>(KC))
-        bulk_g2s(dst + static_cast<size_t>(kc) * n, P.zeros, (KC - kc) * rb, full + st);
-      // rows [a0, a0 + kc) are contiguous except across the ring's wrap
+        bulk_g2s(dst + static_cast<size_t>(kc) * n, P.zeros, (KC - kc) * rb, xfull + st);
       if (a0 + kc <= src.len0 || a0 >= src.len0) {
-        bulk_g2s(dst, row_ptr(src, a0, n), kc * rb, full + st);
-      } else {
+        bulk_g2s(dst, row_ptr(src, a0, n), kc * rb, xfull + st);
+      } else {  // across the ring's wrap
         const uint32_t k1 = src.len0 - a0;
-        bulk_g2s(dst, row_ptr(src, a0, n), k1 * rb, full + st);
-        bulk_g2s(dst + static_cast<size_t>(k1) * n, src.seg1, (kc - k1) * rb, full + st);
+        bulk_g2s(dst, row_ptr(src, a0, n), k1 * rb, xfull + st);
+        bulk_g2s(dst + static_cast<size_t>(k1) * n, src.seg1, (kc - k1) * rb, xfull + st);
       }
       ++next_issue;
     }
   };
 
-  const int gl = warp * 8 + r;  // group slot in the tile
+  const int gl = pw * 8 + r;  // group slot in the tile
   const bool gvalid = gl < static_cast<int>(tile.nrows);
   const uint32_t gi = tile.row0 + (gvalid ? gl : 0);
   const DmmaGroup grp = P.groups[gi];
-  int pidx[LM1 > 0 ? LM1 : 1];
-#pragma unroll
-  for (int t = 0; t < LM1; ++t) pidx[t] = grp.pidx[t];
   const int lo = grp.lo;
+  const bool update = P.npass == 2;
+  const size_t pair = tile.pad1;
+  constexpr size_t PASS_STRIDE = CWARPS * 32 * 64 + CWARPS * 32 * 2;
+  double* base = update ? P.scratch + pair * (2 * PASS_STRIDE) : nullptr;
 
+  if (producer) {
+    int pidx[LM1 > 0 ? LM1 : 1];
+#pragma unroll
+    for (int t = 0; t < LM1; ++t) pidx[t] = grp.pidx[t];
+    const int gp = q4;
+    double lowacc[2] = {0.0, 0.0};
+    for (uint32_t c = 0; c < chunks; ++c) {
+      const uint32_t st = c % STAGES;
+      if (warp == CWARPS) pump(c);
+      __syncwarp();
+      mbar_wait(xfull + st, (c / STAGES) & 1u);
+      const double* xst = xs + st * stage_elems;
+#pragma unroll 1
+      for (int hc = 0; hc < KC / (4 * HSTEPS); ++hc) {
+        const uint32_t u = c * (KC / (4 * HSTEPS)) + hc;
+        const int slot = u & 1;
+        if (u >= 2) mbar_wait(aempty + pw * 2 + slot, ((u >> 1) - 1) & 1u);
+        double* as = aring + slot * ASLOT;
+#pragma unroll
+        for (int t = 0; t < HSTEPS; ++t)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const double* xr = xst + static_cast<size_t>(hc * 4 * HSTEPS + 4 * t + q) * n;
+            double Pv = xr[pidx[0]];
+#pragma unroll
+            for (int t2 = 1; t2 < LM1; ++t2) Pv = __dmul_rn(Pv, xr[pidx[t2]]);
+            const double2 xv = *reinterpret_cast<const double2*>(xr + h8 + 2 * gp);
+            const double a0 = __dmul_rn(Pv, xv.x), a1 = __dmul_rn(Pv, xv.y);
+            if (do_low) {
+              lowacc[0] = __dadd_rn(lowacc[0], a0);  // row order, plain adds (moments.cpp:44)
+              lowacc[1] = __dadd_rn(lowacc[1], a1);
+            }
+            *reinterpret_cast<double2*>(as + t * 32 * ASTRIDE + (r * 4 + q) * ASTRIDE + 2 * gp) =
+                make_double2(a0, a1);
+          }
+        mbar_arrive(afull + pw * 2 + slot);  // every lane: its stores are released
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(xempty + st);
+      if (warp == CWARPS) pump(0);
+    }
+    // ---- producer epilogue: order L (= d-1) ----
+    if (update) {
+      double* mine = base + pass * PASS_STRIDE + CWARPS * 32 * 64;
+      mine[pw * 32 + lane] = __dmul_rn(lowacc[0], P.inv);
+      mine[CWARPS * 32 + pw * 32 + lane] = __dmul_rn(lowacc[1], P.inv);
+    }
+    if (update) {
+      // same two barriers as the consumers' fixup (thread 0 takes the ticket)
+      __threadfence();
+      __syncthreads();
+      __syncthreads();
+      if (*flag_smem == 0) return;
+    }
+    if (!gvalid || !do_low) return;
+    const double cc = P.c;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int g = 2 * gp + e;
+      const int iL = h8 + g;
+      if (g < lo || iL >= n) continue;
+      const PrefixRow& pr = P.rows[static_cast<size_t>(gi) * 8 + g];
+      if (update) {
+        const size_t ix = CWARPS * 32 * 64 + static_cast<size_t>(e) * CWARPS * 32 + pw * 32 + lane;
+        const double mv = base[pass * PASS_STRIDE + ix], ov = __ldcg(base + (pass ^ 1) * PASS_STRIDE + ix);
+        const double delta = pass == 0 ? __dsub_rn(mv, ov) : __dsub_rn(ov, mv);  // a - b
+        P.low[pr.low_off] = __fma_rn(cc, delta, P.low[pr.low_off]);
+        if (pr.idx[7] & 1u) P.dlow[pr.low_off] = delta;
+      } else {
+        P.low[pr.low_off] = __dmul_rn(lowacc[e], P.inv);
+      }
+    }
+    return;
+  }
+
+  // ================= DMMA consumer =================
+  const int q = q4;
   double acc[8][NC][2];
 #pragma unroll
   for (int g = 0; g < 8; ++g)
 #pragma unroll
     for (int c = 0; c < NC; ++c) acc[g][c][0] = acc[g][c][1] = 0.0;
-  double lowacc[2] = {0.0, 0.0};
-
-  auto mma_step = [&](const Raw<LM1, NC>& op) {
-#pragma unroll
-    for (int c = 0; c < NC; ++c)
-#pragma unroll
-      for (int g = 0; g < 8; ++g) dmma(acc[g][c][0], acc[g][c][1], op.a[g], op.b[c]);
-  };
-  // order L sums: the 8 x 4 block (rows g, k) of a step is transposed
-  // through shared memory so lane q owns rows 2q, 2q+1 and adds their four
-  // k values in row order (moments.cpp:44, plain adds).  Written at step t,
-  // read (after the next __syncwarp) at step t + 1.
-  auto low_put = [&](const Raw<LM1, NC>& op, int buf) {
-    double2* wb = reinterpret_cast<double2*>(lowbuf + buf * 264 + q * 66 + r * 8);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) wb[u] = make_double2(op.a[2 * u], op.a[2 * u + 1]);
-  };
-  auto low_get = [&](double2 (&v)[4], int buf) {
-#pragma unroll
-    for (int kp = 0; kp < 4; ++kp) v[kp] = *reinterpret_cast<const double2*>(lowbuf + buf * 264 + kp * 66 + r * 8 + 2 * q);
-  };
-  auto low_add = [&](const double2 (&v)[4], int kleft) {
-#pragma unroll
-    for (int kp = 0; kp < 4; ++kp)
-      if (kp < kleft) {
-        lowacc[0] = __dadd_rn(lowacc[0], v[kp].x);
-        lowacc[1] = __dadd_rn(lowacc[1], v[kp].y);
-      }
-  };
-
-  bool lowpend = false;  // previous step's A values wait in lowbuf[1 - cur]
-  int lb = 0;
-  // one step: loads of the next step, DMMAs of this one, row sums, products
-  auto step = [&](const Raw<LM1, NC>& cur, Raw<LM1, NC>& nxt, const double* xnext, bool has_next) {
-    if (has_next) load_raw<LM1, NC>(nxt, xnext, h8, col0, r, pidx);
-    double2 lv[4];
-    if (do_low && lowpend) {
-      __syncwarp();
-      low_get(lv, lb ^ 1);
-    }
-    mma_step(cur);
-    if (do_low) {
-      low_put(cur, lb);
-      if (lowpend) low_add(lv, 4);
-      lowpend = true;
-      lb ^= 1;
-    }
-    if (has_next) finish<LM1, NC>(nxt, false);
-  };
-  // The step stream is continuous across chunks: the last step of chunk c
-  // loads the first operands of chunk c + 1, so the pipeline never drains.
-  auto stage_ptr = [&](uint32_t c) {
-    return xs + (c % STAGES) * stage_elems + static_cast<size_t>(q) * n;
-  };
-  Raw<LM1, NC> o0, o1;
-  if (warp == 0) pump(0);
-  __syncwarp();
-  mbar_wait(full + 0, 0u);
-  load_raw<LM1, NC>(o0, stage_ptr(0), h8, col0, r, pidx);
-  finish<LM1, NC>(o0, false);
   for (uint32_t c = 0; c < chunks; ++c) {
-    const double* xst = stage_ptr(c);
+    const uint32_t st = c % STAGES;
+    mbar_wait(xfull + st, (c / STAGES) & 1u);
+    const double* xst = xs + st * stage_elems + static_cast<size_t>(q) * n + col0 + r;
 #pragma unroll 1
-    for (int t = 0; t < KC / 4 - 2; t += 2) {
-      step(o0, o1, xst + (4 * t + 4) * n, true);
-      step(o1, o0, xst + (4 * t + 8) * n, true);
+    for (int hc = 0; hc < KC / (4 * HSTEPS); ++hc) {
+      const uint32_t u = c * (KC / (4 * HSTEPS)) + hc;
+      const int slot = u & 1;
+      mbar_wait(afull + pw * 2 + slot, (u >> 1) & 1u);
+      const double* as = aring + slot * ASLOT + (r * 4 + q) * ASTRIDE;
+      const double* xb = xst + static_cast<size_t>(hc * 4 * HSTEPS) * n;
+      double a[2][8], bb[2][NC];
+      auto load = [&](int t, int buf) {
+        const double2* ap = reinterpret_cast<const double2*>(as + t * 32 * ASTRIDE);
+#pragma unroll
+        for (int s2 = 0; s2 < 4; ++s2) {
+          const double2 v = ap[s2];
+          a[buf][2 * s2] = v.x;
+          a[buf][2 * s2 + 1] = v.y;
+        }
+#pragma unroll
+        for (int cc = 0; cc < NC; ++cc) bb[buf][cc] = xb[static_cast<size_t>(4 * t) * n + 8 * cc];
+      };
+      load(0, 0);
+#pragma unroll
+      for (int t = 0; t < HSTEPS; ++t) {
+        if (t + 1 < HSTEPS) load(t + 1, (t + 1) & 1);
+#pragma unroll
+        for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+          for (int g = 0; g < 8; ++g) dmma(acc[g][cc][0], acc[g][cc][1], a[t & 1][g], bb[t & 1][cc]);
+      }
+      mbar_arrive(aempty + pw * 2 + slot);  // every lane has consumed the slot
     }
-    step(o0, o1, xst + (KC - 4) * n, true);
-    // every lane has loaded its rows of this stage: release it
     __syncwarp();
-    if (lane == 0) mbar_arrive(empty + (c % STAGES));
-    const bool more = c + 1 < chunks;
-    if (more) {
-      if (warp == 0) pump(c + 1);
-      __syncwarp();
-      mbar_wait(full + ((c + 1) % STAGES), ((c + 1) / STAGES) & 1u);
-    }
-    step(o1, o0, more ? stage_ptr(c + 1) : xst, more);
-    if (warp == 0) pump(0);  // refill without blocking
-  }
-  if (do_low && lowpend) {
-    __syncwarp();
-    double2 lv[4];
-    low_get(lv, lb ^ 1);
-    low_add(lv, 4);
+    if (lane == 0) mbar_arrive(xempty + st);
   }
 
   // ---- pair fixup: the second of (incoming, outgoing) does the update ----
-  const bool update = P.npass == 2;
-  const size_t pair = tile.pad1;
-  const int tid = threadIdx.x;
+  const int tid = pw * 32 + lane;  // consumer thread index
   double* mine = nullptr;
   const double* other = nullptr;
   if (update) {
-    double* base = P.scratch + pair * (2 * (THREADS * 64 + THREADS * 2));
-    mine = base + pass * (THREADS * 64 + THREADS * 2);
-    other = base + (pass ^ 1) * (THREADS * 64 + THREADS * 2);
+    mine = base + pass * PASS_STRIDE;
+    other = base + (pass ^ 1) * PASS_STRIDE;
 #pragma unroll
     for (int g = 0; g < 8; ++g)
 #pragma unroll
       for (int c = 0; c < NC; ++c)
 #pragma unroll
         for (int e = 0; e < 2; ++e)
-          mine[static_cast<size_t>((g * NC + c) * 2 + e) * THREADS + tid] = __dmul_rn(acc[g][c][e], P.inv);
-    mine[THREADS * 64 + tid] = __dmul_rn(lowacc[0], P.inv);
-    mine[THREADS * 64 + THREADS + tid] = __dmul_rn(lowacc[1], P.inv);
+          mine[static_cast<size_t>((g * NC + c) * 2 + e) * (CWARPS * 32) + tid] = __dmul_rn(acc[g][c][e], P.inv);
     __threadfence();
     __syncthreads();
-    if (tid == 0) *flag_smem = atomicAdd(P.flags + pair, 1u);
+    if (threadIdx.x == 0) *flag_smem = atomicAdd(P.flags + pair, 1u);
     __syncthreads();
     if (*flag_smem == 0) return;  // partner still running: it finishes the pair
     __threadfence();
-    if (tid == 0) P.flags[pair] = 0;  // self-resetting for the next launch
+    if (threadIdx.x == 0) P.flags[pair] = 0;  // self-resetting for the next launch
   }
 
   // ---- epilogue: canonical entries only ----
@@ -373,7 +369,7 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
         off[c][e] = pr.top_base + static_cast<uint64_t>(pr.vprime) * b * (jd - J) +
                     static_cast<uint64_t>(pr.poff) * ext_of(jd, n, b) + (col - jd * b);
         if (update) {
-          const size_t ix = static_cast<size_t>((g * NC + c) * 2 + e) * THREADS + tid;
+          const size_t ix = static_cast<size_t>((g * NC + c) * 2 + e) * (CWARPS * 32) + tid;
           const double mv = mine[ix];
           const double ov = ok[c][e] ? __ldcg(other + ix) : 0.0;
           val[c][e] = pass == 0 ? __dsub_rn(mv, ov) : __dsub_rn(ov, mv);  // a - b
@@ -403,41 +399,29 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
           if (ok[c][e]) P.top[off[c][e]] = val[c][e];
     }
   }
-  if (do_low) {
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int g = 2 * q + e;
-      const int iL = h8 + g;
-      if (g < lo || iL >= n) continue;
-      const PrefixRow& pr = P.rows[static_cast<size_t>(gi) * 8 + g];
-      if (update) {
-        const size_t ix = THREADS * 64 + static_cast<size_t>(e) * THREADS + tid;
-        const double mv = mine[ix], ov2 = __ldcg(other + ix);
-        const double delta = pass == 0 ? __dsub_rn(mv, ov2) : __dsub_rn(ov2, mv);
-        P.low[pr.low_off] = __fma_rn(cc, delta, P.low[pr.low_off]);
-        if (pr.idx[7] & 1u) P.dlow[pr.low_off] = delta;
-      } else {
-        P.low[pr.low_off] = __dmul_rn(lowacc[e], P.inv);
-      }
-    }
-  }
 }
 
-__global__ void __launch_bounds__(THREADS, 2) moment_top_dmma_kernel(const MomParams P) {
+__global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomParams P) {
   extern __shared__ __align__(128) double smem[];
-  __shared__ __align__(8) uint64_t full[STAGES];
-  __shared__ __align__(8) uint64_t empty[STAGES];
+  __shared__ __align__(8) uint64_t xfull[STAGES];
+  __shared__ __align__(8) uint64_t xempty[STAGES];
+  __shared__ __align__(8) uint64_t afull[CWARPS * 2];
+  __shared__ __align__(8) uint64_t aempty[CWARPS * 2];
   __shared__ uint32_t flag_smem;
   double* xs = smem;
   // dense staging ring; reads past row n of a stage (the last 8-column
   // window / column group) only feed rows and columns that are never stored
-  double* lowbufs = xs + static_cast<size_t>(STAGES) * KC * P.n + 64;  // WARPS x 2 x 4 x 66
+  double* arings = xs + static_cast<size_t>(STAGES) * KC * P.n + 64;  // CWARPS x 2 x ASLOT
   const int pass = static_cast<int>(blockIdx.x % P.npass);
   const MomTile tile = P.tiles[blockIdx.x / P.npass];
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full + s, 1);
-      mbar_init(empty + s, WARPS);
+      mbar_init(xfull + s, 1);
+      mbar_init(xempty + s, WARPS);
+    }
+    for (int s = 0; s < CWARPS * 2; ++s) {
+      mbar_init(afull + s, 32);
+      mbar_init(aempty + s, 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -445,7 +429,8 @@ __global__ void __launch_bounds__(THREADS, 2) moment_top_dmma_kernel(const MomPa
   const int nc = static_cast<int>(tile.pad0);
   switch (P.L * 8 + nc) {
 #define CSB_CASE(LL, NCC) \
-  case (LL) * 8 + (NCC): run_tile<(LL) - 1, NCC>(P, tile, pass, xs, full, empty, lowbufs, &flag_smem); break;
+  case (LL) * 8 + (NCC): \
+    run_tile<(LL) - 1, NCC>(P, tile, pass, xs, arings, xfull, xempty, afull, aempty, &flag_smem); break;
 #define CSB_CASES(LL) CSB_CASE(LL, 1) CSB_CASE(LL, 2) CSB_CASE(LL, 3) CSB_CASE(LL, 4)
     CSB_CASES(2) CSB_CASES(3) CSB_CASES(4) CSB_CASES(5)
 #undef CSB_CASES
@@ -504,20 +489,21 @@ __global__ void __launch_bounds__(256) mirror_kernel(double* __restrict__ m, con
 }
 
 size_t smem_bytes(int n) {
-  return sizeof(double) * (static_cast<size_t>(STAGES) * KC * n + 64 + WARPS * 2 * 4 * 66);
+  return sizeof(double) * (static_cast<size_t>(STAGES) * KC * n + 64 + CWARPS * 2 * ASLOT);
 }
 
 }  // namespace
 
-int dmma_warps() { return WARPS; }
+int dmma_warps() { return CWARPS; }
 
-// per tile pair: both passes' stashes (64 values + 2 low sums per thread)
-size_t dmma_scratch_per_tile() { return static_cast<size_t>(2) * (THREADS * 64 + THREADS * 2); }
+// per tile pair: both passes' stashes (64 values per consumer thread + 2
+// row sums per producer thread)
+size_t dmma_scratch_per_tile() { return static_cast<size_t>(2) * (CWARPS * 32 * 64 + CWARPS * 32 * 2); }
 
 bool dmma_supported(const MomParams& p) {
   // instantiated for orders 3..6 (L = 2..5); the staging ring must fit
   if (p.n % 2 != 0 || p.L < 2 || p.L > 5) return false;
-  if (smem_bytes(p.n) > 110 * 1024) return false;  // two CTAs per SM
+  if (smem_bytes(p.n) > 220 * 1024) return false;
   return true;
 }
 
