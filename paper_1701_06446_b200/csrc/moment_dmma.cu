@@ -37,10 +37,10 @@ namespace {
 constexpr int CWARPS = 4;           // DMMA consumer warps
 constexpr int WARPS = 2 * CWARPS;   // + one producer warp per consumer
 constexpr int THREADS = WARPS * 32;
-constexpr int HSTEPS = 4;           // k4 steps per A-ring slot (16 rows)
+constexpr int HSTEPS = 8;           // k4 steps per A-ring slot (one 32-row chunk)
 constexpr int ASTRIDE = 10;         // doubles per (r, q) entry: 8 used, bank-conflict free
 constexpr int ASLOT = HSTEPS * 32 * ASTRIDE;
-constexpr int STAGES = 3;
+constexpr int STAGES = 2;
 constexpr int KC = 32;        // data rows per stage
 
 
