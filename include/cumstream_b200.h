@@ -175,6 +175,26 @@ int csb_stream_norm_partials(csb_stream* st, int order, double* host, uint64_t c
 /* Device stream (cudaStream_t) the engine launches on, for interop. */
 int csb_stream_cuda_stream(csb_stream* st, void** cuda_stream);
 
+/* ---- multi-GPU: block-prefix shards + NCCL ------------------ */
+/* One process per GPU.  Rank 0 makes an id, every rank passes it to
+ * csb_comm_init (NCCL is loaded at run time from libnccl.so.2); a stream
+ * primed with shard_count == nranks, shard_index == rank then owns a
+ * contiguous range of order-d and order-(d-1) blocks (prefix (j1, j2)
+ * ranges balanced by canonical weight), replicates orders <= d-2, gathers
+ * M_{d-1} and reduces the order-d norm partials / diagonal with NCCL. */
+int csb_comm_unique_id(unsigned char* out /* 128 bytes */);
+int csb_comm_init(int nranks, int rank, const unsigned char* id /* 128 bytes */);
+int csb_comm_destroy(void);
+/* Block and element range of one shard: which = 0 for order d, 1 for d-1. */
+int csb_shard_range(int max_order, int dim, int block, int shard_index, int shard_count, int which,
+                    uint64_t* blk_lo, uint64_t* blk_hi, uint64_t* elem_lo, uint64_t* elem_hi);
+/* Series-level shard computations without any exchange (the caller owns the
+ * assembly): the shard's blocks of orders d and d-1, all orders <= d-2. */
+int csb_moments_update_shard(csb_series* m, const double* incoming, const double* outgoing,
+                             uint64_t rows, uint64_t cols, int shard_index, int shard_count);
+/* C_1..C_{d-1} in full and the shard's blocks of C_d (m must be complete). */
+int csb_moms2cums_shard(const csb_series* m, csb_series* c, int shard_index, int shard_count);
+
 /* ---- instrumentation (bench.py) ------------------------------------------ */
 /* Kernels launched by this library so far in this process. */
 uint64_t csb_launch_count(void);

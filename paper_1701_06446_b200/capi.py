@@ -127,6 +127,13 @@ def lib() -> C.CDLL:
             "csb_stream_materialize": ([C.c_void_p, _dp, _u64], C.c_int),
             "csb_stream_norm_partials": ([C.c_void_p, C.c_int, _dp, _u64, C.POINTER(_u64)], C.c_int),
             "csb_stream_cuda_stream": ([C.c_void_p, C.POINTER(C.c_void_p)], C.c_int),
+            "csb_comm_unique_id": ([C.c_char_p], C.c_int),
+            "csb_comm_init": ([C.c_int, C.c_int, C.c_char_p], C.c_int),
+            "csb_comm_destroy": ([], C.c_int),
+            "csb_shard_range": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(_u64),
+                                 C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64)], C.c_int),
+            "csb_moments_update_shard": ([C.c_void_p, _dp, _dp, _u64, _u64, C.c_int, C.c_int], C.c_int),
+            "csb_moms2cums_shard": ([C.c_void_p, C.c_void_p, C.c_int, C.c_int], C.c_int),
             "csb_launch_count": ([], _u64),
             "csb_profile_enable": ([C.c_int], C.c_int),
             "csb_profile_read": ([C.c_char_p, C.POINTER(C.c_double), C.POINTER(_u64)], C.c_int),
@@ -173,6 +180,23 @@ def profile_read(tag: str) -> tuple[float, int]:
     ms, cnt = C.c_double(), _u64()
     check(lib().csb_profile_read(tag.encode(), C.byref(ms), C.byref(cnt)))
     return ms.value, cnt.value
+
+
+def shard_range(max_order: int, dim: int, block: int, shard: int, count: int, which: int = 0):
+    """(blk_lo, blk_hi, elem_lo, elem_hi) of a shard for order d (which=0) or d-1 (which=1)."""
+    v = [_u64() for _ in range(4)]
+    check(lib().csb_shard_range(max_order, dim, block, shard, count, which, *[C.byref(x) for x in v]))
+    return tuple(x.value for x in v)
+
+
+def comm_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(lib().csb_comm_unique_id(buf))
+    return buf.raw
+
+
+def comm_init(nranks: int, rank: int, uid: bytes) -> None:
+    check(lib().csb_comm_init(nranks, rank, uid))
 
 
 class Series:
@@ -251,6 +275,18 @@ def moments_update(m: Series, incoming: np.ndarray, outgoing: np.ndarray) -> Non
     if xi.shape != xo.shape:
         raise CsbInvalidArgument("moments_update: batch sizes differ")
     check(lib().csb_moments_update(m.h, _dptr(xi), _dptr(xo), xi.shape[0], xi.shape[1]))
+
+
+def moments_update_shard(m: Series, incoming: np.ndarray, outgoing: np.ndarray, shard: int, count: int) -> None:
+    xi = np.ascontiguousarray(incoming, dtype=np.float64)
+    xo = np.ascontiguousarray(outgoing, dtype=np.float64)
+    check(lib().csb_moments_update_shard(m.h, _dptr(xi), _dptr(xo), xi.shape[0], xi.shape[1], shard, count))
+
+
+def moms2cums_shard(m: Series, shard: int, count: int) -> Series:
+    c = Series(m.dim, m.max_order, m.block)
+    check(lib().csb_moms2cums_shard(m.h, c.h, shard, count))
+    return c
 
 
 def moms2cums(m: Series) -> Series:

@@ -447,6 +447,14 @@ __global__ void __launch_bounds__(1024) norm_finalize_kernel(const NormParams P)
   }
 }
 
+// Diagonal entries of a sharded tensor: the owner's value, zero elsewhere
+// (summed over ranks this reproduces the full diagonal exactly).
+__global__ void diag_pick_kernel(const double* c, const uint64_t* off, uint64_t lo, uint64_t hi, int n,
+                                 double* out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = (off[i] >= lo && off[i] < hi) ? c[off[i]] : 0.0;
+}
+
 __global__ void combine_kernel(const double* a, const double* b, double w1, double w2, double* out,
                                uint64_t count) {
   // combine (moments.cpp:258-262): z = w1 * z + w2 * b, contracted to
@@ -515,6 +523,13 @@ void launch_knorm_partials(const double* t, const LayoutDev& lay, uint64_t nbloc
                            double* partial, cudaStream_t st) {
   if (!nblocks) return;
   knorm_partials_kernel<<<static_cast<unsigned>(nblocks), 256, 0, st>>>(t, lay, nblocks, k, partial);
+  CSB_CUDA(cudaGetLastError());
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+void launch_diag_pick(const double* c, const uint64_t* off, uint64_t lo, uint64_t hi, int n, double* out,
+                      cudaStream_t st) {
+  diag_pick_kernel<<<(n + 255) / 256, 256, 0, st>>>(c, off, lo, hi, n, out);
   CSB_CUDA(cudaGetLastError());
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }

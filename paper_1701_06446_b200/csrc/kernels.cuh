@@ -88,6 +88,8 @@ void launch_copy_c1(const double* m1, double* c1, double* partial, const LayoutD
 void launch_norm_finalize(const NormParams& p, cudaStream_t st);
 void launch_knorm_partials(const double* t, const LayoutDev& lay, uint64_t nblocks, double k,
                            double* partial, cudaStream_t st);
+void launch_diag_pick(const double* c, const uint64_t* off, uint64_t lo, uint64_t hi, int n, double* out,
+                      cudaStream_t st);
 void launch_combine(const double* a, const double* b, double w1, double w2, double* out,
                     uint64_t count, cudaStream_t st);
 

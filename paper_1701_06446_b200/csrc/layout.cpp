@@ -152,8 +152,97 @@ PrefixRow MomentPlan::make_row(const int* t, const Layout& top, const Layout* lo
   return r;
 }
 
+void ShardPlan::build(int d_, int n_, int b_, int count_, const Layout& top, const Layout& low) {
+  d = d_;
+  n = n_;
+  b = b_;
+  count = std::max(1, count_);
+  // prefix length: the (d-2)-prefix pi of a DMMA group fixes the first d-2
+  // block coordinates; 2 (d = 4) or 3 (d >= 5) gives enough granularity
+  plen = std::max(0, std::min(d >= 5 ? 3 : 2, d - 2));
+  const int g = top.grid;
+  prefix_rank = plen > 0 ? std::make_shared<Layout>(plen, g, 1) : nullptr;
+  const uint64_t nprefix = plen == 0 ? 1 : prefix_rank->nblocks;
+  std::vector<double> w(nprefix, 0.0);
+  auto prank = [&](const uint16_t* j) -> uint64_t {
+    if (plen == 0) return 0;
+    int t[3];
+    for (int k = 0; k < plen; ++k) t[k] = j[k];
+    return prefix_rank->rank(t);
+  };
+  for (uint64_t r = 0; r < top.nblocks; ++r) {
+    const uint16_t* j = &top.index[r * d];
+    // canonical entries of the block: prod over runs C(e + len - 1, len)
+    double c = 1.0;
+    for (int a = 0; a < d;) {
+      int e2 = a + 1;
+      while (e2 < d && j[e2] == j[a]) ++e2;
+      c *= static_cast<double>(multiset_count(top.ext(j[a]), e2 - a));
+      a = e2;
+    }
+    w[prank(j)] += c;
+  }
+  // contiguous min-max partition of the prefix sequence into `count`
+  // ranges (binary search on the largest range weight, greedy fill)
+  double total = 0.0, wmax = 0.0;
+  for (double v : w) {
+    total += v;
+    wmax = std::max(wmax, v);
+  }
+  auto fits = [&](double cap) {
+    int used = 1;
+    double acc = 0.0;
+    for (double v : w) {
+      if (acc + v > cap) {
+        ++used;
+        acc = 0.0;
+      }
+      acc += v;
+    }
+    return used <= count;
+  };
+  double lo = std::max(wmax, total / count), hi = total;
+  for (int it = 0; it < 100 && hi - lo > 1e-9 * total; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    (fits(mid) ? hi : lo) = mid;
+  }
+  shard_of_prefix.assign(nprefix, 0);
+  {
+    int cur = 0;
+    double acc = 0.0;
+    for (uint64_t p = 0; p < nprefix; ++p) {
+      // open a new range when the cap is exceeded, or when the remaining
+      // prefixes are needed to give every later shard at least one
+      if (cur < count - 1 && (acc + w[p] > hi || nprefix - p <= static_cast<uint64_t>(count - 1 - cur))) {
+        if (acc > 0.0) {
+          ++cur;
+          acc = 0.0;
+        }
+      }
+      shard_of_prefix[p] = cur;
+      acc += w[p];
+    }
+  }
+  auto bounds = [&](const Layout& L, std::vector<uint64_t>& out) {
+    out.assign(count + 1, L.nblocks);
+    out[0] = 0;
+    int last = 0;
+    for (uint64_t r = 0; r < L.nblocks; ++r) {
+      const int sh = plen == 0 ? 0 : shard_of_prefix[prank(&L.index[r * L.order])];
+      while (last < sh) out[++last] = r;
+    }
+  };
+  bounds(top, top_blk);
+  bounds(low, low_blk);
+}
+
+int ShardPlan::owner(const int* jp) const {
+  if (plen == 0) return 0;
+  return shard_of_prefix[prefix_rank->rank(jp)];
+}
+
 void MomentPlan::build_dmma(int S_, int n_, int b_, const Layout& top, const Layout* low, int warps,
-                            uint64_t scratch) {
+                            uint64_t scratch, const ShardPlan* shard, int shard_index) {
   S = S_;
   L = S_ - 1;
   n = n_;
@@ -190,6 +279,11 @@ void MomentPlan::build_dmma(int S_, int n_, int b_, const Layout& top, const Lay
     for (const auto& pi : pis) {
       const int last = LM1 > 0 ? pi[LM1 - 1] : 0;
       if (last > 8 * h + 7) continue;  // every row of this group has i_L < i_{L-1}
+      if (shard && shard->count > 1) {
+        int jp[3] = {0, 0, 0};
+        for (int k = 0; k < shard->plen; ++k) jp[k] = pi[k] / b;
+        if (shard->owner(jp) != shard_index) continue;  // another shard's blocks
+      }
       DmmaGroup g{};
       for (int k = 0; k < 6; ++k) g.pidx[k] = pi[k];
       g.lo = static_cast<uint16_t>(std::max(0, last - 8 * h));

@@ -15,6 +15,7 @@
 #pragma once
 
 #include <cstdint>
+#include <memory>
 #include <vector>
 
 #include "common.hpp"
@@ -69,6 +70,22 @@ struct MomTile {
   uint32_t pad0, pad1;
 };
 
+// Block-prefix sharding of the top pair of orders: order-d
+// blocks are owned by their first plen block coordinates (2 for d = 4, 3 for
+// d >= 5, never more than d-2), in contiguous prefix ranges from a min-max
+// partition of the canonical-element weight.  Ownership then depends only on the (d-2)-prefix pi of a DMMA
+// group, so a shard computes whole groups, owns a contiguous range of
+// order-d blocks AND a contiguous range of order-(d-1) blocks.
+struct ShardPlan {
+  int d = 0, n = 0, b = 0, count = 1;
+  int plen = 0;                          // prefix length (block coordinates)
+  std::shared_ptr<Layout> prefix_rank;   // lexicographic ranker of prefixes
+  std::vector<int> shard_of_prefix;      // by lexicographic prefix rank
+  std::vector<uint64_t> top_blk, low_blk;  // count + 1 block boundaries (orders d, d-1)
+  void build(int d, int n, int b, int count, const Layout& top, const Layout& low);
+  int owner(const int* block_prefix) const;  // shard of a block prefix (plen coords)
+};
+
 struct MomentPlan {
   int S = 0, L = 0, n = 0, b = 0;
   std::vector<PrefixRow> rows;
@@ -84,7 +101,7 @@ struct MomentPlan {
   // warp; columns [8h, n) in ranges of at most 4 groups of 8; rows[8 g + r]
   // is the PrefixRow of row r of group g (zero for masked rows).
   void build_dmma(int S, int n, int b, const Layout& top, const Layout* low, int warps,
-                  uint64_t scratch_per_tile);
+                  uint64_t scratch_per_tile, const ShardPlan* shard = nullptr, int shard_index = 0);
   void upload();
 
  private:

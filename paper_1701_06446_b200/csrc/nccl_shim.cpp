@@ -1,0 +1,112 @@
+#include "nccl_shim.hpp"
+
+#include <dlfcn.h>
+
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "common.hpp"
+
+namespace csb {
+namespace nccl {
+
+namespace {
+
+// ABI of the few NCCL entry points used (nccl.h, stable since NCCL 2.0)
+typedef int ncclResult_t;
+typedef struct {
+  char internal[kUniqueIdBytes];
+} ncclUniqueId;
+typedef void* ncclComm_t;
+constexpr int ncclDouble = 8;  // ncclFloat64
+constexpr int ncclSum = 0;
+
+struct Api {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+Api& api() {
+  static Api a;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+      a.h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+      if (a.h) break;
+    }
+    if (!a.h) return;
+    a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(a.h, "ncclGetUniqueId"));
+    a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(dlsym(a.h, "ncclCommInitRank"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(a.h, "ncclCommDestroy"));
+    a.Broadcast = reinterpret_cast<decltype(a.Broadcast)>(dlsym(a.h, "ncclBroadcast"));
+    a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(dlsym(a.h, "ncclAllReduce"));
+    a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(dlsym(a.h, "ncclGroupStart"));
+    a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(dlsym(a.h, "ncclGroupEnd"));
+    a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(a.h, "ncclGetErrorString"));
+  });
+  return a;
+}
+
+void check(ncclResult_t r, const char* what) {
+  if (r != 0) {
+    const char* msg = api().GetErrorString ? api().GetErrorString(r) : "?";
+    fail(CSB_ERUNTIME, std::string(what) + ": " + msg);
+  }
+}
+
+Api& need() {
+  Api& a = api();
+  if (!a.h || !a.GetUniqueId || !a.CommInitRank || !a.Broadcast || !a.AllReduce)
+    fail(CSB_ERUNTIME, "NCCL (libnccl.so.2) is not available");
+  return a;
+}
+
+}  // namespace
+
+bool available() { return api().h != nullptr; }
+
+void get_unique_id(unsigned char out[kUniqueIdBytes]) {
+  ncclUniqueId id;
+  check(need().GetUniqueId(&id), "ncclGetUniqueId");
+  std::memcpy(out, id.internal, kUniqueIdBytes);
+}
+
+void* comm_init(int nranks, int rank, const unsigned char idb[kUniqueIdBytes]) {
+  ncclUniqueId id;
+  std::memcpy(id.internal, idb, kUniqueIdBytes);
+  ncclComm_t c = nullptr;
+  check(need().CommInitRank(&c, nranks, id, rank), "ncclCommInitRank");
+  return c;
+}
+
+void comm_destroy(void* comm) {
+  if (comm && api().CommDestroy) api().CommDestroy(static_cast<ncclComm_t>(comm));
+}
+
+void allgather_ranges(void* comm, double* buf, const uint64_t* off, const uint64_t* cnt, int nranks,
+                      cudaStream_t st) {
+  Api& a = need();
+  check(a.GroupStart(), "ncclGroupStart");
+  for (int r = 0; r < nranks; ++r)
+    if (cnt[r])
+      check(a.Broadcast(buf + off[r], buf + off[r], cnt[r], ncclDouble, r, static_cast<ncclComm_t>(comm), st),
+            "ncclBroadcast");
+  check(a.GroupEnd(), "ncclGroupEnd");
+}
+
+void allreduce_sum(void* comm, double* buf, uint64_t count, cudaStream_t st) {
+  if (!count) return;
+  check(need().AllReduce(buf, buf, count, ncclDouble, ncclSum, static_cast<ncclComm_t>(comm), st),
+        "ncclAllReduce");
+}
+
+}  // namespace nccl
+}  // namespace csb

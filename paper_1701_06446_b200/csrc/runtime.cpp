@@ -18,6 +18,7 @@
 #include "common.hpp"
 #include "kernels.cuh"
 #include "layout.hpp"
+#include "nccl_shim.hpp"
 
 namespace csb {
 
@@ -34,6 +35,13 @@ struct DevLayout {
   DevBuf<double> mult;
   DevBuf<uint32_t> diag;  // blocks with equal neighbouring coordinates
   uint32_t ndiag = 0;
+  std::vector<uint32_t> diag_host;
+  // [first, count) of the diagonal-block list inside block range [lo, hi)
+  std::pair<uint32_t, uint32_t> diag_range(uint64_t lo, uint64_t hi) const {
+    const auto a = std::lower_bound(diag_host.begin(), diag_host.end(), lo);
+    const auto b = std::lower_bound(diag_host.begin(), diag_host.end(), hi);
+    return {static_cast<uint32_t>(a - diag_host.begin()), static_cast<uint32_t>(b - a)};
+  }
   LayoutDev view() const {
     LayoutDev v;
     v.offset = offset.ptr;
@@ -54,6 +62,9 @@ struct Device {
   std::map<std::tuple<int, int, int>, std::shared_ptr<DevLayout>> layouts;
   std::map<std::tuple<int, int, int, int>, std::shared_ptr<MomentPlan>> plans;
   std::map<std::tuple<int, int, int>, std::shared_ptr<DevBuf<LowerElem>>> lower;
+  std::map<std::tuple<int, int, int, int>, std::shared_ptr<ShardPlan>> shards;
+  void* comm = nullptr;  // NCCL communicator (csb_comm_init)
+  int nranks = 1, rank = 0;
 };
 
 std::mutex g_dev_mu;
@@ -109,6 +120,7 @@ std::shared_ptr<DevLayout> get_layout(Device& dev, int order, int n, int b) {
       if (runs) diag.push_back(static_cast<uint32_t>(r));
     }
     L->ndiag = static_cast<uint32_t>(diag.size());
+    L->diag_host = diag;
     L->diag.alloc(diag.size());
     if (!diag.empty())
       CSB_CUDA(cudaMemcpy(L->diag.ptr, diag.data(), L->diag.bytes(), cudaMemcpyHostToDevice));
@@ -117,15 +129,31 @@ std::shared_ptr<DevLayout> get_layout(Device& dev, int order, int n, int b) {
   return slot;
 }
 
-std::shared_ptr<MomentPlan> get_plan(Device& dev, int S, int n, int b, bool dmma) {
+std::shared_ptr<ShardPlan> get_shard_plan(Device& dev, int d, int n, int b, int count) {
+  auto top = get_layout(dev, d, n, b);
+  auto low = get_layout(dev, d > 1 ? d - 1 : 1, n, b);
+  std::lock_guard<std::mutex> lk(dev.mu);
+  auto& slot = dev.shards[{d, n, b, count}];
+  if (!slot) {
+    auto sp = std::make_shared<ShardPlan>();
+    sp->build(d, n, b, count, top->host, low->host);
+    slot = sp;
+  }
+  return slot;
+}
+
+std::shared_ptr<MomentPlan> get_plan(Device& dev, int S, int n, int b, bool dmma, const ShardPlan* sp = nullptr,
+                                     int shard_index = 0) {
   auto top = get_layout(dev, S, n, b);
   std::shared_ptr<DevLayout> low = S > 1 ? get_layout(dev, S - 1, n, b) : nullptr;
+  const int count = sp ? sp->count : 1;
   std::lock_guard<std::mutex> lk(dev.mu);
-  auto& slot = dev.plans[{S, n, b, dmma ? 1 : 0}];
+  auto& slot = dev.plans[{S, n, b, (dmma ? 1 : 0) + 2 * (count * 256 + shard_index)}];
   if (!slot) {
     auto p = std::make_shared<MomentPlan>();
     if (dmma)
-      p->build_dmma(S, n, b, top->host, low ? &low->host : nullptr, dmma_warps(), dmma_scratch_per_tile());
+      p->build_dmma(S, n, b, top->host, low ? &low->host : nullptr, dmma_warps(), dmma_scratch_per_tile(), sp,
+                    shard_index);
     else
       p->build(S, n, b, top->host, low ? &low->host : nullptr, kMomThreads);
     p->upload();
@@ -287,8 +315,20 @@ const bool g_use_dmma = [] {
 // multiply-add of the reference's deepest loop (moments.cpp:47) on the
 // FP64 tensor cores when possible -- and every order <= d-2 by the
 // element-parallel low-order kernel (plain product + add, moments.cpp:55-57).
+// Which part of the top pair this process owns.  comm is the
+// NCCL communicator of the stream engine; the series-level shard entry
+// points run without one (no exchange: the caller assembles shards).
+struct ShardCtx {
+  const ShardPlan* plan = nullptr;
+  int index = 0;
+  void* comm = nullptr;
+  bool active() const { return plan && plan->count > 1; }
+  uint64_t lo(int which) const { return (which ? plan->low_blk : plan->top_blk)[index]; }
+  uint64_t hi(int which) const { return (which ? plan->low_blk : plan->top_blk)[index + 1]; }
+};
+
 void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, double c,
-                 cudaStream_t st, int only_order = 0) {
+                 cudaStream_t st, int only_order = 0, const ShardCtx& sh = ShardCtx{}) {
   Device& dev = *m->dev;
   const int d = m->d;
   const int S = only_order ? only_order : d;
@@ -332,7 +372,9 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
     // the top pair runs on the FP64 tensor cores when the rows allow TMA
     // bulk copies; otherwise on the DFMA kernel
     const bool use_dmma = g_use_dmma && dmma_supported(p);
-    auto plan = get_plan(dev, S, m->n, m->b, use_dmma);
+    // sharding applies to the DMMA plan (the DFMA fallback computes all blocks)
+    const bool sharded = use_dmma && sh.active() && !only_order;
+    auto plan = get_plan(dev, S, m->n, m->b, use_dmma, sharded ? sh.plan : nullptr, sharded ? sh.index : 0);
     p.rows = plan->d_rows.ptr;
     p.tiles = plan->d_tiles.ptr;
     p.groups = plan->d_groups.ptr;
@@ -348,10 +390,24 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
       }
       launch_moment_top_dmma(p, static_cast<int>(ntiles), st);
       const auto& LT = m->lay[S - 1];
-      launch_mirror(S, p.top, p.dtop, LT->view(), LT->diag.ptr, LT->ndiag, m->n, m->b, npass == 2, c, st);
+      auto rt = sharded ? LT->diag_range(sh.lo(0), sh.hi(0)) : std::make_pair(0u, LT->ndiag);
+      launch_mirror(S, p.top, p.dtop, LT->view(), LT->diag.ptr + rt.first, rt.second, m->n, m->b, npass == 2, c, st);
       if (p.low) {
         const auto& LL = m->lay[S - 2];
-        launch_mirror(S - 1, p.low, p.dlow, LL->view(), LL->diag.ptr, LL->ndiag, m->n, m->b, npass == 2, c, st);
+        auto rl = sharded ? LL->diag_range(sh.lo(1), sh.hi(1)) : std::make_pair(0u, LL->ndiag);
+        launch_mirror(S - 1, p.low, p.dlow, LL->view(), LL->diag.ptr + rl.first, rl.second, m->n, m->b, npass == 2,
+                      c, st);
+        if (sharded && sh.comm) {
+          // collective C2: every rank needs all of M_{d-1} (its own blocks
+          // were just updated, the rest arrive from their owners)
+          std::vector<uint64_t> off(sh.plan->count), cnt(sh.plan->count);
+          for (int r = 0; r < sh.plan->count; ++r) {
+            off[r] = LL->host.offset[sh.plan->low_blk[r]];
+            cnt[r] = LL->host.offset[sh.plan->low_blk[r + 1]] - off[r];
+          }
+          ProfScope pc("allgather", st);
+          nccl::allgather_ranges(sh.comm, p.low, off.data(), cnt.data(), sh.plan->count, st);
+        }
       }
     } else {
       launch_moment_pair(p, static_cast<int>(ntiles), true, st);
@@ -369,11 +425,13 @@ void check_batch(uint64_t rows, uint64_t cols, const char* what) {
 // moms2cums into c, with per-block partial squared norms for every order.
 struct NormScratch {
   std::vector<DevBuf<double>> partial;  // per order
+  DevBuf<double> diag;                  // gathered diagonal of a sharded C_d
   DevBuf<double> out;
   std::vector<double> host;
 };
 
-void run_moms2cums(const csb_series* m, csb_series* c, NormScratch& ns, cudaStream_t st) {
+void run_moms2cums(const csb_series* m, csb_series* c, NormScratch& ns, cudaStream_t st,
+                   const ShardCtx& sh = ShardCtx{}) {
   const int d = m->d;
   if (ns.partial.size() != static_cast<size_t>(d)) {
     ns.partial.clear();
@@ -391,9 +449,23 @@ void run_moms2cums(const csb_series* m, csb_series* c, NormScratch& ns, cudaStre
     for (int k = 1; k <= s; ++k) p.lay[k - 1] = m->lay[k - 1]->view();
     p.n = m->n;
     p.b = m->b;
-    p.blk0 = 0;
-    p.partial = ns.partial[s - 1].ptr;
-    launch_moms2cums_v2(s, p, m->lay[s - 1]->host.nblocks, st);
+    if (s == d && sh.active()) {
+      // C_d only for the owned blocks; the other partials stay zero so a
+      // sum over ranks reproduces the unsharded partial array exactly
+      const uint64_t lo = sh.lo(0), hi = sh.hi(0);
+      CSB_CUDA(cudaMemsetAsync(ns.partial[s - 1].ptr, 0, ns.partial[s - 1].bytes(), st));
+      p.blk0 = lo;
+      p.partial = ns.partial[s - 1].ptr + lo;
+      launch_moms2cums_v2(s, p, hi - lo, st);
+      if (sh.comm) {
+        ProfScope pc("allreduce", st);
+        nccl::allreduce_sum(sh.comm, ns.partial[s - 1].ptr, m->lay[s - 1]->host.nblocks, st);  // collective C3
+      }
+    } else {
+      p.blk0 = 0;
+      p.partial = ns.partial[s - 1].ptr;
+      launch_moms2cums_v2(s, p, m->lay[s - 1]->host.nblocks, st);
+    }
   }
   c->window_len = m->window_len;
 }
@@ -401,6 +473,7 @@ void run_moms2cums(const csb_series* m, csb_series* c, NormScratch& ns, cudaStre
 // Device offsets of the diagonals c_2[i,i], c_3[i,i,i], c_4[i,i,i,i].
 struct DiagTables {
   DevBuf<uint64_t> off[3];
+  DevBuf<uint64_t> iota;  // 0..n-1
 };
 
 DiagTables& diag_tables(const csb_series* c) {
@@ -419,12 +492,16 @@ DiagTables& diag_tables(const csb_series* c) {
       t.off[q].alloc(c->n);
       CSB_CUDA(cudaMemcpy(t.off[q].ptr, off.data(), t.off[q].bytes(), cudaMemcpyHostToDevice));
     }
+    std::vector<uint64_t> io(c->n);
+    for (int i = 0; i < c->n; ++i) io[i] = static_cast<uint64_t>(i);
+    t.iota.alloc(c->n);
+    CSB_CUDA(cudaMemcpy(t.iota.ptr, io.data(), t.iota.bytes(), cudaMemcpyHostToDevice));
   }
   return t;
 }
 
 // Norm sums of orders 1..d (from partials) + diagonals, to the host.
-void finalize_norms(const csb_series* c, NormScratch& ns, cudaStream_t st) {
+void finalize_norms(const csb_series* c, NormScratch& ns, cudaStream_t st, const ShardCtx& sh = ShardCtx{}) {
   const int d = c->d;
   NormParams p;
   p.norders = d;
@@ -437,6 +514,16 @@ void finalize_norms(const csb_series* c, NormScratch& ns, cudaStream_t st) {
   for (int q = 0; q < 3; ++q) {
     p.diag_src[q] = (q + 2 <= d) ? c->data[q + 1].ptr : nullptr;
     p.diag_off[q] = dt.off[q].ptr;
+  }
+  if (sh.active() && d <= 4) {
+    // the diagonal of C_d is sharded: owners contribute, others add zeros
+    const auto& L = c->lay[d - 1];
+    if (ns.diag.count < static_cast<uint64_t>(c->n)) ns.diag.alloc(c->n);
+    launch_diag_pick(c->data[d - 1].ptr, dt.off[d - 2].ptr, L->host.offset[sh.lo(0)], L->host.offset[sh.hi(0)],
+                     c->n, ns.diag.ptr, st);
+    if (sh.comm) nccl::allreduce_sum(sh.comm, ns.diag.ptr, c->n, st);
+    p.diag_src[d - 2] = ns.diag.ptr;
+    p.diag_off[d - 2] = dt.iota.ptr;
   }
   p.n = c->n;
   const uint64_t need = d + 3ull * c->n;
@@ -528,6 +615,8 @@ struct csb_stream {
   uint64_t steps_since_resync = 0;
   NormScratch ns;
   bool norms_valid = false;
+  std::shared_ptr<ShardPlan> splan;  // shard_count > 1
+  ShardCtx sh;
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
   ~csb_stream() {
     for (auto& e : ev)
@@ -570,7 +659,7 @@ void stream_exchange_and_update(csb_stream* s, const double* x_dev) {
     src[0].seg0 = x_dev;
     src[0].len0 = static_cast<uint32_t>(p);
     src[1] = out;
-    run_moments(s->M.get(), src, 2, p, static_cast<double>(p) / static_cast<double>(T), s->st);
+    run_moments(s->M.get(), src, 2, p, static_cast<double>(p) / static_cast<double>(T), s->st, 0, s->sh);
     g_rows_read.fetch_add(2 * p, std::memory_order_relaxed);
   }
   // incoming rows take the outgoing slots
@@ -587,7 +676,7 @@ void stream_exchange_and_update(csb_stream* s, const double* x_dev) {
     src[0].len0 = static_cast<uint32_t>(T - s->head);
     src[0].seg1 = s->ring.ptr;
     src[0].len1 = static_cast<uint32_t>(s->head);
-    run_moments(s->M.get(), src, 1, T, 0.0, s->st);
+    run_moments(s->M.get(), src, 1, T, 0.0, s->st, 0, s->sh);
     g_rows_read.fetch_add(T, std::memory_order_relaxed);
     s->steps_since_resync = 0;
   } else {
@@ -611,12 +700,12 @@ int stream_step_impl(csb_stream* s, const double* x, bool on_device, uint64_t ro
     CSB_CUDA(cudaEventRecord(s->ev[0], s->st));
     stream_exchange_and_update(s, xd);
     CSB_CUDA(cudaEventRecord(s->ev[1], s->st));
-    run_moms2cums(s->M.get(), s->C.get(), s->ns, s->st);
+    run_moms2cums(s->M.get(), s->C.get(), s->ns, s->st, s->sh);
     CSB_CUDA(cudaEventRecord(s->ev[2], s->st));
     s->norms_valid = false;
     ++s->window;
     if (report) {
-      finalize_norms(s->C.get(), s->ns, s->st);
+      finalize_norms(s->C.get(), s->ns, s->st, s->sh);
       s->norms_valid = true;
       build_report(s->C.get(), s->ns, s->window, report);
     }
@@ -746,11 +835,12 @@ int csb_series_download(const csb_series* s, int order, double* host, uint64_t c
   });
 }
 
-static void moment_series_impl(csb_series* out, const double* xd, uint64_t rows, uint64_t) {
+static void moment_series_impl(csb_series* out, const double* xd, uint64_t rows, uint64_t,
+                               const ShardCtx& sh = ShardCtx{}) {
   RowSource src[2];
   src[0].seg0 = xd;
   src[0].len0 = static_cast<uint32_t>(rows);
-  run_moments(out, src, 1, rows, 0.0, out->dev->stream);
+  run_moments(out, src, 1, rows, 0.0, out->dev->stream, 0, sh);
   out->window_len = rows;
   g_rows_read.fetch_add(rows, std::memory_order_relaxed);
 }
@@ -911,6 +1001,16 @@ int csb_stream_prime(const csb_stream_config* cfg, const double* first, uint64_t
     s->cfg = *cfg;
     s->dev = &device();
     s->st = s->dev->stream;
+    if (cfg->shard_count > 1) {
+      if (cfg->shard_index < 0 || cfg->shard_index >= cfg->shard_count)
+        fail(CSB_EINVAL, "StreamConfig: shard_index must be in [0, shard_count)");
+      if (!s->dev->comm || s->dev->nranks != cfg->shard_count || s->dev->rank != cfg->shard_index)
+        fail(CSB_EINVAL, "prime: shard_count > 1 needs csb_comm_init(shard_count, shard_index, id) first");
+      s->splan = get_shard_plan(*s->dev, cfg->max_order, cfg->dim, cfg->block_size, cfg->shard_count);
+      s->sh.plan = s->splan.get();
+      s->sh.index = cfg->shard_index;
+      s->sh.comm = s->dev->comm;
+    }
     s->M = make_series(cfg->dim, cfg->max_order, cfg->block_size);
     s->C = make_series(cfg->dim, cfg->max_order, cfg->block_size);
     s->ring.alloc(rows * cols);
@@ -918,8 +1018,8 @@ int csb_stream_prime(const csb_stream_config* cfg, const double* first, uint64_t
     for (auto& e : s->ev) CSB_CUDA(cudaEventCreate(&e));
     CSB_CUDA(cudaMemcpyAsync(s->ring.ptr, first, s->ring.bytes(), cudaMemcpyHostToDevice, s->st));
     s->head = 0;
-    moment_series_impl(s->M.get(), s->ring.ptr, rows, cols);
-    run_moms2cums(s->M.get(), s->C.get(), s->ns, s->st);
+    moment_series_impl(s->M.get(), s->ring.ptr, rows, cols, s->sh);
+    run_moms2cums(s->M.get(), s->C.get(), s->ns, s->st, s->sh);
     s->window = 1;
     s->steps_since_resync = 0;
     CSB_CUDA(cudaStreamSynchronize(s->st));
@@ -945,7 +1045,7 @@ int csb_stream_report(csb_stream* s, csb_report* r) {
   return guard([&] {
     require(s && r, "stream_report: null argument");
     if (!s->norms_valid) {
-      finalize_norms(s->C.get(), s->ns, s->st);
+      finalize_norms(s->C.get(), s->ns, s->st, s->sh);
       s->norms_valid = true;
     }
     build_report(s->C.get(), s->ns, s->window, r);
@@ -996,7 +1096,89 @@ int csb_stream_norm_partials(csb_stream* s, int order, double* host, uint64_t co
     require(count == buf.count, "norm_partials: size mismatch");
     CSB_CUDA(cudaStreamSynchronize(s->st));
     CSB_CUDA(cudaMemcpy(host, buf.ptr, buf.bytes(), cudaMemcpyDeviceToHost));
-    if (first_block) *first_block = 0;
+    if (first_block) *first_block = (s->sh.active() && order == s->cfg.max_order) ? s->sh.lo(0) : 0;
+  });
+}
+
+int csb_comm_unique_id(unsigned char* out) {
+  return guard([&] {
+    require(out != nullptr, "comm_unique_id: null output");
+    nccl::get_unique_id(out);
+  });
+}
+
+int csb_comm_init(int nranks, int rank, const unsigned char* id) {
+  return guard([&] {
+    require(id != nullptr && nranks >= 1 && rank >= 0 && rank < nranks, "comm_init: bad arguments");
+    Device& dev = device();
+    if (dev.comm) nccl::comm_destroy(dev.comm);
+    dev.comm = nranks > 1 ? nccl::comm_init(nranks, rank, id) : nullptr;
+    dev.nranks = nranks;
+    dev.rank = rank;
+  });
+}
+
+int csb_comm_destroy(void) {
+  return guard([&] {
+    Device& dev = device();
+    if (dev.comm) nccl::comm_destroy(dev.comm);
+    dev.comm = nullptr;
+    dev.nranks = 1;
+    dev.rank = 0;
+  });
+}
+
+int csb_shard_range(int max_order, int dim, int block, int shard_index, int shard_count, int which,
+                    uint64_t* blk_lo, uint64_t* blk_hi, uint64_t* elem_lo, uint64_t* elem_hi) {
+  return guard([&] {
+    require(max_order >= 2 && max_order <= kMaxOrder, "shard_range: max_order must be in [2, 8]");
+    require(shard_count >= 1 && shard_index >= 0 && shard_index < shard_count, "shard_range: bad shard");
+    require(which == 0 || which == 1, "shard_range: which must be 0 (order d) or 1 (order d-1)");
+    Layout top(max_order, dim, block), low(max_order - 1, dim, block);
+    ShardPlan sp;
+    sp.build(max_order, dim, block, shard_count, top, low);
+    const auto& bl = which ? sp.low_blk : sp.top_blk;
+    const Layout& L = which ? low : top;
+    if (blk_lo) *blk_lo = bl[shard_index];
+    if (blk_hi) *blk_hi = bl[shard_index + 1];
+    if (elem_lo) *elem_lo = L.offset[bl[shard_index]];
+    if (elem_hi) *elem_hi = L.offset[bl[shard_index + 1]];
+  });
+}
+
+int csb_moments_update_shard(csb_series* m, const double* in, const double* outg, uint64_t rows, uint64_t cols,
+                             int shard_index, int shard_count) {
+  return guard([&] {
+    check_update(m, rows, cols);
+    require(shard_count >= 1 && shard_index >= 0 && shard_index < shard_count, "moments_update_shard: bad shard");
+    auto sp = get_shard_plan(*m->dev, m->d, m->n, m->b, shard_count);
+    ShardCtx sh{sp.get(), shard_index, nullptr};
+    DevBuf<double> xd(2 * rows * cols);
+    const uint64_t nb = rows * cols * sizeof(double);
+    CSB_CUDA(cudaMemcpyAsync(xd.ptr, in, nb, cudaMemcpyHostToDevice, m->dev->stream));
+    CSB_CUDA(cudaMemcpyAsync(xd.ptr + rows * cols, outg, nb, cudaMemcpyHostToDevice, m->dev->stream));
+    RowSource src[2];
+    src[0].seg0 = xd.ptr;
+    src[0].len0 = static_cast<uint32_t>(rows);
+    src[1].seg0 = xd.ptr + rows * cols;
+    src[1].len0 = static_cast<uint32_t>(rows);
+    run_moments(m, src, 2, rows, static_cast<double>(rows) / static_cast<double>(m->window_len), m->dev->stream, 0,
+                sh);
+    g_rows_read.fetch_add(2 * rows, std::memory_order_relaxed);
+    CSB_CUDA(cudaStreamSynchronize(m->dev->stream));
+  });
+}
+
+int csb_moms2cums_shard(const csb_series* m, csb_series* c, int shard_index, int shard_count) {
+  return guard([&] {
+    require(m && c, "moms2cums_shard: null series");
+    require(m->n == c->n && m->d == c->d && m->b == c->b, "moms2cums: series tensors disagree on shape");
+    require(shard_count >= 1 && shard_index >= 0 && shard_index < shard_count, "moms2cums_shard: bad shard");
+    auto sp = get_shard_plan(*m->dev, m->d, m->n, m->b, shard_count);
+    ShardCtx sh{sp.get(), shard_index, nullptr};
+    NormScratch ns;
+    run_moms2cums(m, c, ns, m->dev->stream, sh);
+    CSB_CUDA(cudaStreamSynchronize(m->dev->stream));
   });
 }
 
