@@ -73,4 +73,19 @@ inline uint64_t multiset_count(int a, int r) { return binom(a + r - 1, r); }
 
 void ensure_device();  // throws CSB_ERUNTIME without a usable CUDA device
 
+// Host -> device upload of metadata / user data that is COMPLETE when this
+// returns.  A plain cudaMemcpy from pageable memory may return before its DMA
+// lands, and the library's non-blocking streams do not order against the
+// legacy stream, so every such upload is followed by a device sync.
+inline void h2d_sync(void* dst, const void* src, std::size_t bytes) {
+  if (!bytes) return;
+  CSB_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+  CSB_CUDA(cudaDeviceSynchronize());
+}
+inline void memset_sync(void* dst, int v, std::size_t bytes) {
+  if (!bytes) return;
+  CSB_CUDA(cudaMemset(dst, v, bytes));
+  CSB_CUDA(cudaDeviceSynchronize());
+}
+
 }  // namespace csb

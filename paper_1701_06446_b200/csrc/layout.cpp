@@ -368,11 +368,11 @@ void MomentPlan::upload() {
   d_tiles.alloc(tiles.size());
   d_groups.alloc(groups.size());
   if (!groups.empty())
-    CSB_CUDA(cudaMemcpy(d_groups.ptr, groups.data(), d_groups.bytes(), cudaMemcpyHostToDevice));
+    h2d_sync(d_groups.ptr, groups.data(), d_groups.bytes());
   if (!rows.empty())
-    CSB_CUDA(cudaMemcpy(d_rows.ptr, rows.data(), d_rows.bytes(), cudaMemcpyHostToDevice));
+    h2d_sync(d_rows.ptr, rows.data(), d_rows.bytes());
   if (!tiles.empty())
-    CSB_CUDA(cudaMemcpy(d_tiles.ptr, tiles.data(), d_tiles.bytes(), cudaMemcpyHostToDevice));
+    h2d_sync(d_tiles.ptr, tiles.data(), d_tiles.bytes());
 }
 
 }  // namespace csb

@@ -109,10 +109,10 @@ std::shared_ptr<DevLayout> get_layout(Device& dev, int order, int n, int b) {
       for (int k = 0; k < order; ++k) j[k] = h.index[r * order + k];
       mult[r] = static_cast<double>(block_multiplicity(j, order));
     }
-    CSB_CUDA(cudaMemcpy(L->offset.ptr, h.offset.data(), L->offset.bytes(), cudaMemcpyHostToDevice));
-    CSB_CUDA(cudaMemcpy(L->index.ptr, h.index.data(), L->index.bytes(), cudaMemcpyHostToDevice));
-    CSB_CUDA(cudaMemcpy(L->prefix.ptr, h.prefix.data(), L->prefix.bytes(), cudaMemcpyHostToDevice));
-    CSB_CUDA(cudaMemcpy(L->mult.ptr, mult.data(), L->mult.bytes(), cudaMemcpyHostToDevice));
+    h2d_sync(L->offset.ptr, h.offset.data(), L->offset.bytes());
+    h2d_sync(L->index.ptr, h.index.data(), L->index.bytes());
+    h2d_sync(L->prefix.ptr, h.prefix.data(), L->prefix.bytes());
+    h2d_sync(L->mult.ptr, mult.data(), L->mult.bytes());
     std::vector<uint32_t> diag;
     for (uint64_t r = 0; r < h.nblocks; ++r) {
       bool runs = false;
@@ -123,7 +123,7 @@ std::shared_ptr<DevLayout> get_layout(Device& dev, int order, int n, int b) {
     L->diag_host = diag;
     L->diag.alloc(diag.size());
     if (!diag.empty())
-      CSB_CUDA(cudaMemcpy(L->diag.ptr, diag.data(), L->diag.bytes(), cudaMemcpyHostToDevice));
+      h2d_sync(L->diag.ptr, diag.data(), L->diag.bytes());
     slot = L;
   }
   return slot;
@@ -215,7 +215,7 @@ std::shared_ptr<DevBuf<LowerElem>> get_lower_elems(Device& dev, int s, int n, in
       for (int l = k; l < s; ++l) t[l] = val;
     }
     auto buf = std::make_shared<DevBuf<LowerElem>>(v.size());
-    CSB_CUDA(cudaMemcpy(buf->ptr, v.data(), buf->bytes(), cudaMemcpyHostToDevice));
+    h2d_sync(buf->ptr, v.data(), buf->bytes());
     slot = buf;
   }
   return slot;
@@ -289,14 +289,14 @@ struct Scratch {
   const double* get_zeros(uint64_t count) {
     if (zeros.count < count) {
       zeros.alloc(count);
-      CSB_CUDA(cudaMemset(zeros.ptr, 0, zeros.bytes()));
+      memset_sync(zeros.ptr, 0, zeros.bytes());
     }
     return zeros.ptr;
   }
   uint32_t* get_flags(uint64_t count) {
     if (flags.count < count) {
       flags.alloc(count);
-      CSB_CUDA(cudaMemset(flags.ptr, 0, flags.bytes()));
+      memset_sync(flags.ptr, 0, flags.bytes());
     }
     return flags.ptr;
   }
@@ -334,11 +334,16 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
   const int S = only_order ? only_order : d;
   Scratch& sc = g_scratch[dev.id];
   const bool lower = !only_order && d > 2;
+  static const bool serial_low = [] {
+    const char* e = std::getenv("CSB_SERIAL_LOW");  // debug: low orders on the main stream
+    return e && e[0] == '1';
+  }();
+  cudaStream_t side = serial_low ? st : dev.side;
   if (lower) {
     // orders <= d-2 on the side stream, concurrently with the top pair
     CSB_CUDA(cudaEventRecord(dev.fork, st));
-    CSB_CUDA(cudaStreamWaitEvent(dev.side, dev.fork, 0));
-    ProfScope ps("moment_low", dev.side);
+    CSB_CUDA(cudaStreamWaitEvent(side, dev.fork, 0));
+    ProfScope ps("moment_low", side);
     for (int s = 1; s <= d - 2; ++s) {
       auto el = get_lower_elems(dev, s, m->n, m->b, m->lay[s - 1]->host);
       LowerParams lp;
@@ -352,9 +357,9 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
       lp.m = m->data[s - 1].ptr;
       lp.c = c;
       lp.inv = 1.0 / static_cast<double>(K);
-      launch_moment_lower(s, lp, dev.side);
+      launch_moment_lower(s, lp, side);
     }
-    CSB_CUDA(cudaEventRecord(dev.join, dev.side));
+    CSB_CUDA(cudaEventRecord(dev.join, side));
   }
   {
     MomParams p;
@@ -490,12 +495,12 @@ DiagTables& diag_tables(const csb_series* c) {
         off[i] = c->lay[order - 1]->host.element_offset(idx);
       }
       t.off[q].alloc(c->n);
-      CSB_CUDA(cudaMemcpy(t.off[q].ptr, off.data(), t.off[q].bytes(), cudaMemcpyHostToDevice));
+      h2d_sync(t.off[q].ptr, off.data(), t.off[q].bytes());
     }
     std::vector<uint64_t> io(c->n);
     for (int i = 0; i < c->n; ++i) io[i] = static_cast<uint64_t>(i);
     t.iota.alloc(c->n);
-    CSB_CUDA(cudaMemcpy(t.iota.ptr, io.data(), t.iota.bytes(), cudaMemcpyHostToDevice));
+    h2d_sync(t.iota.ptr, io.data(), t.iota.bytes());
   }
   return t;
 }
@@ -822,7 +827,7 @@ int csb_series_upload(csb_series* s, int order, const double* host, uint64_t cou
   return guard([&] {
     check_order(s, order);
     require(count == s->lay[order - 1]->host.stored, "series_upload: size mismatch");
-    CSB_CUDA(cudaMemcpy(s->data[order - 1].ptr, host, count * sizeof(double), cudaMemcpyHostToDevice));
+    h2d_sync(s->data[order - 1].ptr, host, count * sizeof(double));
   });
 }
 
