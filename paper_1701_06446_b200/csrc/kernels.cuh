@@ -28,6 +28,7 @@ struct MomParams {
   double* scratch = nullptr;  // pass-0 stash (DMMA: per tile pair, both passes)
   uint32_t* flags = nullptr;  // DMMA: per tile pair arrival counters (self-resetting)
   const double* zeros = nullptr;  // DMMA: >= 32 x n zero doubles (tail rows of a pass)
+  int debug = 0;                  // timing experiments only (CSB_DMMA_DEBUG): 1 no row sums, 2 no products
   double* dtop = nullptr;         // DMMA update: canonical deltas of M_S (diagonal blocks)
   double* dlow = nullptr;         // DMMA update: canonical deltas of M_{S-1}
   double c = 0.0;             // p / T        (moments.cpp:287)

@@ -11,11 +11,9 @@
 // reference's row-ordered fma(A, x, acc) (moments.cpp:47) bit for bit.
 //
 // Work unit: a tile = 32 groups (pi, h) of 8 prefix rows (pi, 8h + g) x up
-// to 4 column groups of 8, for ONE pass (incoming or outgoing rows).  The
-// two passes of a tile pair run as independent CTAs; whichever finishes
-// second reads its partner's means from scratch and performs the fused
-// update M = fma(p/T, a - b, M) (moments.cpp:297) -- the result does not
-// depend on the order they finish.
+// to 4 column groups of 8.  A CTA streams the incoming rows, stashes their
+// means, streams the outgoing rows and applies the fused update
+// M = fma(p/T, a - b, M) (moments.cpp:297) to the canonical entries.
 //
 // Per CTA (4 warps): rows of the batch stream through a 4-stage shared
 // memory ring filled by cp.async.bulk (one TMA bulk copy per 32-row chunk,
@@ -137,9 +135,8 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // Consumer lane (r, q): fragment g of step t is aring[...][t][(r*4+q)*10+g]
 // (4 x LDS.128), B fragment c is x[k = 4 t + q][col0 + 8c + r].
 template <int LM1, int NC>
-__device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile, int pass, double* xs,
-                                         double* arings, uint64_t* xfull, uint64_t* xempty, uint64_t* afull,
-                                         uint64_t* aempty, uint32_t* flag_smem) {
+__device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile, double* xs, double* arings,
+                                         uint64_t* xfull, uint64_t* xempty, uint64_t* afull, uint64_t* aempty) {
   constexpr int L = LM1 + 1;
   const int n = P.n, b = P.b;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -151,8 +148,8 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
   const bool do_low = (P.low != nullptr) && tile.low;
   const size_t stage_elems = static_cast<size_t>(KC) * n;
   const uint32_t K = P.K;
-  const uint32_t chunks = (K + KC - 1) / KC;
-  const RowSource& src = P.src[pass];
+  const uint32_t cpp = (K + KC - 1) / KC;  // chunks per pass
+  const uint32_t chunks = cpp * P.npass;   // incoming pass, then outgoing pass
   double* aring = arings + static_cast<size_t>(pw) * 2 * ASLOT;
 
   // ---- TMA producer: lane 0 of the first producer warp ----
@@ -169,7 +166,8 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
           mbar_wait(xempty + st, par);
         }
       }
-      const uint32_t a0 = i * KC;
+      const RowSource& src = P.src[i / cpp];
+      const uint32_t a0 = (i % cpp) * KC;
       const uint32_t kc = min(static_cast<uint32_t>(KC), K - a0);
       double* dst = xs + st * stage_elems;
       const uint32_t rb = static_cast<uint32_t>(n) * 8u;
@@ -194,16 +192,15 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
   const DmmaGroup grp = P.groups[gi];
   const int lo = grp.lo;
   const bool update = P.npass == 2;
-  const size_t pair = tile.pad1;
-  constexpr size_t PASS_STRIDE = CWARPS * 32 * 64 + CWARPS * 32 * 2;
-  double* base = update ? P.scratch + pair * (2 * PASS_STRIDE) : nullptr;
+  // pass-0 means of the consumer threads (the producers keep theirs in registers)
+  double* stash = P.scratch + static_cast<size_t>(blockIdx.x) * (CWARPS * 32 * 64);
 
   if (producer) {
     int pidx[LM1 > 0 ? LM1 : 1];
 #pragma unroll
     for (int t = 0; t < LM1; ++t) pidx[t] = grp.pidx[t];
     const int gp = q4;
-    double lowacc[2] = {0.0, 0.0};
+    double lowacc[2] = {0.0, 0.0}, lowin[2] = {0.0, 0.0};
     for (uint32_t c = 0; c < chunks; ++c) {
       const uint32_t st = c % STAGES;
       if (warp == CWARPS) pump(c);
@@ -225,8 +222,15 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
 #pragma unroll
             for (int t2 = 1; t2 < LM1; ++t2) Pv = __dmul_rn(Pv, xr[pidx[t2]]);
             const double2 xv = *reinterpret_cast<const double2*>(xr + h8 + 2 * gp);
-            const double a0 = __dmul_rn(Pv, xv.x), a1 = __dmul_rn(Pv, xv.y);
-            if (do_low) {
+            double a0, a1;
+            if (P.debug & 2) {
+              a0 = xv.x;
+              a1 = xv.y;
+            } else {
+              a0 = __dmul_rn(Pv, xv.x);
+              a1 = __dmul_rn(Pv, xv.y);
+            }
+            if (do_low && !(P.debug & 1)) {
               lowacc[0] = __dadd_rn(lowacc[0], a0);  // row order, plain adds (moments.cpp:44)
               lowacc[1] = __dadd_rn(lowacc[1], a1);
             }
@@ -238,20 +242,13 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
       __syncwarp();
       if (lane == 0) mbar_arrive(xempty + st);
       if (warp == CWARPS) pump(0);
+      if (update && c + 1 == cpp) {  // end of the incoming pass
+        lowin[0] = __dmul_rn(lowacc[0], P.inv);
+        lowin[1] = __dmul_rn(lowacc[1], P.inv);
+        lowacc[0] = lowacc[1] = 0.0;
+      }
     }
     // ---- producer epilogue: order L (= d-1) ----
-    if (update) {
-      double* mine = base + pass * PASS_STRIDE + CWARPS * 32 * 64;
-      mine[pw * 32 + lane] = __dmul_rn(lowacc[0], P.inv);
-      mine[CWARPS * 32 + pw * 32 + lane] = __dmul_rn(lowacc[1], P.inv);
-    }
-    if (update) {
-      // same two barriers as the consumers' fixup (thread 0 takes the ticket)
-      __threadfence();
-      __syncthreads();
-      __syncthreads();
-      if (*flag_smem == 0) return;
-    }
     if (!gvalid || !do_low) return;
     const double cc = P.c;
 #pragma unroll
@@ -261,9 +258,7 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
       if (g < lo || iL >= n) continue;
       const PrefixRow& pr = P.rows[static_cast<size_t>(gi) * 8 + g];
       if (update) {
-        const size_t ix = CWARPS * 32 * 64 + static_cast<size_t>(e) * CWARPS * 32 + pw * 32 + lane;
-        const double mv = base[pass * PASS_STRIDE + ix], ov = __ldcg(base + (pass ^ 1) * PASS_STRIDE + ix);
-        const double delta = pass == 0 ? __dsub_rn(mv, ov) : __dsub_rn(ov, mv);  // a - b
+        const double delta = __dsub_rn(lowin[e], __dmul_rn(lowacc[e], P.inv));  // a - b
         P.low[pr.low_off] = __fma_rn(cc, delta, P.low[pr.low_off]);
         if (pr.idx[7] & 1u) P.dlow[pr.low_off] = delta;
       } else {
@@ -316,30 +311,22 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(xempty + st);
+    if (update && c + 1 == cpp) {
+      // end of the incoming pass: stash its means, restart the accumulators
+      const int tid = pw * 32 + lane;
+#pragma unroll
+      for (int g = 0; g < 8; ++g)
+#pragma unroll
+        for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            stash[static_cast<size_t>((g * NC + cc) * 2 + e) * (CWARPS * 32) + tid] = __dmul_rn(acc[g][cc][e], P.inv);
+            acc[g][cc][e] = 0.0;
+          }
+    }
   }
 
-  // ---- pair fixup: the second of (incoming, outgoing) does the update ----
   const int tid = pw * 32 + lane;  // consumer thread index
-  double* mine = nullptr;
-  const double* other = nullptr;
-  if (update) {
-    mine = base + pass * PASS_STRIDE;
-    other = base + (pass ^ 1) * PASS_STRIDE;
-#pragma unroll
-    for (int g = 0; g < 8; ++g)
-#pragma unroll
-      for (int c = 0; c < NC; ++c)
-#pragma unroll
-        for (int e = 0; e < 2; ++e)
-          mine[static_cast<size_t>((g * NC + c) * 2 + e) * (CWARPS * 32) + tid] = __dmul_rn(acc[g][c][e], P.inv);
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) *flag_smem = atomicAdd(P.flags + pair, 1u);
-    __syncthreads();
-    if (*flag_smem == 0) return;  // partner still running: it finishes the pair
-    __threadfence();
-    if (threadIdx.x == 0) P.flags[pair] = 0;  // self-resetting for the next launch
-  }
 
   // ---- epilogue: canonical entries only ----
   // Entries of blocks with equal neighbouring coordinates have symmetric
@@ -370,9 +357,7 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
                     static_cast<uint64_t>(pr.poff) * ext_of(jd, n, b) + (col - jd * b);
         if (update) {
           const size_t ix = static_cast<size_t>((g * NC + c) * 2 + e) * (CWARPS * 32) + tid;
-          const double mv = mine[ix];
-          const double ov = ok[c][e] ? __ldcg(other + ix) : 0.0;
-          val[c][e] = pass == 0 ? __dsub_rn(mv, ov) : __dsub_rn(ov, mv);  // a - b
+          val[c][e] = __dsub_rn(stash[ix], __dmul_rn(acc[g][c][e], P.inv));  // a - b
         } else {
           val[c][e] = __dmul_rn(acc[g][c][e], P.inv);
         }
@@ -407,13 +392,11 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
   __shared__ __align__(8) uint64_t xempty[STAGES];
   __shared__ __align__(8) uint64_t afull[CWARPS * 2];
   __shared__ __align__(8) uint64_t aempty[CWARPS * 2];
-  __shared__ uint32_t flag_smem;
   double* xs = smem;
   // dense staging ring; reads past row n of a stage (the last 8-column
   // window / column group) only feed rows and columns that are never stored
   double* arings = xs + static_cast<size_t>(STAGES) * KC * P.n + 64;  // CWARPS x 2 x ASLOT
-  const int pass = static_cast<int>(blockIdx.x % P.npass);
-  const MomTile tile = P.tiles[blockIdx.x / P.npass];
+  const MomTile tile = P.tiles[blockIdx.x];
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(xfull + s, 1);
@@ -430,7 +413,7 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
   switch (P.L * 8 + nc) {
 #define CSB_CASE(LL, NCC) \
   case (LL) * 8 + (NCC): \
-    run_tile<(LL) - 1, NCC>(P, tile, pass, xs, arings, xfull, xempty, afull, aempty, &flag_smem); break;
+    run_tile<(LL) - 1, NCC>(P, tile, xs, arings, xfull, xempty, afull, aempty); break;
 #define CSB_CASES(LL) CSB_CASE(LL, 1) CSB_CASE(LL, 2) CSB_CASE(LL, 3) CSB_CASE(LL, 4)
     CSB_CASES(2) CSB_CASES(3) CSB_CASES(4) CSB_CASES(5)
 #undef CSB_CASES
@@ -496,9 +479,8 @@ size_t smem_bytes(int n) {
 
 int dmma_warps() { return CWARPS; }
 
-// per tile pair: both passes' stashes (64 values per consumer thread + 2
-// row sums per producer thread)
-size_t dmma_scratch_per_tile() { return static_cast<size_t>(2) * (CWARPS * 32 * 64 + CWARPS * 32 * 2); }
+// per tile: the incoming pass's means (64 values per consumer thread)
+size_t dmma_scratch_per_tile() { return static_cast<size_t>(CWARPS) * 32 * 64; }
 
 bool dmma_supported(const MomParams& p) {
   // instantiated for orders 3..6 (L = 2..5); the staging ring must fit
@@ -526,7 +508,7 @@ void launch_moment_top_dmma(const MomParams& p, int ntiles, cudaStream_t st) {
   const size_t smem = smem_bytes(p.n);
   CSB_CUDA(cudaFuncSetAttribute(moment_top_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
-  moment_top_dmma_kernel<<<ntiles * p.npass, THREADS, smem, st>>>(p);
+  moment_top_dmma_kernel<<<ntiles, THREADS, smem, st>>>(p);
   CSB_CUDA(cudaGetLastError());
   count_launch();
 }

@@ -387,6 +387,11 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
     if (npass == 2 || use_dmma) p.scratch = sc.get(ntiles * plan->scratch_per_tile);
     ProfScope ps("moment_top", st);
     if (use_dmma) {
+      static const int dbg = [] {
+        const char* e = std::getenv("CSB_DMMA_DEBUG");
+        return e ? std::atoi(e) : 0;
+      }();
+      p.debug = dbg;
       p.flags = sc.get_flags(ntiles);
       p.zeros = sc.get_zeros(32ull * m->n);
       if (npass == 2) {
