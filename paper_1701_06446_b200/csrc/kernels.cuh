@@ -31,6 +31,10 @@ struct MomParams {
   int debug = 0;                  // timing experiments only (CSB_DMMA_DEBUG): 1 no row sums, 2 no products
   double* dtop = nullptr;         // DMMA update: canonical deltas of M_S (diagonal blocks)
   double* dlow = nullptr;         // DMMA update: canonical deltas of M_{S-1}
+  // DMMA, unsharded: orders 1..S-2 from the representative groups
+  const uint64_t* rep_off = nullptr;  // MomentPlan::rep_off (nullptr: not computed here)
+  double* lower[4] = {nullptr, nullptr, nullptr, nullptr};   // M_1 .. M_{S-2}
+  double* dlower[4] = {nullptr, nullptr, nullptr, nullptr};  // their canonical deltas (update)
   double c = 0.0;             // p / T        (moments.cpp:287)
   double inv = 1.0;           // 1.0 / rows   (moments.cpp:148)
 };

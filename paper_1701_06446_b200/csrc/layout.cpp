@@ -242,7 +242,8 @@ int ShardPlan::owner(const int* jp) const {
 }
 
 void MomentPlan::build_dmma(int S_, int n_, int b_, const Layout& top, const Layout* low, int warps,
-                            uint64_t scratch, const ShardPlan* shard, int shard_index) {
+                            uint64_t scratch, const ShardPlan* shard, int shard_index,
+                            const Layout* const* lowers) {
   S = S_;
   L = S_ - 1;
   n = n_;
@@ -250,6 +251,7 @@ void MomentPlan::build_dmma(int S_, int n_, int b_, const Layout& top, const Lay
   rows.clear();
   tiles.clear();
   groups.clear();
+  rep_off.clear();
   dmma = true;
   require(L >= 1 && L <= 7, "build_dmma: order out of range");
   const int LM1 = L - 1;
@@ -288,6 +290,25 @@ void MomentPlan::build_dmma(int S_, int n_, int b_, const Layout& top, const Lay
       for (int k = 0; k < 6; ++k) g.pidx[k] = pi[k];
       g.lo = static_cast<uint16_t>(std::max(0, last - 8 * h));
       g.h = static_cast<uint16_t>(h);
+      if (lowers && LM1 > 0 && last / 8 == h) {
+        // depths s whose tuple this group represents: pi_{s+1..} == pi_s
+        for (int sd = 1; sd <= LM1; ++sd) {
+          bool rep = true;
+          for (int k = sd; k < LM1; ++k) rep &= pi[k] == pi[sd - 1];
+          if (!rep) continue;
+          const Layout& Ls = *lowers[sd - 1];
+          int tup[8], jb[8];
+          bool runs = false;
+          for (int k = 0; k < sd; ++k) {
+            tup[k] = pi[k];
+            jb[k] = pi[k] / b;
+            if (k > 0) runs |= jb[k] == jb[k - 1];
+          }
+          if (!g.rep_mask) g.rep = static_cast<uint32_t>(rep_off.size());
+          g.rep_mask |= 1u << (sd - 1);
+          rep_off.push_back(Ls.element_offset(tup) | (runs ? (1ull << 63) : 0ull));
+        }
+      }
       groups.push_back(g);
       int t[8];
       for (int k = 0; k < LM1; ++k) t[k] = pi[k];
@@ -367,6 +388,8 @@ void MomentPlan::upload() {
   d_rows.alloc(rows.size());
   d_tiles.alloc(tiles.size());
   d_groups.alloc(groups.size());
+  d_rep_off.alloc(rep_off.size());
+  if (!rep_off.empty()) h2d_sync(d_rep_off.ptr, rep_off.data(), d_rep_off.bytes());
   if (!groups.empty())
     h2d_sync(d_groups.ptr, groups.data(), d_groups.bytes());
   if (!rows.empty())

@@ -55,12 +55,21 @@ static_assert(sizeof(PrefixRow) == 48, "PrefixRow layout");
 // One group of 8 prefix rows (pi, 8h + g), g = 0..7, for the DMMA kernel:
 // pi = (i_1..i_{L-1}); rows with g < lo (i_L < i_{L-1}) or 8h + g >= n are
 // not canonical and are masked.
+//
+// A group may also represent lower-order elements: its prefix products at
+// depth s (x[pi_1] ... x[pi_s]) are the order-s moment products of the
+// tuple (pi_1..pi_s); the group (pi_1..pi_s, pi_s, ..., pi_s) in its first
+// window h = pi_s / 8 is that tuple's unique representative (rep_mask bit
+// s-1), so the producer warps compute every order <= d-2 as well.
 struct DmmaGroup {
   uint16_t pidx[6];
   uint16_t lo;
   uint16_t h;
+  uint32_t rep;       // first entry in MomentPlan::rep_off (valid when rep_mask != 0)
+  uint32_t rep_mask;  // bit s-1: this group represents order-s tuple (pi_1..pi_s)
+  uint32_t pad[2];
 };
-static_assert(sizeof(DmmaGroup) == 16, "DmmaGroup layout");
+static_assert(sizeof(DmmaGroup) == 32, "DmmaGroup layout");
 
 struct MomTile {
   uint32_t row0, nrows;  // range in the row table
@@ -96,12 +105,17 @@ struct MomentPlan {
   bool dmma = false;  // tiles are for moment_top_dmma_kernel (pad0 = column groups)
   std::vector<DmmaGroup> groups;
   DevBuf<DmmaGroup> d_groups;
+  std::vector<uint64_t> rep_off;  // canonical offset in M_s (bit 63: block has copies)
+  DevBuf<uint64_t> d_rep_off;
   void build(int S, int n, int b, const Layout& top, const Layout* low, int threads);
   // Tiles for the DMMA kernel: groups (pi, h) of 8 prefix rows, 8 groups per
   // warp; columns [8h, n) in ranges of at most 4 groups of 8; rows[8 g + r]
   // is the PrefixRow of row r of group g (zero for masked rows).
+  // lowers[s-1] = layout of order s (s <= S-2) when the groups should also
+  // compute the lower orders (unsharded plans), nullptr otherwise
   void build_dmma(int S, int n, int b, const Layout& top, const Layout* low, int warps,
-                  uint64_t scratch_per_tile, const ShardPlan* shard = nullptr, int shard_index = 0);
+                  uint64_t scratch_per_tile, const ShardPlan* shard = nullptr, int shard_index = 0,
+                  const Layout* const* lowers = nullptr);
   void upload();
 
  private:

@@ -201,6 +201,11 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
     for (int t = 0; t < LM1; ++t) pidx[t] = grp.pidx[t];
     const int gp = q4;
     double lowacc[2] = {0.0, 0.0}, lowin[2] = {0.0, 0.0};
+    // lower orders: lane gp accumulates depth gp + 1 of the prefix chain
+    // (the order-(gp+1) product of (pi_1..pi_{gp+1})) when the group
+    // represents that tuple; other lanes' sums are discarded
+    const bool rep = do_low && P.rep_off != nullptr && gp < LM1 && ((grp.rep_mask >> gp) & 1u);
+    double repacc = 0.0, repin = 0.0;
     for (uint32_t c = 0; c < chunks; ++c) {
       const uint32_t st = c % STAGES;
       if (warp == CWARPS) pump(c);
@@ -219,8 +224,13 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
           for (int q = 0; q < 4; ++q) {
             const double* xr = xst + static_cast<size_t>(hc * 4 * HSTEPS + 4 * t + q) * n;
             double Pv = xr[pidx[0]];
+            double Ps = Pv;
 #pragma unroll
-            for (int t2 = 1; t2 < LM1; ++t2) Pv = __dmul_rn(Pv, xr[pidx[t2]]);
+            for (int t2 = 1; t2 < LM1; ++t2) {
+              Pv = __dmul_rn(Pv, xr[pidx[t2]]);
+              if (gp >= t2) Ps = Pv;
+            }
+            if (LM1 > 0) repacc = __dadd_rn(repacc, Ps);  // row order, plain adds (moments.cpp:44)
             const double2 xv = *reinterpret_cast<const double2*>(xr + h8 + 2 * gp);
             double a0, a1;
             if (P.debug & 2) {
@@ -246,6 +256,20 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
         lowin[0] = __dmul_rn(lowacc[0], P.inv);
         lowin[1] = __dmul_rn(lowacc[1], P.inv);
         lowacc[0] = lowacc[1] = 0.0;
+        repin = __dmul_rn(repacc, P.inv);
+        repacc = 0.0;
+      }
+    }
+    if (rep && gvalid) {  // order gp + 1, canonical element (pi_1..pi_{gp+1})
+      const uint64_t e = P.rep_off[grp.rep + __popc(grp.rep_mask & ((1u << gp) - 1u))];
+      const uint64_t off = e & ~(1ull << 63);
+      double* Ms = P.lower[gp];
+      if (update) {
+        const double delta = __dsub_rn(repin, __dmul_rn(repacc, P.inv));
+        Ms[off] = __fma_rn(P.c, delta, Ms[off]);
+        if (e >> 63) P.dlower[gp][off] = delta;
+      } else {
+        Ms[off] = __dmul_rn(repacc, P.inv);
       }
     }
     // ---- producer epilogue: order L (= d-1) ----

@@ -56,8 +56,6 @@ struct DevLayout {
 struct Device {
   int id = 0;
   cudaStream_t stream = nullptr;
-  cudaStream_t side = nullptr;  // low-order moments overlap the top kernel
-  cudaEvent_t fork = nullptr, join = nullptr;
   std::mutex mu;
   std::map<std::tuple<int, int, int>, std::shared_ptr<DevLayout>> layouts;
   std::map<std::tuple<int, int, int, int>, std::shared_ptr<MomentPlan>> plans;
@@ -85,9 +83,6 @@ Device& device() {
     slot = std::make_unique<Device>();
     slot->id = id;
     CSB_CUDA(cudaStreamCreateWithFlags(&slot->stream, cudaStreamNonBlocking));
-    CSB_CUDA(cudaStreamCreateWithFlags(&slot->side, cudaStreamNonBlocking));
-    CSB_CUDA(cudaEventCreateWithFlags(&slot->fork, cudaEventDisableTiming));
-    CSB_CUDA(cudaEventCreateWithFlags(&slot->join, cudaEventDisableTiming));
   }
   return *slot;
 }
@@ -147,13 +142,21 @@ std::shared_ptr<MomentPlan> get_plan(Device& dev, int S, int n, int b, bool dmma
   auto top = get_layout(dev, S, n, b);
   std::shared_ptr<DevLayout> low = S > 1 ? get_layout(dev, S - 1, n, b) : nullptr;
   const int count = sp ? sp->count : 1;
+  // unsharded DMMA plans also carry the lower orders' representative groups
+  std::vector<std::shared_ptr<DevLayout>> lows;
+  std::vector<const Layout*> lowp;
+  if (dmma && !sp)
+    for (int s = 1; s <= S - 2; ++s) {
+      lows.push_back(get_layout(dev, s, n, b));
+      lowp.push_back(&lows.back()->host);
+    }
   std::lock_guard<std::mutex> lk(dev.mu);
   auto& slot = dev.plans[{S, n, b, (dmma ? 1 : 0) + 2 * (count * 256 + shard_index)}];
   if (!slot) {
     auto p = std::make_shared<MomentPlan>();
     if (dmma)
       p->build_dmma(S, n, b, top->host, low ? &low->host : nullptr, dmma_warps(), dmma_scratch_per_tile(), sp,
-                    shard_index);
+                    shard_index, lowp.empty() ? nullptr : lowp.data());
     else
       p->build(S, n, b, top->host, low ? &low->host : nullptr, kMomThreads);
     p->upload();
@@ -282,6 +285,7 @@ struct Scratch {
   }
   DevBuf<double> zeros;
   DevBuf<double> dtop, dlow;
+  DevBuf<double> dlower[4];
   double* get_delta(DevBuf<double>& d, uint64_t count) {
     if (d.count < count) d.alloc(count);
     return d.ptr;
@@ -334,16 +338,33 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
   const int S = only_order ? only_order : d;
   Scratch& sc = g_scratch[dev.id];
   const bool lower = !only_order && d > 2;
-  static const bool serial_low = [] {
-    const char* e = std::getenv("CSB_SERIAL_LOW");  // debug: low orders on the main stream
+  MomParams p;
+  p.src[0] = src[0];
+  p.src[1] = src[1];
+  p.npass = npass;
+  p.K = static_cast<uint32_t>(K);
+  p.n = m->n;
+  p.b = m->b;
+  p.L = S - 1;
+  p.top = m->data[S - 1].ptr;
+  p.low = (S > 1 && !only_order) ? m->data[S - 2].ptr : nullptr;
+  p.c = c;
+  p.inv = 1.0 / static_cast<double>(K);
+  // the top pair runs on the FP64 tensor cores when the rows allow TMA
+  // bulk copies; otherwise on the DFMA kernel
+  const bool use_dmma = g_use_dmma && dmma_supported(p);
+  // sharding applies to the DMMA plan (the DFMA fallback computes all blocks)
+  const bool sharded = use_dmma && sh.active() && !only_order;
+  // unsharded DMMA: the producer warps also compute orders <= d-2
+  static const bool no_fuse = [] {
+    const char* e = std::getenv("CSB_NO_FUSED_LOW");  // A/B: separate lower-order kernel
     return e && e[0] == '1';
   }();
-  cudaStream_t side = serial_low ? st : dev.side;
-  if (lower) {
-    // orders <= d-2 on the side stream, concurrently with the top pair
-    CSB_CUDA(cudaEventRecord(dev.fork, st));
-    CSB_CUDA(cudaStreamWaitEvent(side, dev.fork, 0));
-    ProfScope ps("moment_low", side);
+  const bool fused_lower = lower && use_dmma && !sharded && !no_fuse;
+  if (lower && !fused_lower) {
+    // orders <= d-2: element-parallel kernel, ahead of the top pair on the
+    // same stream (concurrent CTAs would hold SMs the DMMA tiles need)
+    ProfScope ps("moment_low", st);
     for (int s = 1; s <= d - 2; ++s) {
       auto el = get_lower_elems(dev, s, m->n, m->b, m->lay[s - 1]->host);
       LowerParams lp;
@@ -357,28 +378,10 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
       lp.m = m->data[s - 1].ptr;
       lp.c = c;
       lp.inv = 1.0 / static_cast<double>(K);
-      launch_moment_lower(s, lp, side);
+      launch_moment_lower(s, lp, st);
     }
-    CSB_CUDA(cudaEventRecord(dev.join, side));
   }
   {
-    MomParams p;
-    p.src[0] = src[0];
-    p.src[1] = src[1];
-    p.npass = npass;
-    p.K = static_cast<uint32_t>(K);
-    p.n = m->n;
-    p.b = m->b;
-    p.L = S - 1;
-    p.top = m->data[S - 1].ptr;
-    p.low = (S > 1 && !only_order) ? m->data[S - 2].ptr : nullptr;
-    p.c = c;
-    p.inv = 1.0 / static_cast<double>(K);
-    // the top pair runs on the FP64 tensor cores when the rows allow TMA
-    // bulk copies; otherwise on the DFMA kernel
-    const bool use_dmma = g_use_dmma && dmma_supported(p);
-    // sharding applies to the DMMA plan (the DFMA fallback computes all blocks)
-    const bool sharded = use_dmma && sh.active() && !only_order;
     auto plan = get_plan(dev, S, m->n, m->b, use_dmma, sharded ? sh.plan : nullptr, sharded ? sh.index : 0);
     p.rows = plan->d_rows.ptr;
     p.tiles = plan->d_tiles.ptr;
@@ -398,7 +401,20 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
         p.dtop = sc.get_delta(sc.dtop, m->lay[S - 1]->host.stored);
         if (p.low) p.dlow = sc.get_delta(sc.dlow, m->lay[S - 2]->host.stored);
       }
+      if (fused_lower) {
+        p.rep_off = plan->d_rep_off.ptr;
+        for (int s = 1; s <= d - 2; ++s) {
+          p.lower[s - 1] = m->data[s - 1].ptr;
+          if (npass == 2) p.dlower[s - 1] = sc.get_delta(sc.dlower[s - 1], m->lay[s - 1]->host.stored);
+        }
+      }
       launch_moment_top_dmma(p, static_cast<int>(ntiles), st);
+      if (fused_lower)
+        for (int s = 2; s <= d - 2; ++s) {
+          const auto& Ls = m->lay[s - 1];
+          launch_mirror(s, p.lower[s - 1], p.dlower[s - 1], Ls->view(), Ls->diag.ptr, Ls->ndiag, m->n, m->b,
+                        npass == 2, c, st);
+        }
       const auto& LT = m->lay[S - 1];
       auto rt = sharded ? LT->diag_range(sh.lo(0), sh.hi(0)) : std::make_pair(0u, LT->ndiag);
       launch_mirror(S, p.top, p.dtop, LT->view(), LT->diag.ptr + rt.first, rt.second, m->n, m->b, npass == 2, c, st);
@@ -423,7 +439,6 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
       launch_moment_pair(p, static_cast<int>(ntiles), true, st);
     }
   }
-  if (lower) CSB_CUDA(cudaStreamWaitEvent(st, dev.join, 0));
 }
 
 void check_batch(uint64_t rows, uint64_t cols, const char* what) {
