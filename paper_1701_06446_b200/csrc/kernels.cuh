@@ -22,19 +22,14 @@ struct MomParams {
   int n = 0, b = 0, L = 0;
   const PrefixRow* rows = nullptr;
   const MomTile* tiles = nullptr;
-  const DmmaGroup* groups = nullptr;  // DMMA kernel only
+  const DmmaPair* pairs = nullptr;  // DMMA kernel only
   double* top = nullptr;      // M_S
   double* low = nullptr;      // M_{S-1} (nullptr: not written)
-  double* scratch = nullptr;  // pass-0 stash (DMMA: per tile pair, both passes)
-  uint32_t* flags = nullptr;  // DMMA: per tile pair arrival counters (self-resetting)
-  const double* zeros = nullptr;  // DMMA: >= 32 x n zero doubles (tail rows of a pass)
-  int debug = 0;                  // timing experiments only (CSB_DMMA_DEBUG): 1 no row sums, 2 no products
+  double* scratch = nullptr;  // pass-0 stash (DMMA: per tile)
+  const double* zeros = nullptr;  // DMMA: >= 16 x n zero doubles (tail rows of a pass)
+  int stages = 0;                 // DMMA: row-chunk stages in shared memory
   double* dtop = nullptr;         // DMMA update: canonical deltas of M_S (diagonal blocks)
   double* dlow = nullptr;         // DMMA update: canonical deltas of M_{S-1}
-  // DMMA, unsharded: orders 1..S-2 from the representative groups
-  const uint64_t* rep_off = nullptr;  // MomentPlan::rep_off (nullptr: not computed here)
-  double* lower[4] = {nullptr, nullptr, nullptr, nullptr};   // M_1 .. M_{S-2}
-  double* dlower[4] = {nullptr, nullptr, nullptr, nullptr};  // their canonical deltas (update)
   double c = 0.0;             // p / T        (moments.cpp:287)
   double inv = 1.0;           // 1.0 / rows   (moments.cpp:148)
 };
@@ -107,7 +102,6 @@ void count_launch();
 
 // FP64 tensor-core (DMMA) kernel for the top pair of orders (moment_dmma.cu)
 bool dmma_supported(const MomParams& p);
-int dmma_warps();
 size_t dmma_scratch_per_tile();
 void launch_moment_top_dmma(const MomParams& p, int ntiles, cudaStream_t st);
 // copies of canonical entries in blocks with runs (after the DMMA kernel)

@@ -241,110 +241,97 @@ int ShardPlan::owner(const int* jp) const {
   return shard_of_prefix[prefix_rank->rank(jp)];
 }
 
-void MomentPlan::build_dmma(int S_, int n_, int b_, const Layout& top, const Layout* low, int warps,
-                            uint64_t scratch, const ShardPlan* shard, int shard_index,
-                            const Layout* const* lowers) {
+void MomentPlan::build_dmma(int S_, int n_, int b_, const Layout& top, const Layout* low, uint64_t scratch,
+                            const ShardPlan* shard, int shard_index) {
   S = S_;
   L = S_ - 1;
   n = n_;
   b = b_;
   rows.clear();
   tiles.clear();
-  groups.clear();
-  rep_off.clear();
+  pairs.clear();
   dmma = true;
-  require(L >= 1 && L <= 7, "build_dmma: order out of range");
+  require(L >= 2 && L <= 7, "build_dmma: order out of range");
   const int LM1 = L - 1;
-  // all (L-1)-tuples pi in lexicographic order (one empty tuple when L == 1)
+  // all (L-1)-tuples pi in lexicographic order
   std::vector<std::array<uint16_t, 6>> pis;
   {
     int t[8] = {0};
-    if (LM1 == 0) {
-      pis.push_back({});
-    } else {
-      for (;;) {
-        std::array<uint16_t, 6> a{};
-        for (int k = 0; k < LM1; ++k) a[k] = static_cast<uint16_t>(t[k]);
-        pis.push_back(a);
-        int k = LM1 - 1;
-        while (k >= 0 && t[k] == n - 1) --k;
-        if (k < 0) break;
-        const int v = t[k] + 1;
-        for (int l = k; l < LM1; ++l) t[l] = v;
-      }
+    for (;;) {
+      std::array<uint16_t, 6> a{};
+      for (int k = 0; k < LM1; ++k) a[k] = static_cast<uint16_t>(t[k]);
+      pis.push_back(a);
+      int k = LM1 - 1;
+      while (k >= 0 && t[k] == n - 1) --k;
+      if (k < 0) break;
+      const int v = t[k] + 1;
+      for (int l = k; l < LM1; ++l) t[l] = v;
     }
   }
   const int nh = (n + 7) / 8;
-  const int per_tile = warps * 8;  // groups per CTA
   for (int h = 0; h < nh; ++h) {
-    const uint32_t g0 = static_cast<uint32_t>(groups.size());
+    const int hi = std::min(8 * h + 8, n);
+    const uint32_t rs0 = static_cast<uint32_t>(pairs.size() / 32);
+    int t[8];
     for (const auto& pi : pis) {
-      const int last = LM1 > 0 ? pi[LM1 - 1] : 0;
-      if (last > 8 * h + 7) continue;  // every row of this group has i_L < i_{L-1}
+      const int last = pi[LM1 - 1];
+      if (last >= hi) continue;  // every row of this window has i_L < i_{L-1}
       if (shard && shard->count > 1) {
         int jp[3] = {0, 0, 0};
         for (int k = 0; k < shard->plen; ++k) jp[k] = pi[k] / b;
         if (shard->owner(jp) != shard_index) continue;  // another shard's blocks
       }
-      DmmaGroup g{};
-      for (int k = 0; k < 6; ++k) g.pidx[k] = pi[k];
-      g.lo = static_cast<uint16_t>(std::max(0, last - 8 * h));
-      g.h = static_cast<uint16_t>(h);
-      if (lowers && LM1 > 0 && last / 8 == h) {
-        // depths s whose tuple this group represents: pi_{s+1..} == pi_s
-        for (int sd = 1; sd <= LM1; ++sd) {
-          bool rep = true;
-          for (int k = sd; k < LM1; ++k) rep &= pi[k] == pi[sd - 1];
-          if (!rep) continue;
-          const Layout& Ls = *lowers[sd - 1];
-          int tup[8], jb[8];
-          bool runs = false;
-          for (int k = 0; k < sd; ++k) {
-            tup[k] = pi[k];
-            jb[k] = pi[k] / b;
-            if (k > 0) runs |= jb[k] == jb[k - 1];
-          }
-          if (!g.rep_mask) g.rep = static_cast<uint32_t>(rep_off.size());
-          g.rep_mask |= 1u << (sd - 1);
-          rep_off.push_back(Ls.element_offset(tup) | (runs ? (1ull << 63) : 0ull));
-        }
-      }
-      groups.push_back(g);
-      int t[8];
       for (int k = 0; k < LM1; ++k) t[k] = pi[k];
-      for (int r = 0; r < 8; ++r) {
-        const int iL = 8 * h + r;
-        if (r < g.lo || iL >= n) {
-          rows.push_back(PrefixRow{});
-          continue;
-        }
-        t[LM1] = iL;
+      for (int a = std::max(last, 8 * h); a < hi; a += 2) {
+        const bool two = a + 1 < hi;
+        DmmaPair pr{};
+        for (int k = 0; k < 6; ++k) pr.pidx[k] = pi[k];
+        pr.a0 = static_cast<uint16_t>(a);
+        pr.a1 = static_cast<uint16_t>(two ? a + 1 : a);
+        pairs.push_back(pr);
+        t[LM1] = a;
         rows.push_back(make_row(t, top, low));
+        if (two) {
+          t[LM1] = a + 1;
+          rows.push_back(make_row(t, top, low));
+        } else {
+          rows.push_back(PrefixRow{});  // masked slot
+        }
       }
     }
-    const uint32_t ng = static_cast<uint32_t>(groups.size()) - g0;
-    if (!ng) continue;
-    const int ncg_all = (n - 8 * h + 7) / 8;
-    const int nranges = (ncg_all + 3) / 4;
+    while (pairs.size() % 32) {  // pad the window's last row set
+      pairs.push_back(DmmaPair{});
+      rows.push_back(PrefixRow{});
+      rows.push_back(PrefixRow{});
+    }
+    const uint32_t nrs = static_cast<uint32_t>(pairs.size() / 32) - rs0;
+    if (!nrs) continue;
+    // R row sets x 4/R column ranges of at most 4 column tiles per DMMA warp
+    const int ncg = (n - 8 * h + 7) / 8;
+    const int R = ncg <= 4 ? 4 : ncg <= 8 ? 2 : 1;
+    const int per_cta = 4 * (4 / R);
+    const int nranges = (ncg + per_cta - 1) / per_cta;
     for (int q = 0; q < nranges; ++q) {
-      const int c0 = q * ncg_all / nranges, c1 = (q + 1) * ncg_all / nranges;
-      for (uint32_t s0 = 0; s0 < ng; s0 += per_tile) {
-        MomTile t{};
-        t.row0 = g0 + s0;
-        t.nrows = std::min<uint32_t>(per_tile, ng - s0);
-        t.J = static_cast<uint32_t>(h);
-        t.col0 = static_cast<uint32_t>(8 * h + 8 * c0);
-        t.ncols = static_cast<uint32_t>(std::min(8 * c1, n - 8 * h) - 8 * c0);
-        t.low = (q == 0 && low) ? 1u : 0u;
-        t.pad0 = static_cast<uint32_t>(c1 - c0);
-        tiles.push_back(t);
+      const int c0 = q * ncg / nranges, c1 = (q + 1) * ncg / nranges;
+      for (uint32_t s0 = 0; s0 < nrs; s0 += static_cast<uint32_t>(R)) {
+        MomTile tl{};
+        tl.row0 = rs0 + s0;
+        tl.nrows = std::min<uint32_t>(static_cast<uint32_t>(R), nrs - s0);
+        tl.J = static_cast<uint32_t>(h);
+        tl.col0 = static_cast<uint32_t>(8 * h + 8 * c0);
+        tl.ncols = static_cast<uint32_t>(c1 - c0);
+        tl.low = (q == 0 && low) ? 1u : 0u;
+        tl.pad0 = static_cast<uint32_t>(R);
+        tiles.push_back(tl);
       }
     }
   }
-  std::stable_sort(tiles.begin(), tiles.end(), [](const MomTile& a, const MomTile& c) {
-    return static_cast<uint64_t>(a.nrows) * a.pad0 > static_cast<uint64_t>(c.nrows) * c.pad0;
-  });
-  for (size_t i = 0; i < tiles.size(); ++i) tiles[i].pad1 = static_cast<uint32_t>(i);  // pair slot
+  // longest tiles first (the hardware dispatches in blockIdx order): a
+  // tile's time is set by its widest DMMA warp
+  auto width = [](const MomTile& t) { return (t.ncols + (4 / t.pad0) - 1) / (4 / t.pad0); };
+  std::stable_sort(tiles.begin(), tiles.end(),
+                   [&](const MomTile& a, const MomTile& c) { return width(a) > width(c); });
+  for (size_t i = 0; i < tiles.size(); ++i) tiles[i].pad1 = static_cast<uint32_t>(i);
   scratch_per_tile = scratch;
 }
 
@@ -387,11 +374,9 @@ void MomentPlan::build(int S_, int n_, int b_, const Layout& top, const Layout* 
 void MomentPlan::upload() {
   d_rows.alloc(rows.size());
   d_tiles.alloc(tiles.size());
-  d_groups.alloc(groups.size());
-  d_rep_off.alloc(rep_off.size());
-  if (!rep_off.empty()) h2d_sync(d_rep_off.ptr, rep_off.data(), d_rep_off.bytes());
-  if (!groups.empty())
-    h2d_sync(d_groups.ptr, groups.data(), d_groups.bytes());
+  d_pairs.alloc(pairs.size());
+  if (!pairs.empty())
+    h2d_sync(d_pairs.ptr, pairs.data(), d_pairs.bytes());
   if (!rows.empty())
     h2d_sync(d_rows.ptr, rows.data(), d_rows.bytes());
   if (!tiles.empty())

@@ -52,31 +52,29 @@ struct alignas(16) PrefixRow {
 };
 static_assert(sizeof(PrefixRow) == 48, "PrefixRow layout");
 
-// One group of 8 prefix rows (pi, 8h + g), g = 0..7, for the DMMA kernel:
-// pi = (i_1..i_{L-1}); rows with g < lo (i_L < i_{L-1}) or 8h + g >= n are
-// not canonical and are masked.
-//
-// A group may also represent lower-order elements: its prefix products at
-// depth s (x[pi_1] ... x[pi_s]) are the order-s moment products of the
-// tuple (pi_1..pi_s); the group (pi_1..pi_s, pi_s, ..., pi_s) in its first
-// window h = pi_s / 8 is that tuple's unique representative (rep_mask bit
-// s-1), so the producer warps compute every order <= d-2 as well.
-struct DmmaGroup {
+// One pair of prefix rows (pi, a0), (pi, a1) of the DMMA kernel, pi =
+// (i_1..i_{L-1}).  The kernel packs the canonical prefix rows of one
+// column window h (8h <= i_L < 8h + 8) densely, two per producer lane: a
+// lane forms P = x[pi_1] ... x[pi_{L-1}] once per data row and the two
+// Khatri-Rao values P x[a0], P x[a1].  a1 == a0 when the pair's second
+// row does not exist (its slot is masked: PrefixRow::vprime == 0).
+struct DmmaPair {
   uint16_t pidx[6];
-  uint16_t lo;
-  uint16_t h;
-  uint32_t rep;       // first entry in MomentPlan::rep_off (valid when rep_mask != 0)
-  uint32_t rep_mask;  // bit s-1: this group represents order-s tuple (pi_1..pi_s)
-  uint32_t pad[2];
+  uint16_t a0, a1;
 };
-static_assert(sizeof(DmmaGroup) == 32, "DmmaGroup layout");
+static_assert(sizeof(DmmaPair) == 16, "DmmaPair layout");
 
+// DFMA kernel: rows [row0, row0 + nrows) of the row table, columns
+// [col0, col0 + ncols).  DMMA kernel: row sets [row0, row0 + nrows) (64
+// prefix-row slots / 32 pairs each), column tiles of 8 starting at col0,
+// ncols of them, R = pad0 row-set slots per CTA (1, 2 or 4; the 4 DMMA warps
+// of the CTA cover R row sets x 4/R column ranges).
 struct MomTile {
-  uint32_t row0, nrows;  // range in the row table
-  uint32_t J;            // block of the last prefix index
-  uint32_t col0, ncols;  // absolute column range [col0, col0 + ncols)
+  uint32_t row0, nrows;  // range in the row table (DMMA: row sets)
+  uint32_t J;            // block of the last prefix index (DMMA: column window h)
+  uint32_t col0, ncols;  // DFMA: absolute column range; DMMA: first column, column tiles
   uint32_t low;          // 1: this tile also owns the M_{S-1} sums of its rows
-  uint32_t pad0, pad1;
+  uint32_t pad0, pad1;   // DMMA: R, tile index
 };
 
 // Block-prefix sharding of the top pair of orders: order-d
@@ -102,20 +100,17 @@ struct MomentPlan {
   DevBuf<PrefixRow> d_rows;
   DevBuf<MomTile> d_tiles;
   uint64_t scratch_per_tile = 0;  // doubles
-  bool dmma = false;  // tiles are for moment_top_dmma_kernel (pad0 = column groups)
-  std::vector<DmmaGroup> groups;
-  DevBuf<DmmaGroup> d_groups;
-  std::vector<uint64_t> rep_off;  // canonical offset in M_s (bit 63: block has copies)
-  DevBuf<uint64_t> d_rep_off;
+  bool dmma = false;  // tiles are for moment_top_dmma_kernel
+  std::vector<DmmaPair> pairs;  // DMMA: 32 per row set
+  DevBuf<DmmaPair> d_pairs;
   void build(int S, int n, int b, const Layout& top, const Layout* low, int threads);
-  // Tiles for the DMMA kernel: groups (pi, h) of 8 prefix rows, 8 groups per
-  // warp; columns [8h, n) in ranges of at most 4 groups of 8; rows[8 g + r]
-  // is the PrefixRow of row r of group g (zero for masked rows).
-  // lowers[s-1] = layout of order s (s <= S-2) when the groups should also
-  // compute the lower orders (unsharded plans), nullptr otherwise
-  void build_dmma(int S, int n, int b, const Layout& top, const Layout* low, int warps,
-                  uint64_t scratch_per_tile, const ShardPlan* shard = nullptr, int shard_index = 0,
-                  const Layout* const* lowers = nullptr);
+  // Tiles for the DMMA kernel.  Per column window h, the canonical prefix
+  // rows with 8h <= i_L < 8h + 8 are packed in pairs (lexicographic pi, then
+  // i_L), 32 pairs = 64 row slots per row set; rows[64 s + 2 j + e] is the
+  // PrefixRow of element e of pair j of row set s (vprime == 0: masked).
+  // Columns [8h, n) are covered in tiles of 8.
+  void build_dmma(int S, int n, int b, const Layout& top, const Layout* low, uint64_t scratch_per_tile,
+                  const ShardPlan* shard = nullptr, int shard_index = 0);
   void upload();
 
  private:

@@ -10,18 +10,27 @@
 // chaining the MMAs over k in row order therefore reproduces the
 // reference's row-ordered fma(A, x, acc) (moments.cpp:47) bit for bit.
 //
-// Work unit: a tile = 32 groups (pi, h) of 8 prefix rows (pi, 8h + g) x up
-// to 4 column groups of 8.  A CTA streams the incoming rows, stashes their
-// means, streams the outgoing rows and applies the fused update
-// M = fma(p/T, a - b, M) (moments.cpp:297) to the canonical entries.
+// Work decomposition (MomentPlan::build_dmma).  The canonical prefix rows
+// (i_1 <= ... <= i_L) whose last index lies in the column window
+// [8h, 8h + 8) all need the output columns [8h, n); they are packed densely
+// in pairs (pi, a0), (pi, a0 + 1) -- no masked rows apart from odd tails --
+// into row sets of 64 rows.  A CTA takes R row sets (R = 4, 2, 1 for windows
+// with <= 4, <= 8, > 8 column tiles) and a range of <= 16/R column tiles;
+// its 4 DMMA warps cover R row sets x 4/R column ranges, so each Khatri-Rao
+// value is formed once per CTA and reused over up to 128 columns.
 //
-// Per CTA (4 warps): rows of the batch stream through a 4-stage shared
-// memory ring filled by cp.async.bulk (one TMA bulk copy per 32-row chunk,
-// mbarrier completion; lane 0 of warp 0 is the producer and refills a stage
-// once all warps released it -- no CTA-wide barrier in the loop).  Each warp
-// builds its Khatri-Rao fragments in registers straight from the staged
-// rows, software-pipelined so the next step's loads and products overlap
-// the current step's DMMAs.
+// Per CTA: 4 DMMA (consumer) warps + up to 4 producer warps (one per row
+// set).  Data rows stream through a shared-memory ring of 16-row chunks
+// filled by TMA bulk copies (cp.async.bulk, mbarrier complete_tx); the last
+// warp to release a stage refills it at once.  A producer
+// lane owns one pair: per data row it forms P = x[pi_1] ... x[pi_{L-1}] and
+// the two products P x[a0], P x[a1], adds them to its order-(d-1) row sums
+// in row order and stores them in MMA fragment order into its row set's
+// A ring (2 slots of one chunk each, full/empty mbarriers).  The DMMA warps
+// read A fragments from the ring and B fragments (the data rows) straight
+// from the staged chunk.  The incoming pass's means are stashed at the pass
+// boundary; the epilogue applies M = fma(p/T, a - b, M) (moments.cpp:297) to
+// the canonical entries (mirror_kernel then fixes the symmetric copies).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -32,15 +41,16 @@ namespace csb {
 
 namespace {
 
-constexpr int CWARPS = 4;           // DMMA consumer warps
-constexpr int WARPS = 2 * CWARPS;   // + one producer warp per consumer
-constexpr int THREADS = WARPS * 32;
-constexpr int HSTEPS = 8;           // k4 steps per A-ring slot (one 32-row chunk)
-constexpr int ASTRIDE = 10;         // doubles per (r, q) entry: 8 used, bank-conflict free
+constexpr int CWARPS = 4;                 // DMMA consumer warps
+constexpr int PWARPS = 4;                 // producer warps (one per row set)
+constexpr int THREADS = (CWARPS + PWARPS) * 32;
+constexpr int HSTEPS = 4;                 // k4 steps per chunk
+constexpr int KC = 4 * HSTEPS;            // data rows per chunk / stage
+constexpr int ASTRIDE = 10;               // doubles per (r, q) entry: 8 used, bank-conflict free
 constexpr int ASLOT = HSTEPS * 32 * ASTRIDE;
-constexpr int STAGES = 2;
-constexpr int KC = 32;        // data rows per stage
-
+constexpr int ASLOTS = 2;                 // A-ring slots per row set
+constexpr int MAX_STAGES = 12;
+constexpr int SLOTS_PER_SET = 64;         // prefix rows per row set
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -107,263 +117,212 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// Per-warp layout: lane = 4 r + q.  The warp owns 8 groups; group r is
-// (pi_r, h): the 8 prefix rows (pi_r, 8h + g), g = 0..7.  For MMA fragment
-// g, row m = r of A is the Khatri-Rao value of row (pi_r, 8h + g) at data
-// row k = q, so each thread forms P = x[pi_r] once per k and the 8 row values
-// as P * x[8h + g] (prefix sharing of moments.cpp:55,71).  B fragment c is
-// x[k = q][col0 + 8c + r].  Accumulator (g, c, e) is the element
-// (pi_r, 8h + g, col0 + 8c + 2q + e).
-//
-// The k loop runs over "steps" of 4 data rows, flat across both passes and
-// all staged chunks, software-pipelined in registers: step s+1's operands
-// are loaded from shared memory and multiplied out while step s's DMMAs
-// occupy the FP64 tensor pipe.
+// ---------------------------------------------------------------------------
+// Shared state of one CTA.
+struct Ring {
+  double* xs;          // stages x KC x n data rows
+  double* arings;      // PWARPS x ASLOTS x ASLOT
+  uint64_t* xfull;     // per stage: TMA bytes landed
+  uint32_t* rel;       // per stage: release counter (active warps per round)
+  uint64_t* afull;     // per row set and slot: producer lanes stored
+  uint64_t* aempty;    // per row set and slot: DMMA lanes consumed
+  int stages;
+  uint32_t active;       // warps that consume the staged chunks
+  uint32_t chunks, cpp;  // chunks in total, per pass
+};
 
-// Warp-specialized tile: warps 0..CWARPS-1 are DMMA consumers, warps
-// CWARPS..2*CWARPS-1 their producers.  A DMMA stalls its warp for 15 cycles
-// (SASS control bits), so a warp cannot overlap its own FP64 products and
-// row sums with its DMMAs; split across warps, the products, the order-L
-// row sums and the DMMAs share the FP64 pipe of the SM sub-partition.
-//
-// Producer lane (r, gp) of producer warp w: rows (pi_r, 8h + 2gp + e),
-// e = 0, 1, of the consumer warp's group r.  Per data row k it forms
-// P = x[pi_1] ... x[pi_{L-1}] and the two products P * x[8h + 2gp + e]
-// (moments.cpp:55,71), adds them to its row sums in row order, and stores
-// them to the A ring in fragment order:
-//   aring[w][slot][t][(r * 4 + q) * ASTRIDE + g],  k = 16 half + 4 t + q.
-// Consumer lane (r, q): fragment g of step t is aring[...][t][(r*4+q)*10+g]
-// (4 x LDS.128), B fragment c is x[k = 4 t + q][col0 + 8c + r].
-template <int LM1, int NC>
-__device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile, double* xs, double* arings,
-                                         uint64_t* xfull, uint64_t* xempty, uint64_t* afull, uint64_t* aempty) {
-  constexpr int L = LM1 + 1;
-  const int n = P.n, b = P.b;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const bool producer = warp >= CWARPS;
-  const int pw = producer ? warp - CWARPS : warp;  // pair index
-  const int r = lane >> 2, q4 = lane & 3;          // (r, q) consumer / (r, gp) producer
-  const int h8 = static_cast<int>(tile.J) * 8;
-  const int col0 = static_cast<int>(tile.col0);
-  const bool do_low = (P.low != nullptr) && tile.low;
-  const size_t stage_elems = static_cast<size_t>(KC) * n;
+// TMA bulk copies of data-row chunk i into its stage (one thread).
+__device__ __forceinline__ void issue_chunk(const MomParams& P, const Ring& g, uint32_t i) {
+  const int n = P.n;
   const uint32_t K = P.K;
-  const uint32_t cpp = (K + KC - 1) / KC;  // chunks per pass
-  const uint32_t chunks = cpp * P.npass;   // incoming pass, then outgoing pass
-  double* aring = arings + static_cast<size_t>(pw) * 2 * ASLOT;
-
-  // ---- TMA producer: lane 0 of the first producer warp ----
-  uint32_t next_issue = 0;
-  auto pump = [&](uint32_t needed) {
-    if (threadIdx.x != CWARPS * 32) return;
-    while (next_issue < chunks) {
-      const uint32_t i = next_issue;
-      const uint32_t st = i % STAGES;
-      if (i >= STAGES) {
-        const uint32_t par = ((i / STAGES) - 1) & 1u;
-        if (!mbar_test(xempty + st, par)) {
-          if (i > needed) break;
-          mbar_wait(xempty + st, par);
-        }
-      }
-      const RowSource& src = P.src[i / cpp];
-      const uint32_t a0 = (i % cpp) * KC;
-      const uint32_t kc = min(static_cast<uint32_t>(KC), K - a0);
-      double* dst = xs + st * stage_elems;
-      const uint32_t rb = static_cast<uint32_t>(n) * 8u;
-      mbar_expect_tx(xfull + st, static_cast<uint32_t>(KC) * rb);
-      // rows past the end of the pass are zero rows: they add exact zeros
-      if (kc < static_cast<uint32_t>(KC))
-        bulk_g2s(dst + static_cast<size_t>(kc) * n, P.zeros, (KC - kc) * rb, xfull + st);
-      if (a0 + kc <= src.len0 || a0 >= src.len0) {
-        bulk_g2s(dst, row_ptr(src, a0, n), kc * rb, xfull + st);
-      } else {  // across the ring's wrap
-        const uint32_t k1 = src.len0 - a0;
-        bulk_g2s(dst, row_ptr(src, a0, n), k1 * rb, xfull + st);
-        bulk_g2s(dst + static_cast<size_t>(k1) * n, src.seg1, (kc - k1) * rb, xfull + st);
-      }
-      ++next_issue;
-    }
-  };
-
-  const int gl = pw * 8 + r;  // group slot in the tile
-  const bool gvalid = gl < static_cast<int>(tile.nrows);
-  const uint32_t gi = tile.row0 + (gvalid ? gl : 0);
-  const DmmaGroup grp = P.groups[gi];
-  const int lo = grp.lo;
-  const bool update = P.npass == 2;
-  // pass-0 means of the consumer threads (the producers keep theirs in registers)
-  double* stash = P.scratch + static_cast<size_t>(blockIdx.x) * (CWARPS * 32 * 64);
-
-  if (producer) {
-    int pidx[LM1 > 0 ? LM1 : 1];
-#pragma unroll
-    for (int t = 0; t < LM1; ++t) pidx[t] = grp.pidx[t];
-    const int gp = q4;
-    double lowacc[2] = {0.0, 0.0}, lowin[2] = {0.0, 0.0};
-    // lower orders: lane gp accumulates depth gp + 1 of the prefix chain
-    // (the order-(gp+1) product of (pi_1..pi_{gp+1})) when the group
-    // represents that tuple; other lanes' sums are discarded
-    const bool rep = do_low && P.rep_off != nullptr && gp < LM1 && ((grp.rep_mask >> gp) & 1u);
-    double repacc = 0.0, repin = 0.0;
-    for (uint32_t c = 0; c < chunks; ++c) {
-      const uint32_t st = c % STAGES;
-      if (warp == CWARPS) pump(c);
-      __syncwarp();
-      mbar_wait(xfull + st, (c / STAGES) & 1u);
-      const double* xst = xs + st * stage_elems;
-#pragma unroll 1
-      for (int hc = 0; hc < KC / (4 * HSTEPS); ++hc) {
-        const uint32_t u = c * (KC / (4 * HSTEPS)) + hc;
-        const int slot = u & 1;
-        if (u >= 2) mbar_wait(aempty + pw * 2 + slot, ((u >> 1) - 1) & 1u);
-        double* as = aring + slot * ASLOT;
-#pragma unroll
-        for (int t = 0; t < HSTEPS; ++t)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const double* xr = xst + static_cast<size_t>(hc * 4 * HSTEPS + 4 * t + q) * n;
-            double Pv = xr[pidx[0]];
-            double Ps = Pv;
-#pragma unroll
-            for (int t2 = 1; t2 < LM1; ++t2) {
-              Pv = __dmul_rn(Pv, xr[pidx[t2]]);
-              if (gp >= t2) Ps = Pv;
-            }
-            if (LM1 > 0) repacc = __dadd_rn(repacc, Ps);  // row order, plain adds (moments.cpp:44)
-            const double2 xv = *reinterpret_cast<const double2*>(xr + h8 + 2 * gp);
-            double a0, a1;
-            if (P.debug & 2) {
-              a0 = xv.x;
-              a1 = xv.y;
-            } else {
-              a0 = __dmul_rn(Pv, xv.x);
-              a1 = __dmul_rn(Pv, xv.y);
-            }
-            if (do_low && !(P.debug & 1)) {
-              lowacc[0] = __dadd_rn(lowacc[0], a0);  // row order, plain adds (moments.cpp:44)
-              lowacc[1] = __dadd_rn(lowacc[1], a1);
-            }
-            *reinterpret_cast<double2*>(as + t * 32 * ASTRIDE + (r * 4 + q) * ASTRIDE + 2 * gp) =
-                make_double2(a0, a1);
-          }
-        mbar_arrive(afull + pw * 2 + slot);  // every lane: its stores are released
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(xempty + st);
-      if (warp == CWARPS) pump(0);
-      if (update && c + 1 == cpp) {  // end of the incoming pass
-        lowin[0] = __dmul_rn(lowacc[0], P.inv);
-        lowin[1] = __dmul_rn(lowacc[1], P.inv);
-        lowacc[0] = lowacc[1] = 0.0;
-        repin = __dmul_rn(repacc, P.inv);
-        repacc = 0.0;
-      }
-    }
-    if (rep && gvalid) {  // order gp + 1, canonical element (pi_1..pi_{gp+1})
-      const uint64_t e = P.rep_off[grp.rep + __popc(grp.rep_mask & ((1u << gp) - 1u))];
-      const uint64_t off = e & ~(1ull << 63);
-      double* Ms = P.lower[gp];
-      if (update) {
-        const double delta = __dsub_rn(repin, __dmul_rn(repacc, P.inv));
-        Ms[off] = __fma_rn(P.c, delta, Ms[off]);
-        if (e >> 63) P.dlower[gp][off] = delta;
-      } else {
-        Ms[off] = __dmul_rn(repacc, P.inv);
-      }
-    }
-    // ---- producer epilogue: order L (= d-1) ----
-    if (!gvalid || !do_low) return;
-    const double cc = P.c;
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int g = 2 * gp + e;
-      const int iL = h8 + g;
-      if (g < lo || iL >= n) continue;
-      const PrefixRow& pr = P.rows[static_cast<size_t>(gi) * 8 + g];
-      if (update) {
-        const double delta = __dsub_rn(lowin[e], __dmul_rn(lowacc[e], P.inv));  // a - b
-        P.low[pr.low_off] = __fma_rn(cc, delta, P.low[pr.low_off]);
-        if (pr.idx[7] & 1u) P.dlow[pr.low_off] = delta;
-      } else {
-        P.low[pr.low_off] = __dmul_rn(lowacc[e], P.inv);
-      }
-    }
-    return;
+  const uint32_t rb = static_cast<uint32_t>(n) * 8u;
+  const uint32_t st = i % g.stages;
+  const RowSource& src = P.src[i / g.cpp];
+  const uint32_t a0 = (i % g.cpp) * KC;
+  const uint32_t kc = min(static_cast<uint32_t>(KC), K - a0);
+  double* dst = g.xs + st * static_cast<size_t>(KC) * n;
+  mbar_expect_tx(g.xfull + st, static_cast<uint32_t>(KC) * rb);
+  // rows past the end of the pass are zero rows: they add exact zeros
+  if (kc < static_cast<uint32_t>(KC))
+    bulk_g2s(dst + static_cast<size_t>(kc) * n, P.zeros, (KC - kc) * rb, g.xfull + st);
+  if (a0 + kc <= src.len0 || a0 >= src.len0) {
+    bulk_g2s(dst, row_ptr(src, a0, n), kc * rb, g.xfull + st);
+  } else {  // across the ring's wrap
+    const uint32_t k1 = src.len0 - a0;
+    bulk_g2s(dst, row_ptr(src, a0, n), k1 * rb, g.xfull + st);
+    bulk_g2s(dst + static_cast<size_t>(k1) * n, src.seg1, (kc - k1) * rb, g.xfull + st);
   }
+}
 
-  // ================= DMMA consumer =================
-  const int q = q4;
+// A warp is done with chunk c: the last of the CTA's active warps to
+// release the stage refills it with chunk c + stages right away (the
+// per-stage release counters only grow; every `active`-th release is a
+// round's last).
+__device__ __forceinline__ void release_chunk(const MomParams& P, const Ring& g, uint32_t c) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) {
+    const uint32_t st = c % g.stages;
+    __threadfence_block();  // this warp's reads of the stage happen before the release
+    const uint32_t old = atomicAdd(g.rel + st, 1u);
+    if ((old + 1) % g.active == 0 && c + g.stages < g.chunks) {
+      __threadfence_block();
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before async-proxy writes
+      issue_chunk(P, g, c + g.stages);
+    }
+  }
+}
+
+// Producer warp of row set rs.  Lane j owns pair j of the row set: slots
+// (r, 2gp) and (r, 2gp + 1) of the MMA A operand, r = j >> 2, gp = j & 3.
+// Ring layout: aring[slot][t][(r * 4 + q) * ASTRIDE + g] holds the value of
+// row slot (r, g) at data row k = 4t + q of the chunk, so a DMMA lane
+// (r, q) loads its 8 fragments with 4 x LDS.128.
+template <int LM1>
+__device__ __forceinline__ void produce(const MomParams& P, const MomTile& tile, const Ring& g, int rs) {
+  const int n = P.n;
+  const int lane = threadIdx.x & 31;
+  const uint32_t set = tile.row0 + rs;
+  const DmmaPair pr = P.pairs[static_cast<size_t>(set) * 32 + lane];
+  int pidx[LM1];
+#pragma unroll
+  for (int t = 0; t < LM1; ++t) pidx[t] = pr.pidx[t];
+  const int a0 = pr.a0, a1 = pr.a1;
+  const bool update = P.npass == 2;
+  const bool do_low = P.low != nullptr && tile.low;
+  const size_t stage_elems = static_cast<size_t>(KC) * n;
+  double* aring = g.arings + static_cast<size_t>(rs) * ASLOTS * ASLOT;
+  uint64_t* afull = g.afull + rs * ASLOTS;
+  uint64_t* aempty = g.aempty + rs * ASLOTS;
+  const int wofs = ((lane >> 2) * 4) * ASTRIDE + 2 * (lane & 3);
+  double s0 = 0.0, s1 = 0.0, in0 = 0.0, in1 = 0.0;
+  for (uint32_t c = 0; c < g.chunks; ++c) {
+    const uint32_t st = c % g.stages;
+    mbar_wait(g.xfull + st, (c / g.stages) & 1u);
+    const uint32_t slot = c % ASLOTS;
+    if (c >= ASLOTS) mbar_wait(aempty + slot, ((c / ASLOTS) - 1) & 1u);
+    const double* xst = g.xs + st * stage_elems;
+    double* as = aring + slot * ASLOT + wofs;
+#pragma unroll
+    for (int t = 0; t < HSTEPS; ++t)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double* xr = xst + (4 * t + q) * n;
+        double pv = xr[pidx[0]];
+#pragma unroll
+        for (int u = 1; u < LM1; ++u) pv = __dmul_rn(pv, xr[pidx[u]]);
+        const double v0 = __dmul_rn(pv, xr[a0]);
+        const double v1 = __dmul_rn(pv, xr[a1]);
+        s0 = __dadd_rn(s0, v0);  // row order, plain adds (moments.cpp:44)
+        s1 = __dadd_rn(s1, v1);
+        *reinterpret_cast<double2*>(as + t * 32 * ASTRIDE + q * ASTRIDE) = make_double2(v0, v1);
+      }
+    mbar_arrive(afull + slot);  // every lane: its stores are released
+    release_chunk(P, g, c);
+    if (update && c + 1 == g.cpp) {  // end of the incoming pass
+      in0 = __dmul_rn(s0, P.inv);
+      in1 = __dmul_rn(s1, P.inv);
+      s0 = s1 = 0.0;
+    }
+  }
+  // ---- order L = d-1: the row sums of this lane's two slots ----
+  if (!do_low) return;
+  const double cc = P.c;
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const PrefixRow& row = P.rows[static_cast<size_t>(set) * SLOTS_PER_SET + 2 * lane + e];
+    if (row.vprime == 0) continue;
+    const double s = e ? s1 : s0;
+    if (update) {
+      const double delta = __dsub_rn(e ? in1 : in0, __dmul_rn(s, P.inv));  // a - b
+      P.low[row.low_off] = __fma_rn(cc, delta, P.low[row.low_off]);
+      if (row.idx[7] & 1u) P.dlow[row.low_off] = delta;
+    } else {
+      P.low[row.low_off] = __dmul_rn(s, P.inv);
+    }
+  }
+}
+
+// DMMA warp: row set rs, column tiles [ct0, ct0 + NC) of the CTA's range.
+// Lane (r, q): A fragment g = row slot (r, g) at k = q; B fragment c =
+// x[k = q][col + 8c + r]; accumulator (g, c, e) = row slot (r, g), column
+// col + 8c + 2q + e.
+template <int NC>
+__device__ __forceinline__ void consume(const MomParams& P, const MomTile& tile, const Ring& g, int rs, int ct0,
+                                        int warp) {
+  const int n = P.n, b = P.b;
+  const int lane = threadIdx.x & 31;
+  const int r = lane >> 2, q = lane & 3;
+  const uint32_t set = tile.row0 + rs;
+  const int colbase = static_cast<int>(tile.col0) + 8 * ct0;
+  const bool update = P.npass == 2;
+  const size_t stage_elems = static_cast<size_t>(KC) * n;
+  const double* aring = g.arings + static_cast<size_t>(rs) * ASLOTS * ASLOT + (r * 4 + q) * ASTRIDE;
+  uint64_t* afull = g.afull + rs * ASLOTS;
+  uint64_t* aempty = g.aempty + rs * ASLOTS;
+  // pass-0 means of this thread (64 doubles), in the CTA's scratch
+  double* stash = P.scratch + static_cast<size_t>(blockIdx.x) * (CWARPS * 32 * 64);
+  const int tid = warp * 32 + lane;
   double acc[8][NC][2];
 #pragma unroll
-  for (int g = 0; g < 8; ++g)
+  for (int gg = 0; gg < 8; ++gg)
 #pragma unroll
-    for (int c = 0; c < NC; ++c) acc[g][c][0] = acc[g][c][1] = 0.0;
-  for (uint32_t c = 0; c < chunks; ++c) {
-    const uint32_t st = c % STAGES;
-    mbar_wait(xfull + st, (c / STAGES) & 1u);
-    const double* xst = xs + st * stage_elems + static_cast<size_t>(q) * n + col0 + r;
-#pragma unroll 1
-    for (int hc = 0; hc < KC / (4 * HSTEPS); ++hc) {
-      const uint32_t u = c * (KC / (4 * HSTEPS)) + hc;
-      const int slot = u & 1;
-      mbar_wait(afull + pw * 2 + slot, (u >> 1) & 1u);
-      const double* as = aring + slot * ASLOT + (r * 4 + q) * ASTRIDE;
-      const double* xb = xst + static_cast<size_t>(hc * 4 * HSTEPS) * n;
-      double a[2][8], bb[2][NC];
-      auto load = [&](int t, int buf) {
-        const double2* ap = reinterpret_cast<const double2*>(as + t * 32 * ASTRIDE);
+    for (int c = 0; c < NC; ++c) acc[gg][c][0] = acc[gg][c][1] = 0.0;
+  for (uint32_t c = 0; c < g.chunks; ++c) {
+    const uint32_t st = c % g.stages;
+    const uint32_t slot = c % ASLOTS;
+    mbar_wait(g.xfull + st, (c / g.stages) & 1u);
+    mbar_wait(afull + slot, (c / ASLOTS) & 1u);
+    const double* as = aring + slot * ASLOT;
+    const double* xb = g.xs + st * stage_elems + static_cast<size_t>(q) * n + colbase + r;
+    double a[2][8], bb[2][NC];
+    auto load = [&](int t, int buf) {
+      const double2* ap = reinterpret_cast<const double2*>(as + t * 32 * ASTRIDE);
 #pragma unroll
-        for (int s2 = 0; s2 < 4; ++s2) {
-          const double2 v = ap[s2];
-          a[buf][2 * s2] = v.x;
-          a[buf][2 * s2 + 1] = v.y;
-        }
-#pragma unroll
-        for (int cc = 0; cc < NC; ++cc) bb[buf][cc] = xb[static_cast<size_t>(4 * t) * n + 8 * cc];
-      };
-      load(0, 0);
-#pragma unroll
-      for (int t = 0; t < HSTEPS; ++t) {
-        if (t + 1 < HSTEPS) load(t + 1, (t + 1) & 1);
-#pragma unroll
-        for (int cc = 0; cc < NC; ++cc)
-#pragma unroll
-          for (int g = 0; g < 8; ++g) dmma(acc[g][cc][0], acc[g][cc][1], a[t & 1][g], bb[t & 1][cc]);
+      for (int s2 = 0; s2 < 4; ++s2) {
+        const double2 v = ap[s2];
+        a[buf][2 * s2] = v.x;
+        a[buf][2 * s2 + 1] = v.y;
       }
-      mbar_arrive(aempty + pw * 2 + slot);  // every lane has consumed the slot
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(xempty + st);
-    if (update && c + 1 == cpp) {
-      // end of the incoming pass: stash its means, restart the accumulators
-      const int tid = pw * 32 + lane;
 #pragma unroll
-      for (int g = 0; g < 8; ++g)
+      for (int cc = 0; cc < NC; ++cc) bb[buf][cc] = xb[static_cast<size_t>(4 * t) * n + 8 * cc];
+    };
+    load(0, 0);
+#pragma unroll
+    for (int t = 0; t < HSTEPS; ++t) {
+      if (t + 1 < HSTEPS) load(t + 1, (t + 1) & 1);
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+        for (int gg = 0; gg < 8; ++gg) dmma(acc[gg][cc][0], acc[gg][cc][1], a[t & 1][gg], bb[t & 1][cc]);
+    }
+    mbar_arrive(aempty + slot);  // every lane has consumed the slot
+    release_chunk(P, g, c);
+    if (update && c + 1 == g.cpp) {
+      // end of the incoming pass: stash its means, restart the accumulators
+#pragma unroll
+      for (int gg = 0; gg < 8; ++gg)
 #pragma unroll
         for (int cc = 0; cc < NC; ++cc)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            stash[static_cast<size_t>((g * NC + cc) * 2 + e) * (CWARPS * 32) + tid] = __dmul_rn(acc[g][cc][e], P.inv);
-            acc[g][cc][e] = 0.0;
+            stash[static_cast<size_t>((gg * NC + cc) * 2 + e) * (CWARPS * 32) + tid] =
+                __dmul_rn(acc[gg][cc][e], P.inv);
+            acc[gg][cc][e] = 0.0;
           }
     }
   }
-
-  const int tid = pw * 32 + lane;  // consumer thread index
 
   // ---- epilogue: canonical entries only ----
   // Entries of blocks with equal neighbouring coordinates have symmetric
   // copies; for those the update's delta is also written to the delta
   // buffer at the canonical position and mirror_kernel applies it to every
   // other stored copy (or copies the value, for an assignment).
-  if (!gvalid) return;
   const double cc = P.c;
 #pragma unroll
-  for (int g = 0; g < 8; ++g) {
-    const int iL = h8 + g;
-    if (g < lo || iL >= n) continue;
-    const PrefixRow& pr = P.rows[static_cast<size_t>(gi) * 8 + g];
+  for (int gg = 0; gg < 8; ++gg) {
+    const PrefixRow& pr = P.rows[static_cast<size_t>(set) * SLOTS_PER_SET + r * 8 + gg];
+    if (pr.vprime == 0) continue;  // masked slot
+    const int iL = pr.idx[P.L - 1];
     const bool row_runs = (pr.idx[7] & 1u) != 0;  // runs among (j_1..j_L)
     const int J = iL / b;
     size_t off[NC][2];
@@ -373,17 +332,17 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
     for (int c = 0; c < NC; ++c)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int col = col0 + 8 * c + 2 * q + e;
+        const int col = colbase + 8 * c + 2 * q + e;
         const int jd = col / b;
         ok[c][e] = col < n && col >= iL;
         diag[c][e] = row_runs || jd == J;
         off[c][e] = pr.top_base + static_cast<uint64_t>(pr.vprime) * b * (jd - J) +
                     static_cast<uint64_t>(pr.poff) * ext_of(jd, n, b) + (col - jd * b);
         if (update) {
-          const size_t ix = static_cast<size_t>((g * NC + c) * 2 + e) * (CWARPS * 32) + tid;
-          val[c][e] = __dsub_rn(stash[ix], __dmul_rn(acc[g][c][e], P.inv));  // a - b
+          const size_t ix = static_cast<size_t>((gg * NC + c) * 2 + e) * (CWARPS * 32) + tid;
+          val[c][e] = __dsub_rn(stash[ix], __dmul_rn(acc[gg][c][e], P.inv));  // a - b
         } else {
-          val[c][e] = __dmul_rn(acc[g][c][e], P.inv);
+          val[c][e] = __dmul_rn(acc[gg][c][e], P.inv);
         }
       }
     if (update) {
@@ -412,36 +371,64 @@ __device__ __forceinline__ void run_tile(const MomParams& P, const MomTile& tile
 
 __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomParams P) {
   extern __shared__ __align__(128) double smem[];
-  __shared__ __align__(8) uint64_t xfull[STAGES];
-  __shared__ __align__(8) uint64_t xempty[STAGES];
-  __shared__ __align__(8) uint64_t afull[CWARPS * 2];
-  __shared__ __align__(8) uint64_t aempty[CWARPS * 2];
-  double* xs = smem;
-  // dense staging ring; reads past row n of a stage (the last 8-column
-  // window / column group) only feed rows and columns that are never stored
-  double* arings = xs + static_cast<size_t>(STAGES) * KC * P.n + 64;  // CWARPS x 2 x ASLOT
+  __shared__ __align__(8) uint64_t bars[MAX_STAGES + 2 * PWARPS * ASLOTS];
+  __shared__ uint32_t rel[MAX_STAGES];
   const MomTile tile = P.tiles[blockIdx.x];
+  const int R = static_cast<int>(tile.pad0);    // row-set slots of this CTA: 1, 2, 4
+  const int nrs = static_cast<int>(tile.nrows); // live row sets (<= R)
+  const int C = CWARPS / R;                     // column ranges
+  Ring g;
+  g.stages = P.stages;
+  g.xs = smem;
+  // reads past row n of the last stage (B fragments of the last column
+  // tile) land in this padding and only feed outputs that are never stored
+  g.arings = smem + static_cast<size_t>(g.stages) * KC * P.n + 64;
+  g.xfull = bars;
+  g.rel = rel;
+  g.afull = bars + MAX_STAGES;
+  g.aempty = g.afull + PWARPS * ASLOTS;
+  g.cpp = (P.K + KC - 1) / KC;
+  g.chunks = g.cpp * P.npass;  // incoming pass, then outgoing pass
+  const int warp = threadIdx.x >> 5;
+  // active warps: DMMA warps whose row set is live, one producer per live row set
+  int active = nrs;
+  for (int w = 0; w < CWARPS; ++w) active += (w % R) < nrs;
+  g.active = static_cast<uint32_t>(active);
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(xfull + s, 1);
-      mbar_init(xempty + s, WARPS);
+    for (int s = 0; s < g.stages; ++s) {
+      mbar_init(g.xfull + s, 1);
+      rel[s] = 0;
     }
-    for (int s = 0; s < CWARPS * 2; ++s) {
-      mbar_init(afull + s, 32);
-      mbar_init(aempty + s, 32);
+    for (int s = 0; s < PWARPS * ASLOTS; ++s) {
+      mbar_init(g.afull + s, 32);
+      mbar_init(g.aempty + s, 32 * C);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (uint32_t i = 0; i < g.chunks && i < static_cast<uint32_t>(g.stages); ++i) issue_chunk(P, g, i);
   }
   __syncthreads();
-  const int nc = static_cast<int>(tile.pad0);
-  switch (P.L * 8 + nc) {
-#define CSB_CASE(LL, NCC) \
-  case (LL) * 8 + (NCC): \
-    run_tile<(LL) - 1, NCC>(P, tile, xs, arings, xfull, xempty, afull, aempty); break;
-#define CSB_CASES(LL) CSB_CASE(LL, 1) CSB_CASE(LL, 2) CSB_CASE(LL, 3) CSB_CASE(LL, 4)
-    CSB_CASES(2) CSB_CASES(3) CSB_CASES(4) CSB_CASES(5)
-#undef CSB_CASES
-#undef CSB_CASE
+  if (warp >= CWARPS) {
+    const int rs = warp - CWARPS;
+    if (rs >= nrs) return;
+    switch (P.L) {
+      case 2: produce<1>(P, tile, g, rs); break;
+      case 3: produce<2>(P, tile, g, rs); break;
+      case 4: produce<3>(P, tile, g, rs); break;
+      case 5: produce<4>(P, tile, g, rs); break;
+      default: break;
+    }
+    return;
+  }
+  const int rs = warp % R;
+  if (rs >= nrs) return;
+  const int part = warp / R;
+  const int nct = static_cast<int>(tile.ncols);
+  const int ct0 = nct * part / C, ct1 = nct * (part + 1) / C;
+  switch (ct1 - ct0) {
+    case 1: consume<1>(P, tile, g, rs, ct0, warp); break;
+    case 2: consume<2>(P, tile, g, rs, ct0, warp); break;
+    case 3: consume<3>(P, tile, g, rs, ct0, warp); break;
+    case 4: consume<4>(P, tile, g, rs, ct0, warp); break;
     default: break;
   }
 }
@@ -495,22 +482,28 @@ __global__ void __launch_bounds__(256) mirror_kernel(double* __restrict__ m, con
   }
 }
 
-size_t smem_bytes(int n) {
-  return sizeof(double) * (static_cast<size_t>(STAGES) * KC * n + 64 + CWARPS * 2 * ASLOT);
+size_t smem_bytes(int n, int stages) {
+  return sizeof(double) * (static_cast<size_t>(stages) * KC * n + 64 + PWARPS * ASLOTS * ASLOT);
+}
+
+constexpr size_t kSmemLimit = 227 * 1024 - 1024;
+
+int stages_for(int n) {
+  int s = MAX_STAGES;
+  while (s > 0 && smem_bytes(n, s) > kSmemLimit) --s;
+  return s;
 }
 
 }  // namespace
-
-int dmma_warps() { return CWARPS; }
 
 // per tile: the incoming pass's means (64 values per consumer thread)
 size_t dmma_scratch_per_tile() { return static_cast<size_t>(CWARPS) * 32 * 64; }
 
 bool dmma_supported(const MomParams& p) {
-  // instantiated for orders 3..6 (L = 2..5); the staging ring must fit
+  // instantiated for orders 3..6 (L = 2..5); rows must be 16-byte aligned
+  // for the bulk copies, and at least two stages must fit
   if (p.n % 2 != 0 || p.L < 2 || p.L > 5) return false;
-  if (smem_bytes(p.n) > 220 * 1024) return false;
-  return true;
+  return stages_for(p.n) >= 2;
 }
 
 void launch_mirror(int S, double* m, const double* delta, const LayoutDev& lay, const uint32_t* blocks,
@@ -527,9 +520,12 @@ void launch_mirror(int S, double* m, const double* delta, const LayoutDev& lay, 
   count_launch();
 }
 
-void launch_moment_top_dmma(const MomParams& p, int ntiles, cudaStream_t st) {
+void launch_moment_top_dmma(const MomParams& p_in, int ntiles, cudaStream_t st) {
   if (ntiles <= 0) return;
-  const size_t smem = smem_bytes(p.n);
+  MomParams p = p_in;
+  p.stages = stages_for(p.n);
+  if (p.stages < 2) fail(CSB_EINVAL, "moment_top_dmma: rows too wide for the staging ring");
+  const size_t smem = smem_bytes(p.n, p.stages);
   CSB_CUDA(cudaFuncSetAttribute(moment_top_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
   moment_top_dmma_kernel<<<ntiles, THREADS, smem, st>>>(p);

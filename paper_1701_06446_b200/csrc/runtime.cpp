@@ -142,21 +142,12 @@ std::shared_ptr<MomentPlan> get_plan(Device& dev, int S, int n, int b, bool dmma
   auto top = get_layout(dev, S, n, b);
   std::shared_ptr<DevLayout> low = S > 1 ? get_layout(dev, S - 1, n, b) : nullptr;
   const int count = sp ? sp->count : 1;
-  // unsharded DMMA plans also carry the lower orders' representative groups
-  std::vector<std::shared_ptr<DevLayout>> lows;
-  std::vector<const Layout*> lowp;
-  if (dmma && !sp)
-    for (int s = 1; s <= S - 2; ++s) {
-      lows.push_back(get_layout(dev, s, n, b));
-      lowp.push_back(&lows.back()->host);
-    }
   std::lock_guard<std::mutex> lk(dev.mu);
   auto& slot = dev.plans[{S, n, b, (dmma ? 1 : 0) + 2 * (count * 256 + shard_index)}];
   if (!slot) {
     auto p = std::make_shared<MomentPlan>();
     if (dmma)
-      p->build_dmma(S, n, b, top->host, low ? &low->host : nullptr, dmma_warps(), dmma_scratch_per_tile(), sp,
-                    shard_index, lowp.empty() ? nullptr : lowp.data());
+      p->build_dmma(S, n, b, top->host, low ? &low->host : nullptr, dmma_scratch_per_tile(), sp, shard_index);
     else
       p->build(S, n, b, top->host, low ? &low->host : nullptr, kMomThreads);
     p->upload();
@@ -355,13 +346,7 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
   const bool use_dmma = g_use_dmma && dmma_supported(p);
   // sharding applies to the DMMA plan (the DFMA fallback computes all blocks)
   const bool sharded = use_dmma && sh.active() && !only_order;
-  // unsharded DMMA: the producer warps also compute orders <= d-2
-  static const bool no_fuse = [] {
-    const char* e = std::getenv("CSB_NO_FUSED_LOW");  // A/B: separate lower-order kernel
-    return e && e[0] == '1';
-  }();
-  const bool fused_lower = lower && use_dmma && !sharded && !no_fuse;
-  if (lower && !fused_lower) {
+  if (lower) {
     // orders <= d-2: element-parallel kernel, ahead of the top pair on the
     // same stream (concurrent CTAs would hold SMs the DMMA tiles need)
     ProfScope ps("moment_low", st);
@@ -385,36 +370,17 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
     auto plan = get_plan(dev, S, m->n, m->b, use_dmma, sharded ? sh.plan : nullptr, sharded ? sh.index : 0);
     p.rows = plan->d_rows.ptr;
     p.tiles = plan->d_tiles.ptr;
-    p.groups = plan->d_groups.ptr;
+    p.pairs = plan->d_pairs.ptr;
     const uint64_t ntiles = plan->tiles.size();
     if (npass == 2 || use_dmma) p.scratch = sc.get(ntiles * plan->scratch_per_tile);
     ProfScope ps("moment_top", st);
     if (use_dmma) {
-      static const int dbg = [] {
-        const char* e = std::getenv("CSB_DMMA_DEBUG");
-        return e ? std::atoi(e) : 0;
-      }();
-      p.debug = dbg;
-      p.flags = sc.get_flags(ntiles);
       p.zeros = sc.get_zeros(32ull * m->n);
       if (npass == 2) {
         p.dtop = sc.get_delta(sc.dtop, m->lay[S - 1]->host.stored);
         if (p.low) p.dlow = sc.get_delta(sc.dlow, m->lay[S - 2]->host.stored);
       }
-      if (fused_lower) {
-        p.rep_off = plan->d_rep_off.ptr;
-        for (int s = 1; s <= d - 2; ++s) {
-          p.lower[s - 1] = m->data[s - 1].ptr;
-          if (npass == 2) p.dlower[s - 1] = sc.get_delta(sc.dlower[s - 1], m->lay[s - 1]->host.stored);
-        }
-      }
       launch_moment_top_dmma(p, static_cast<int>(ntiles), st);
-      if (fused_lower)
-        for (int s = 2; s <= d - 2; ++s) {
-          const auto& Ls = m->lay[s - 1];
-          launch_mirror(s, p.lower[s - 1], p.dlower[s - 1], Ls->view(), Ls->diag.ptr, Ls->ndiag, m->n, m->b,
-                        npass == 2, c, st);
-        }
       const auto& LT = m->lay[S - 1];
       auto rt = sharded ? LT->diag_range(sh.lo(0), sh.hi(0)) : std::make_pair(0u, LT->ndiag);
       launch_mirror(S, p.top, p.dtop, LT->view(), LT->diag.ptr + rt.first, rt.second, m->n, m->b, npass == 2, c, st);
