@@ -196,6 +196,63 @@ __global__ void __launch_bounds__(256) moms2cums_v2(const M2CParams P) {
 
 // ---------------------------------------------------------------------------
 
+// Write one canonical element of order S to every stored copy in its block
+// (distinct permutations of the in-block offsets within runs of equal
+// block coordinates): an update applies fma(c, delta, M) to each copy's own
+// value (moments.cpp:294-299), an assignment stores the value.
+template <int S>
+__device__ void write_copies(double* m, const LowerElem& E, int n, int b, bool update, double c, double v) {
+  int j[S], o[S], e[S];
+#pragma unroll
+  for (int k = 0; k < S; ++k) {
+    j[k] = E.idx[k] / b;
+    o[k] = E.idx[k] - j[k] * b;
+    e[k] = ext_of(j[k], n, b);
+  }
+  bool runs = false;
+#pragma unroll
+  for (int k = 1; k < S; ++k) runs |= j[k] == j[k - 1];
+  for (;;) {
+    uint32_t off = 0;
+#pragma unroll
+    for (int k = 0; k < S; ++k) off = off * static_cast<uint32_t>(e[k]) + static_cast<uint32_t>(o[k]);
+    double* p = m + E.blk_off + off;
+    *p = update ? __fma_rn(c, v, *p) : v;
+    if (!runs) break;
+    // next distinct permutation within runs (odometer over runs, from the last)
+    int k = S - 1;
+    bool advanced = false;
+    while (k >= 0 && !advanced) {
+      int s0 = k;
+      while (s0 > 0 && j[s0 - 1] == j[k]) --s0;  // run [s0, k]
+      // std::next_permutation on o[s0..k]
+      int i = k - 1;
+      while (i >= s0 && o[i] >= o[i + 1]) --i;
+      if (i >= s0) {
+        int t = k;
+        while (o[t] <= o[i]) --t;
+        int tmp = o[i];
+        o[i] = o[t];
+        o[t] = tmp;
+        for (int l = i + 1, r = k; l < r; ++l, --r) {
+          tmp = o[l];
+          o[l] = o[r];
+          o[r] = tmp;
+        }
+        advanced = true;
+      } else {
+        for (int l = s0, r = k; l < r; ++l, --r) {
+          const int tmp = o[l];
+          o[l] = o[r];
+          o[r] = tmp;
+        }
+        k = s0 - 1;
+      }
+    }
+    if (!advanced) break;
+  }
+}
+
 // rows in flight per thread (register double buffer)
 template <int S>
 constexpr int low_unroll() { return S <= 2 ? 16 : S == 3 ? 8 : 4; }
@@ -249,59 +306,126 @@ __global__ void __launch_bounds__(128) moment_lower_kernel(const LowerParams P) 
     res[pass] = __dmul_rn(acc, P.inv);
   }
   if (!live) return;
-  // every stored copy: distinct permutations of the offsets within runs
-  const int b = P.b;
-  int j[S], o[S], e[S];
-#pragma unroll
-  for (int k = 0; k < S; ++k) {
-    j[k] = idx[k] / b;
-    o[k] = idx[k] - j[k] * b;
-    e[k] = ext_of(j[k], n, b);
-  }
   const bool update = P.npass == 2;
-  const double delta = update ? __dsub_rn(res[0], res[1]) : 0.0;
-  double* m = P.m;
-  bool runs = false;
+  write_copies<S>(P.m, E, n, P.b, update, P.c, update ? __dsub_rn(res[0], res[1]) : res[0]);
+}
+
+// Orders 1..ST (ST = d-2) of a window update or assignment, with the data
+// rows staged in shared memory (32-row chunks, cp.async, double buffered).
+// A thread owns up to W order-ST elements (pi, t0 + w) sharing the prefix
+// product P = x[pi_1] ... x[pi_{ST-1}] (left to right, moments.cpp:55,71),
+// adds round(P x[t0 + w]) in row order (moments.cpp:44) and, when its pi
+// represents them, the depth-s prefix products (the order-s tuples
+// (pi_1..pi_s), s < ST) -- so each element is the reference's plain
+// row-ordered sum of rounded products, times 1/rows.
+constexpr int LOW2_KC = 32;
+constexpr int LOW2_THREADS = 128;
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+
+template <int ST, int W>
+__global__ void __launch_bounds__(LOW2_THREADS) moment_lower2_kernel(const Lower2Params P) {
+  extern __shared__ double xs[];  // 2 x LOW2_KC x n
+  constexpr int NP = ST - 1;      // prefix length
+  constexpr int NR = NP > 0 ? NP : 1;
+  const int n = P.n;
+  const uint32_t tid = blockIdx.x * LOW2_THREADS + threadIdx.x;
+  const bool live = tid < P.nthreads;
+  const LowerThread T = P.threads[live ? tid : 0];
+  int pidx[NR];
 #pragma unroll
-  for (int k = 1; k < S; ++k) runs |= j[k] == j[k - 1];
-  for (;;) {
-    uint32_t off = 0;
+  for (int k = 0; k < NR; ++k) pidx[k] = NP > 0 ? T.pidx[k] : 0;
+  int col[W];
 #pragma unroll
-    for (int k = 0; k < S; ++k) off = off * static_cast<uint32_t>(e[k]) + static_cast<uint32_t>(o[k]);
-    double* p = m + E.blk_off + off;
-    *p = update ? __fma_rn(P.c, delta, *p) : res[0];
-    if (!runs) break;
-    // next distinct permutation within runs (odometer over runs, from the last)
-    int k = S - 1;
-    bool advanced = false;
-    while (k >= 0 && !advanced) {
-      int s0 = k;
-      while (s0 > 0 && j[s0 - 1] == j[k]) --s0;  // run [s0, k]
-      // std::next_permutation on o[s0..k]
-      int i = k - 1;
-      while (i >= s0 && o[i] >= o[i + 1]) --i;
-      if (i >= s0) {
-        int t = k;
-        while (o[t] <= o[i]) --t;
-        int tmp = o[i];
-        o[i] = o[t];
-        o[t] = tmp;
-        for (int l = i + 1, r = k; l < r; ++l, --r) {
-          tmp = o[l];
-          o[l] = o[r];
-          o[r] = tmp;
-        }
-        advanced = true;
-      } else {
-        for (int l = s0, r = k; l < r; ++l, --r) {
-          const int tmp = o[l];
-          o[l] = o[r];
-          o[r] = tmp;
-        }
-        k = s0 - 1;
+  for (int w = 0; w < W; ++w) col[w] = min(static_cast<int>(T.t0) + w, n - 1);
+  bool rep[NR];
+#pragma unroll
+  for (int k = 0; k < NR; ++k) rep[k] = NP > 0 && T.rep[k] != 0xffffffffu;
+  double res[2][W + NR];
+  const uint32_t K = P.K;
+  const uint32_t nchunks = (K + LOW2_KC - 1) / LOW2_KC;
+  for (int pass = 0; pass < P.npass; ++pass) {
+    const RowSource src = P.src[pass];
+    auto stage = [&](uint32_t ch, int buf) {
+      const uint32_t k0 = ch * LOW2_KC;
+      const uint32_t kc = min(static_cast<uint32_t>(LOW2_KC), K - k0);
+      double* dst = xs + static_cast<size_t>(buf) * LOW2_KC * n;
+      for (uint32_t r = 0; r < kc; ++r) {
+        const uint32_t k = k0 + r;
+        const double* row = k < src.len0 ? src.seg0 + static_cast<size_t>(k) * n
+                                         : src.seg1 + static_cast<size_t>(k - src.len0) * n;
+        for (int cI = threadIdx.x; cI < n; cI += LOW2_THREADS) cp_async8(dst + r * n + cI, row + cI);
       }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    double acc[W + NR];
+#pragma unroll
+    for (int w = 0; w < W + NR; ++w) acc[w] = 0.0;
+    stage(0, 0);
+    for (uint32_t ch = 0; ch < nchunks; ++ch) {
+      const int buf = ch & 1;
+      if (ch + 1 < nchunks) {
+        stage(ch + 1, buf ^ 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+      __syncthreads();
+      const double* xb = xs + static_cast<size_t>(buf) * LOW2_KC * n;
+      const uint32_t kc = min(static_cast<uint32_t>(LOW2_KC), K - ch * LOW2_KC);
+      if (kc == LOW2_KC) {
+#pragma unroll 4
+        for (uint32_t r = 0; r < LOW2_KC; ++r) {
+          const double* x = xb + r * n;
+          double pv = 1.0;
+#pragma unroll
+          for (int k = 0; k < NP; ++k) {
+            pv = k == 0 ? x[pidx[0]] : __dmul_rn(pv, x[pidx[k]]);
+            if (rep[k]) acc[W + k] = __dadd_rn(acc[W + k], pv);
+          }
+#pragma unroll
+          for (int w = 0; w < W; ++w) acc[w] = __dadd_rn(acc[w], NP > 0 ? __dmul_rn(pv, x[col[w]]) : x[col[w]]);
+        }
+      } else {
+        for (uint32_t r = 0; r < kc; ++r) {
+          const double* x = xb + r * n;
+          double pv = 1.0;
+#pragma unroll
+          for (int k = 0; k < NP; ++k) {
+            pv = k == 0 ? x[pidx[0]] : __dmul_rn(pv, x[pidx[k]]);
+            if (rep[k]) acc[W + k] = __dadd_rn(acc[W + k], pv);
+          }
+#pragma unroll
+          for (int w = 0; w < W; ++w) acc[w] = __dadd_rn(acc[w], NP > 0 ? __dmul_rn(pv, x[col[w]]) : x[col[w]]);
+        }
+      }
+      __syncthreads();  // the buffer is refilled next iteration
     }
-    if (!advanced) break;
+#pragma unroll
+    for (int w = 0; w < W + NR; ++w) res[pass][w] = __dmul_rn(acc[w], P.inv);
+  }
+  if (!live) return;
+  const bool update = P.npass == 2;
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    if (w >= T.cnt) break;
+    const double v = update ? __dsub_rn(res[0][w], res[1][w]) : res[0][w];
+    write_copies<ST>(P.m[ST - 1], P.elems[ST - 1][T.e0 + w], n, P.b, update, P.c, v);
+  }
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    if (!rep[k]) continue;
+    const double v = update ? __dsub_rn(res[0][W + k], res[1][W + k]) : res[0][W + k];
+    switch (k) {  // depth k + 1
+      case 0: write_copies<1>(P.m[0], P.elems[0][T.rep[0]], n, P.b, update, P.c, v); break;
+      case 1: write_copies<(ST > 2 ? 2 : 1)>(P.m[1], P.elems[1][T.rep[1]], n, P.b, update, P.c, v); break;
+      case 2: write_copies<(ST > 3 ? 3 : 1)>(P.m[2], P.elems[2][T.rep[2]], n, P.b, update, P.c, v); break;
+      default: break;
+    }
   }
 }
 
@@ -338,6 +462,121 @@ void launch_moms2cums_v2(int S, const M2CParams& p, uint64_t nblocks, cudaStream
     CSB_M2C(2) CSB_M2C(3) CSB_M2C(4) CSB_M2C(5) CSB_M2C(6)
 #undef CSB_M2C
     default: fail(CSB_EINVAL, "moms2cums: device path supports orders <= 6");
+  }
+  CSB_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+// The same work with the rows read through L1 instead of staged: a lean
+// kernel (<= 64 registers, no shared memory) that runs beside the DMMA
+// top-pair kernel on a side stream, in the registers and issue slots the
+// top kernel leaves free.  One element per thread (W = 1 thread table).
+template <int ST>
+__global__ void __launch_bounds__(LOW2_THREADS, 8) moment_lower_side_kernel(const Lower2Params P) {
+  constexpr int NP = ST - 1;
+  constexpr int NR = NP > 0 ? NP : 1;
+  constexpr int U = 4;  // rows in flight
+  const int n = P.n;
+  const uint32_t tid = blockIdx.x * LOW2_THREADS + threadIdx.x;
+  const bool live = tid < P.nthreads;
+  const LowerThread T = P.threads[live ? tid : 0];
+  int pidx[NR];
+#pragma unroll
+  for (int k = 0; k < NR; ++k) pidx[k] = NP > 0 ? T.pidx[k] : 0;
+  const int col = T.t0;
+  bool rep[NR];
+#pragma unroll
+  for (int k = 0; k < NR; ++k) rep[k] = NP > 0 && T.rep[k] != 0xffffffffu;
+  double res[2][1 + NR];
+  const uint32_t K = P.K;
+  for (int pass = 0; pass < P.npass; ++pass) {
+    const RowSource src = P.src[pass];
+    double acc[1 + NR];
+#pragma unroll
+    for (int w = 0; w < 1 + NR; ++w) acc[w] = 0.0;
+    double cur[U][NR + 1];
+    auto load = [&](uint32_t k0, double (&v)[U][NR + 1]) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t k = min(k0 + u, K - 1);
+        const double* row = k < src.len0 ? src.seg0 + static_cast<size_t>(k) * n
+                                         : src.seg1 + static_cast<size_t>(k - src.len0) * n;
+#pragma unroll
+        for (int t = 0; t < NP; ++t) v[u][t] = __ldg(row + pidx[t]);
+        v[u][NR] = __ldg(row + col);
+      }
+    };
+    load(0, cur);
+    for (uint32_t k0 = 0; k0 < K; k0 += U) {
+      double nxt[U][NR + 1];
+      if (k0 + U < K) load(k0 + U, nxt);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (k0 + u >= K) break;
+        double pv = 1.0;
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+          pv = k == 0 ? cur[u][0] : __dmul_rn(pv, cur[u][k]);
+          if (rep[k]) acc[1 + k] = __dadd_rn(acc[1 + k], pv);
+        }
+        acc[0] = __dadd_rn(acc[0], NP > 0 ? __dmul_rn(pv, cur[u][NR]) : cur[u][NR]);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int t = 0; t <= NR; ++t) cur[u][t] = nxt[u][t];
+    }
+#pragma unroll
+    for (int w = 0; w < 1 + NR; ++w) res[pass][w] = __dmul_rn(acc[w], P.inv);
+  }
+  if (!live) return;
+  const bool update = P.npass == 2;
+  {
+    const double v = update ? __dsub_rn(res[0][0], res[1][0]) : res[0][0];
+    write_copies<ST>(P.m[ST - 1], P.elems[ST - 1][T.e0], n, P.b, update, P.c, v);
+  }
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    if (!rep[k]) continue;
+    const double v = update ? __dsub_rn(res[0][1 + k], res[1][1 + k]) : res[0][1 + k];
+    switch (k) {
+      case 0: write_copies<1>(P.m[0], P.elems[0][T.rep[0]], n, P.b, update, P.c, v); break;
+      case 1: write_copies<(ST > 2 ? 2 : 1)>(P.m[1], P.elems[1][T.rep[1]], n, P.b, update, P.c, v); break;
+      case 2: write_copies<(ST > 3 ? 3 : 1)>(P.m[2], P.elems[2][T.rep[2]], n, P.b, update, P.c, v); break;
+      default: break;
+    }
+  }
+}
+
+void launch_moment_lower_side(int ST, const Lower2Params& p, cudaStream_t st) {
+  if (!p.nthreads) return;
+  const unsigned g = (p.nthreads + LOW2_THREADS - 1) / LOW2_THREADS;
+  switch (ST) {
+    case 1: moment_lower_side_kernel<1><<<g, LOW2_THREADS, 0, st>>>(p); break;
+    case 2: moment_lower_side_kernel<2><<<g, LOW2_THREADS, 0, st>>>(p); break;
+    case 3: moment_lower_side_kernel<3><<<g, LOW2_THREADS, 0, st>>>(p); break;
+    case 4: moment_lower_side_kernel<4><<<g, LOW2_THREADS, 0, st>>>(p); break;
+    default: fail(CSB_EINVAL, "moment_lower_side: order out of range");
+  }
+  CSB_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+void launch_moment_lower2(int ST, int W, const Lower2Params& p, cudaStream_t st) {
+  if (!p.nthreads) return;
+  const unsigned g = (p.nthreads + LOW2_THREADS - 1) / LOW2_THREADS;
+  const size_t sm = 2ull * LOW2_KC * p.n * sizeof(double);
+  switch (ST * 8 + W) {
+#define CSB_LOW2(SS, WW)                                                                                  \
+  case SS * 8 + WW:                                                                                       \
+    CSB_CUDA(cudaFuncSetAttribute(moment_lower2_kernel<SS, WW>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                  static_cast<int>(sm)));                                                 \
+    moment_lower2_kernel<SS, WW><<<g, LOW2_THREADS, sm, st>>>(p);                                         \
+    break;
+    CSB_LOW2(1, 1) CSB_LOW2(1, 4) CSB_LOW2(2, 1) CSB_LOW2(2, 4) CSB_LOW2(3, 1) CSB_LOW2(3, 4) CSB_LOW2(4, 1)
+    CSB_LOW2(4, 4)
+#undef CSB_LOW2
+    default: fail(CSB_EINVAL, "moment_lower2: order out of range");
   }
   CSB_CUDA(cudaGetLastError());
   count_launch();

@@ -68,6 +68,31 @@ struct LowerParams {
   double c = 0.0, inv = 1.0;
 };
 
+// One thread of the staged low-order kernel (orders 1..ST, ST = d-2 <= 4):
+// the order-ST elements (pi, t0 + w), w < cnt (consecutive in lexicographic
+// order, element ids e0 + w), and the lower-order tuples (pi_1..pi_s) it
+// represents (rep[s-1], 0xffffffff: none).
+struct LowerThread {
+  uint32_t e0;
+  uint32_t rep[3];
+  uint16_t pidx[4];
+  uint16_t t0, cnt;
+  uint32_t pad;
+};
+static_assert(sizeof(LowerThread) == 32, "LowerThread layout");
+
+struct Lower2Params {
+  RowSource src[2];
+  int npass = 1;
+  uint32_t K = 0;
+  int n = 0, b = 0;
+  const LowerThread* threads = nullptr;
+  uint32_t nthreads = 0;
+  const LowerElem* elems[4] = {nullptr, nullptr, nullptr, nullptr};  // orders 1..ST
+  double* m[4] = {nullptr, nullptr, nullptr, nullptr};                // M_1..M_ST
+  double c = 0.0, inv = 1.0;
+};
+
 struct NormParams {
   const double* partial[kMaxOrder];  // per order, nblocks each
   const double* mult[kMaxOrder];     // per order block multiplicities (as double)
@@ -83,6 +108,8 @@ void launch_moment_pair(const MomParams& p, int ntiles, bool top_fma, cudaStream
 void launch_moms2cums(int S, const M2CParams& p, uint64_t nblocks, cudaStream_t st);
 void launch_moms2cums_v2(int S, const M2CParams& p, uint64_t nblocks, cudaStream_t st);
 void launch_moment_lower(int S, const LowerParams& p, cudaStream_t st);
+void launch_moment_lower2(int ST, int W, const Lower2Params& p, cudaStream_t st);
+void launch_moment_lower_side(int ST, const Lower2Params& p, cudaStream_t st);
 void launch_copy_c1(const double* m1, double* c1, double* partial, const LayoutDev& lay,
                     uint64_t nblocks, uint64_t stored, cudaStream_t st);
 void launch_norm_finalize(const NormParams& p, cudaStream_t st);

@@ -126,19 +126,19 @@ struct Ring {
   uint32_t* rel;       // per stage: release counter (active warps per round)
   uint64_t* afull;     // per row set and slot: producer lanes stored
   uint64_t* aempty;    // per row set and slot: DMMA lanes consumed
-  int stages;
+  uint32_t stages;
   uint32_t active;       // warps that consume the staged chunks
   uint32_t chunks, cpp;  // chunks in total, per pass
 };
 
 // TMA bulk copies of data-row chunk i into its stage (one thread).
-__device__ __forceinline__ void issue_chunk(const MomParams& P, const Ring& g, uint32_t i) {
+__device__ __forceinline__ void issue_chunk(const MomParams& P, const Ring& g, uint32_t i, uint32_t st) {
   const int n = P.n;
   const uint32_t K = P.K;
   const uint32_t rb = static_cast<uint32_t>(n) * 8u;
-  const uint32_t st = i % g.stages;
-  const RowSource& src = P.src[i / g.cpp];
-  const uint32_t a0 = (i % g.cpp) * KC;
+  const uint32_t pass = i >= g.cpp ? 1u : 0u;
+  const RowSource& src = P.src[pass];
+  const uint32_t a0 = (i - pass * g.cpp) * KC;
   const uint32_t kc = min(static_cast<uint32_t>(KC), K - a0);
   double* dst = g.xs + st * static_cast<size_t>(KC) * n;
   mbar_expect_tx(g.xfull + st, static_cast<uint32_t>(KC) * rb);
@@ -154,20 +154,29 @@ __device__ __forceinline__ void issue_chunk(const MomParams& P, const Ring& g, u
   }
 }
 
-// A warp is done with chunk c: the last of the CTA's active warps to
-// release the stage refills it with chunk c + stages right away (the
-// per-stage release counters only grow; every `active`-th release is a
-// round's last).
-__device__ __forceinline__ void release_chunk(const MomParams& P, const Ring& g, uint32_t c) {
+// Position in the stage ring (stage index and mbarrier phase parity).
+struct Cursor {
+  uint32_t st = 0, ph = 0;
+  __device__ __forceinline__ void next(uint32_t stages) {
+    if (++st == stages) {
+      st = 0;
+      ph ^= 1u;
+    }
+  }
+};
+
+// A warp is done with chunk c (in stage st): the last of the CTA's active
+// warps to release the stage refills it with chunk c + stages right away
+// (atomicInc wraps the per-stage counter at `active`).
+__device__ __forceinline__ void release_chunk(const MomParams& P, const Ring& g, uint32_t c, uint32_t st) {
   __syncwarp();
   if ((threadIdx.x & 31) == 0) {
-    const uint32_t st = c % g.stages;
     __threadfence_block();  // this warp's reads of the stage happen before the release
-    const uint32_t old = atomicAdd(g.rel + st, 1u);
-    if ((old + 1) % g.active == 0 && c + g.stages < g.chunks) {
+    const uint32_t old = atomicInc(g.rel + st, g.active - 1);
+    if (old == g.active - 1 && c + g.stages < g.chunks) {
       __threadfence_block();
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before async-proxy writes
-      issue_chunk(P, g, c + g.stages);
+      issue_chunk(P, g, c + g.stages, st);
     }
   }
 }
@@ -177,9 +186,9 @@ __device__ __forceinline__ void release_chunk(const MomParams& P, const Ring& g,
 // Ring layout: aring[slot][t][(r * 4 + q) * ASTRIDE + g] holds the value of
 // row slot (r, g) at data row k = 4t + q of the chunk, so a DMMA lane
 // (r, q) loads its 8 fragments with 4 x LDS.128.
-template <int LM1>
+template <int LM1, int N>
 __device__ __forceinline__ void produce(const MomParams& P, const MomTile& tile, const Ring& g, int rs) {
-  const int n = P.n;
+  const int n = N ? N : P.n;
   const int lane = threadIdx.x & 31;
   const uint32_t set = tile.row0 + rs;
   const DmmaPair pr = P.pairs[static_cast<size_t>(set) * 32 + lane];
@@ -195,9 +204,10 @@ __device__ __forceinline__ void produce(const MomParams& P, const MomTile& tile,
   uint64_t* aempty = g.aempty + rs * ASLOTS;
   const int wofs = ((lane >> 2) * 4) * ASTRIDE + 2 * (lane & 3);
   double s0 = 0.0, s1 = 0.0, in0 = 0.0, in1 = 0.0;
-  for (uint32_t c = 0; c < g.chunks; ++c) {
-    const uint32_t st = c % g.stages;
-    mbar_wait(g.xfull + st, (c / g.stages) & 1u);
+  Cursor cur;
+  for (uint32_t c = 0; c < g.chunks; ++c, cur.next(g.stages)) {
+    const uint32_t st = cur.st;
+    mbar_wait(g.xfull + st, cur.ph);
     const uint32_t slot = c % ASLOTS;
     if (c >= ASLOTS) mbar_wait(aempty + slot, ((c / ASLOTS) - 1) & 1u);
     const double* xst = g.xs + st * stage_elems;
@@ -217,7 +227,7 @@ __device__ __forceinline__ void produce(const MomParams& P, const MomTile& tile,
         *reinterpret_cast<double2*>(as + t * 32 * ASTRIDE + q * ASTRIDE) = make_double2(v0, v1);
       }
     mbar_arrive(afull + slot);  // every lane: its stores are released
-    release_chunk(P, g, c);
+    release_chunk(P, g, c, st);
     if (update && c + 1 == g.cpp) {  // end of the incoming pass
       in0 = __dmul_rn(s0, P.inv);
       in1 = __dmul_rn(s1, P.inv);
@@ -246,10 +256,11 @@ __device__ __forceinline__ void produce(const MomParams& P, const MomTile& tile,
 // Lane (r, q): A fragment g = row slot (r, g) at k = q; B fragment c =
 // x[k = q][col + 8c + r]; accumulator (g, c, e) = row slot (r, g), column
 // col + 8c + 2q + e.
-template <int NC>
+template <int NC, int N>
 __device__ __forceinline__ void consume(const MomParams& P, const MomTile& tile, const Ring& g, int rs, int ct0,
                                         int warp) {
-  const int n = P.n, b = P.b;
+  const int n = N ? N : P.n;
+  const int b = P.b;
   const int lane = threadIdx.x & 31;
   const int r = lane >> 2, q = lane & 3;
   const uint32_t set = tile.row0 + rs;
@@ -267,10 +278,11 @@ __device__ __forceinline__ void consume(const MomParams& P, const MomTile& tile,
   for (int gg = 0; gg < 8; ++gg)
 #pragma unroll
     for (int c = 0; c < NC; ++c) acc[gg][c][0] = acc[gg][c][1] = 0.0;
-  for (uint32_t c = 0; c < g.chunks; ++c) {
-    const uint32_t st = c % g.stages;
+  Cursor cur;
+  for (uint32_t c = 0; c < g.chunks; ++c, cur.next(g.stages)) {
+    const uint32_t st = cur.st;
     const uint32_t slot = c % ASLOTS;
-    mbar_wait(g.xfull + st, (c / g.stages) & 1u);
+    mbar_wait(g.xfull + st, cur.ph);
     mbar_wait(afull + slot, (c / ASLOTS) & 1u);
     const double* as = aring + slot * ASLOT;
     const double* xb = g.xs + st * stage_elems + static_cast<size_t>(q) * n + colbase + r;
@@ -296,7 +308,7 @@ __device__ __forceinline__ void consume(const MomParams& P, const MomTile& tile,
         for (int gg = 0; gg < 8; ++gg) dmma(acc[gg][cc][0], acc[gg][cc][1], a[t & 1][gg], bb[t & 1][cc]);
     }
     mbar_arrive(aempty + slot);  // every lane has consumed the slot
-    release_chunk(P, g, c);
+    release_chunk(P, g, c, st);
     if (update && c + 1 == g.cpp) {
       // end of the incoming pass: stash its means, restart the accumulators
 #pragma unroll
@@ -369,6 +381,9 @@ __device__ __forceinline__ void consume(const MomParams& P, const MomTile& tile,
   }
 }
 
+// N: compile-time row length (0: runtime P.n) -- with it every shared-memory
+// address of the inner loops is a register plus an immediate
+template <int N>
 __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomParams P) {
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t bars[MAX_STAGES + 2 * PWARPS * ASLOTS];
@@ -378,7 +393,7 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
   const int nrs = static_cast<int>(tile.nrows); // live row sets (<= R)
   const int C = CWARPS / R;                     // column ranges
   Ring g;
-  g.stages = P.stages;
+  g.stages = static_cast<uint32_t>(P.stages);
   g.xs = smem;
   // reads past row n of the last stage (B fragments of the last column
   // tile) land in this padding and only feed outputs that are never stored
@@ -395,7 +410,7 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
   for (int w = 0; w < CWARPS; ++w) active += (w % R) < nrs;
   g.active = static_cast<uint32_t>(active);
   if (threadIdx.x == 0) {
-    for (int s = 0; s < g.stages; ++s) {
+    for (uint32_t s = 0; s < g.stages; ++s) {
       mbar_init(g.xfull + s, 1);
       rel[s] = 0;
     }
@@ -404,17 +419,17 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
       mbar_init(g.aempty + s, 32 * C);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (uint32_t i = 0; i < g.chunks && i < static_cast<uint32_t>(g.stages); ++i) issue_chunk(P, g, i);
+    for (uint32_t i = 0; i < g.chunks && i < g.stages; ++i) issue_chunk(P, g, i, i);
   }
   __syncthreads();
   if (warp >= CWARPS) {
     const int rs = warp - CWARPS;
     if (rs >= nrs) return;
     switch (P.L) {
-      case 2: produce<1>(P, tile, g, rs); break;
-      case 3: produce<2>(P, tile, g, rs); break;
-      case 4: produce<3>(P, tile, g, rs); break;
-      case 5: produce<4>(P, tile, g, rs); break;
+      case 2: produce<1, N>(P, tile, g, rs); break;
+      case 3: produce<2, N>(P, tile, g, rs); break;
+      case 4: produce<3, N>(P, tile, g, rs); break;
+      case 5: produce<4, N>(P, tile, g, rs); break;
       default: break;
     }
     return;
@@ -425,10 +440,10 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
   const int nct = static_cast<int>(tile.ncols);
   const int ct0 = nct * part / C, ct1 = nct * (part + 1) / C;
   switch (ct1 - ct0) {
-    case 1: consume<1>(P, tile, g, rs, ct0, warp); break;
-    case 2: consume<2>(P, tile, g, rs, ct0, warp); break;
-    case 3: consume<3>(P, tile, g, rs, ct0, warp); break;
-    case 4: consume<4>(P, tile, g, rs, ct0, warp); break;
+    case 1: consume<1, N>(P, tile, g, rs, ct0, warp); break;
+    case 2: consume<2, N>(P, tile, g, rs, ct0, warp); break;
+    case 3: consume<3, N>(P, tile, g, rs, ct0, warp); break;
+    case 4: consume<4, N>(P, tile, g, rs, ct0, warp); break;
     default: break;
   }
 }
@@ -486,7 +501,8 @@ size_t smem_bytes(int n, int stages) {
   return sizeof(double) * (static_cast<size_t>(stages) * KC * n + 64 + PWARPS * ASLOTS * ASLOT);
 }
 
-constexpr size_t kSmemLimit = 227 * 1024 - 1024;
+// leaves room for a co-resident low-order CTA (1 KB reserved shared memory per CTA)
+constexpr size_t kSmemLimit = 224 * 1024;
 
 int stages_for(int n) {
   int s = MAX_STAGES;
@@ -526,9 +542,13 @@ void launch_moment_top_dmma(const MomParams& p_in, int ntiles, cudaStream_t st) 
   p.stages = stages_for(p.n);
   if (p.stages < 2) fail(CSB_EINVAL, "moment_top_dmma: rows too wide for the staging ring");
   const size_t smem = smem_bytes(p.n, p.stages);
-  CSB_CUDA(cudaFuncSetAttribute(moment_top_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(smem)));
-  moment_top_dmma_kernel<<<ntiles, THREADS, smem, st>>>(p);
+  auto kern = p.n == 96 ? moment_top_dmma_kernel<96>
+            : p.n == 48 ? moment_top_dmma_kernel<48>
+            : p.n == 24 ? moment_top_dmma_kernel<24>
+            : p.n == 256 ? moment_top_dmma_kernel<256>
+                         : moment_top_dmma_kernel<0>;
+  CSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  kern<<<ntiles, THREADS, smem, st>>>(p);
   CSB_CUDA(cudaGetLastError());
   count_launch();
 }

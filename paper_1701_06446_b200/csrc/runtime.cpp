@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <unordered_map>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -56,10 +57,13 @@ struct DevLayout {
 struct Device {
   int id = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;  // low-order kernel beside the top pair
+  cudaEvent_t fork = nullptr, join = nullptr;
   std::mutex mu;
   std::map<std::tuple<int, int, int>, std::shared_ptr<DevLayout>> layouts;
   std::map<std::tuple<int, int, int, int>, std::shared_ptr<MomentPlan>> plans;
   std::map<std::tuple<int, int, int>, std::shared_ptr<DevBuf<LowerElem>>> lower;
+  std::map<std::tuple<int, int, int>, std::shared_ptr<DevBuf<LowerThread>>> lower2;
   std::map<std::tuple<int, int, int, int>, std::shared_ptr<ShardPlan>> shards;
   void* comm = nullptr;  // NCCL communicator (csb_comm_init)
   int nranks = 1, rank = 0;
@@ -83,6 +87,9 @@ Device& device() {
     slot = std::make_unique<Device>();
     slot->id = id;
     CSB_CUDA(cudaStreamCreateWithFlags(&slot->stream, cudaStreamNonBlocking));
+    CSB_CUDA(cudaStreamCreateWithFlags(&slot->side, cudaStreamNonBlocking));
+    CSB_CUDA(cudaEventCreateWithFlags(&slot->fork, cudaEventDisableTiming));
+    CSB_CUDA(cudaEventCreateWithFlags(&slot->join, cudaEventDisableTiming));
   }
   return *slot;
 }
@@ -215,6 +222,72 @@ std::shared_ptr<DevBuf<LowerElem>> get_lower_elems(Device& dev, int s, int n, in
   return slot;
 }
 
+// Thread table of the staged low-order kernel for orders 1..ST: the
+// order-ST tuples in lexicographic order, cut into runs of <= W sharing
+// their (ST-1)-prefix pi; a prefix's first run also represents the tuples
+// (pi_1..pi_s), s < ST, whose trailing coordinates pi_{s+1..} equal pi_s.
+std::shared_ptr<DevBuf<LowerThread>> get_lower2_threads(Device& dev, int ST, int n, int W) {
+  std::lock_guard<std::mutex> lk(dev.mu);
+  auto& slot = dev.lower2[{ST, n, W}];
+  if (!slot) {
+    auto key = [](const int* t, int s) {
+      uint64_t k = static_cast<uint64_t>(s);
+      for (int i = 0; i < s; ++i) k = k * 65536u + static_cast<uint64_t>(t[i]);
+      return k;
+    };
+    // lexicographic element ids of orders 1..ST-1 (the rep targets)
+    std::unordered_map<uint64_t, uint32_t> ids;
+    for (int s = 1; s < ST; ++s) {
+      int t[8] = {0};
+      uint32_t id = 0;
+      for (;;) {
+        ids[key(t, s)] = id++;
+        int k = s - 1;
+        while (k >= 0 && t[k] == n - 1) --k;
+        if (k < 0) break;
+        const int v = t[k] + 1;
+        for (int l = k; l < s; ++l) t[l] = v;
+      }
+    }
+    std::vector<LowerThread> v;
+    int t[8] = {0};
+    uint32_t id = 0;
+    for (;;) {
+      // t = (pi, t_ST) with t_ST = pi_last (or 0): the first tuple of pi
+      const int np = ST - 1;
+      const int first = np > 0 ? t[np - 1] : 0;
+      for (int t0 = first; t0 < n; t0 += W) {
+        LowerThread lt{};
+        lt.e0 = id;
+        for (int k = 0; k < np; ++k) lt.pidx[k] = static_cast<uint16_t>(t[k]);
+        lt.t0 = static_cast<uint16_t>(t0);
+        lt.cnt = static_cast<uint16_t>(std::min(W, n - t0));
+        for (int k = 0; k < 3; ++k) lt.rep[k] = 0xffffffffu;
+        if (t0 == first)
+          for (int s = 1; s <= np; ++s) {
+            bool ok = true;
+            for (int k = s; k < np; ++k) ok &= t[k] == t[s - 1];
+            if (ok) lt.rep[s - 1] = ids.at(key(t, s));
+          }
+        id += lt.cnt;
+        v.push_back(lt);
+      }
+      // next prefix pi (lexicographic)
+      if (np == 0) break;
+      int k = np - 1;
+      while (k >= 0 && t[k] == n - 1) --k;
+      if (k < 0) break;
+      const int val = t[k] + 1;
+      for (int l = k; l < np; ++l) t[l] = val;
+    }
+    require(id == multiset_count(n, ST), "lower2: element count mismatch");
+    auto buf = std::make_shared<DevBuf<LowerThread>>(v.size());
+    h2d_sync(buf->ptr, v.data(), buf->bytes());
+    slot = buf;
+  }
+  return slot;
+}
+
 }  // namespace
 
 void ensure_device() {
@@ -298,6 +371,11 @@ struct Scratch {
 };
 thread_local std::map<int, Scratch> g_scratch;
 // CSB_NO_DMMA=1 forces the DFMA kernel for the top pair (A/B testing)
+// CSB_LOW_INLINE=1 runs the low-order kernel in line (A/B testing)
+const bool g_low_side = [] {
+  const char* e = std::getenv("CSB_LOW_INLINE");
+  return !(e && e[0] == '1');
+}();
 const bool g_use_dmma = [] {
   const char* e = std::getenv("CSB_NO_DMMA");
   return !(e && e[0] == '1');
@@ -346,9 +424,43 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
   const bool use_dmma = g_use_dmma && dmma_supported(p);
   // sharding applies to the DMMA plan (the DFMA fallback computes all blocks)
   const bool sharded = use_dmma && sh.active() && !only_order;
-  if (lower) {
-    // orders <= d-2: element-parallel kernel, ahead of the top pair on the
-    // same stream (concurrent CTAs would hold SMs the DMMA tiles need)
+  // orders <= d-2 beside the DMMA top pair: a lean kernel on the side
+  // stream (joined at the end of this call) when they are few (it is
+  // latency bound and hides under the top pair); else staged, in line
+  const bool side = lower && d - 2 <= 4 && use_dmma && g_low_side && multiset_count(m->n, d - 2) <= 60000;
+  bool joined = true;
+  if (lower && d - 2 <= 4) {
+    ProfScope ps("moment_low", side ? dev.side : st);
+    const int ST = d - 2;
+    const int W = side ? 1 : multiset_count(m->n, ST) > 60000 ? 4 : 1;
+    auto th = get_lower2_threads(dev, ST, m->n, W);
+    Lower2Params lp;
+    lp.src[0] = src[0];
+    lp.src[1] = src[1];
+    lp.npass = npass;
+    lp.K = static_cast<uint32_t>(K);
+    lp.n = m->n;
+    lp.b = m->b;
+    lp.threads = th->ptr;
+    lp.nthreads = static_cast<uint32_t>(th->count);
+    for (int s = 1; s <= ST; ++s) {
+      lp.elems[s - 1] = get_lower_elems(dev, s, m->n, m->b, m->lay[s - 1]->host)->ptr;
+      lp.m[s - 1] = m->data[s - 1].ptr;
+    }
+    lp.c = c;
+    lp.inv = 1.0 / static_cast<double>(K);
+    if (side) {
+      std::lock_guard<std::mutex> lk(dev.mu);
+      CSB_CUDA(cudaEventRecord(dev.fork, st));
+      CSB_CUDA(cudaStreamWaitEvent(dev.side, dev.fork, 0));
+      launch_moment_lower_side(ST, lp, dev.side);
+      CSB_CUDA(cudaEventRecord(dev.join, dev.side));
+      joined = false;
+    } else {
+      launch_moment_lower2(ST, W, lp, st);
+    }
+  } else if (lower) {
+    // orders <= d-2 of d > 6: element-parallel kernel
     ProfScope ps("moment_low", st);
     for (int s = 1; s <= d - 2; ++s) {
       auto el = get_lower_elems(dev, s, m->n, m->b, m->lay[s - 1]->host);
@@ -405,6 +517,7 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
       launch_moment_pair(p, static_cast<int>(ntiles), true, st);
     }
   }
+  if (!joined) CSB_CUDA(cudaStreamWaitEvent(st, dev.join, 0));
 }
 
 void check_batch(uint64_t rows, uint64_t cols, const char* what) {
