@@ -15,7 +15,7 @@ from typing import Sequence
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libcumstream_b200.so")
+LIB_PATH = os.environ.get("CSB_LIB_PATH") or os.path.join(PKG, "lib", "libcumstream_b200.so")
 HEADER = os.path.join(os.path.dirname(PKG), "include", "cumstream_b200.h")
 
 OK, EINVAL, ERANGE, EDOMAIN, ERUNTIME = 0, 1, 2, 3, 4

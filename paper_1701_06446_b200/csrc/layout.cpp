@@ -1,6 +1,7 @@
 #include "layout.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <array>
 #include <numeric>
 
@@ -331,6 +332,26 @@ void MomentPlan::build_dmma(int S_, int n_, int b_, const Layout& top, const Lay
   auto width = [](const MomTile& t) { return (t.ncols + (4 / t.pad0) - 1) / (4 / t.pad0); };
   std::stable_sort(tiles.begin(), tiles.end(),
                    [&](const MomTile& a, const MomTile& c) { return width(a) > width(c); });
+  // Narrow tiles stream the most row bytes per DMMA (every tile stages
+  // whole rows): interleave them with wide ones so the L2 -> SM demand is
+  // spread over the launch instead of piling up at its end.  The last
+  // sixth keeps longest-first order for the tail.
+  {
+    static const bool plain = [] {
+      const char* e = std::getenv("CSB_TILE_ORDER_PLAIN");
+      return e && e[0] == '1';
+    }();
+    const size_t nt = tiles.size(), keep = nt / 6;
+    if (!plain && nt > keep + 2) {
+      std::vector<MomTile> mixed;
+      mixed.reserve(nt);
+      size_t lo = 0, hi = nt - keep;  // [lo, hi) interleaved from both ends
+      bool front = true;
+      while (lo < hi) mixed.push_back(front ? tiles[lo++] : tiles[--hi]), front = !front;
+      for (size_t i = nt - keep; i < nt; ++i) mixed.push_back(tiles[i]);
+      tiles.swap(mixed);
+    }
+  }
   for (size_t i = 0; i < tiles.size(); ++i) tiles[i].pad1 = static_cast<uint32_t>(i);
   scratch_per_tile = scratch;
 }

@@ -34,8 +34,13 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 
 #include "kernels.cuh"
+
+#ifndef CSB_EXP
+#define CSB_EXP 0  // timing experiments (tools/gpu_exp.sh); 0 in the product
+#endif
 
 namespace csb {
 
@@ -48,7 +53,7 @@ constexpr int HSTEPS = 4;                 // k4 steps per chunk
 constexpr int KC = 4 * HSTEPS;            // data rows per chunk / stage
 constexpr int ASTRIDE = 10;               // doubles per (r, q) entry: 8 used, bank-conflict free
 constexpr int ASLOT = HSTEPS * 32 * ASTRIDE;
-constexpr int ASLOTS = 2;                 // A-ring slots per row set
+constexpr int ASLOTS = 3;                 // A-ring slots per row set
 constexpr int MAX_STAGES = 12;
 constexpr int SLOTS_PER_SET = 64;         // prefix rows per row set
 
@@ -204,36 +209,126 @@ __device__ __forceinline__ void produce(const MomParams& P, const MomTile& tile,
   uint64_t* aempty = g.aempty + rs * ASLOTS;
   const int wofs = ((lane >> 2) * 4) * ASTRIDE + 2 * (lane & 3);
   double s0 = 0.0, s1 = 0.0, in0 = 0.0, in1 = 0.0;
+  // Explicit software pipeline: the operands of the next k4 step (4 data
+  // rows; across the chunk boundary too) are loaded before this step's
+  // products are formed and stored, so the loads are not held behind the
+  // A-ring stores and the rows' latency chains overlap.
+  constexpr int NV = LM1 + 2;
+  double xv[2][4][NV];
+  auto load = [&](const double* xst, int t, int buf) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double* xr = xst + (4 * t + q) * n;
+#pragma unroll
+      for (int u = 0; u < LM1; ++u) xv[buf][q][u] = xr[pidx[u]];
+      xv[buf][q][LM1] = xr[a0];
+      xv[buf][q][LM1 + 1] = xr[a1];
+    }
+  };
+  // The row sums lag the products by one k4 step: the adds of the previous
+  // step's products (a dependent chain per slot, ~40 cycles per add while
+  // the DMMA warps hold the FP64 pipe) are interleaved with this step's
+  // independent multiplications instead of serializing them.
+  double h0[4] = {0.0, 0.0, 0.0, 0.0}, h1[4] = {0.0, 0.0, 0.0, 0.0};  // held products (exact zeros at start)
+  auto form = [&](double* as, int t, int buf) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+#if (CSB_EXP & 3) == 3  // timing experiment: no producer work
+      (void)as;
+#else
+      double pv = xv[buf][q][0];
+#pragma unroll
+      for (int u = 1; u < LM1; ++u) pv = __dmul_rn(pv, xv[buf][q][u]);
+      const double v0 = __dmul_rn(pv, xv[buf][q][LM1]);
+      const double v1 = __dmul_rn(pv, xv[buf][q][LM1 + 1]);
+      s0 = __dadd_rn(s0, h0[q]);  // row order, plain adds (moments.cpp:44)
+      s1 = __dadd_rn(s1, h1[q]);
+      h0[q] = v0;
+      h1[q] = v1;
+      *reinterpret_cast<double2*>(as + t * 32 * ASTRIDE + q * ASTRIDE) = make_double2(v0, v1);
+#endif
+    }
+  };
+  auto flush = [&]() {  // add the held products (end of a pass)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      s0 = __dadd_rn(s0, h0[q]);
+      s1 = __dadd_rn(s1, h1[q]);
+      h0[q] = h1[q] = 0.0;
+    }
+  };
   Cursor cur;
-  for (uint32_t c = 0; c < g.chunks; ++c, cur.next(g.stages)) {
-    const uint32_t st = cur.st;
-    mbar_wait(g.xfull + st, cur.ph);
+  mbar_wait(g.xfull, 0);
+  const double* xst = g.xs;
+  load(xst, 0, 0);
+#if CSB_EXP & 128
+  uint64_t pt[16][4];
+#endif
+  for (uint32_t c = 0; c < g.chunks; ++c) {
+#if CSB_EXP & 128
+    uint64_t q0, q1, q2, q3;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(q0));
+#endif
+    Cursor nx = cur;
+    nx.next(g.stages);
+    const double* nxst = g.xs + nx.st * stage_elems;
     const uint32_t slot = c % ASLOTS;
+#if CSB_EXP & 128
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(q1));
+#endif
     if (c >= ASLOTS) mbar_wait(aempty + slot, ((c / ASLOTS) - 1) & 1u);
-    const double* xst = g.xs + st * stage_elems;
+#if CSB_EXP & 128
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(q2));
+    q3 = 0;
+#endif
     double* as = aring + slot * ASLOT + wofs;
 #pragma unroll
-    for (int t = 0; t < HSTEPS; ++t)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const double* xr = xst + (4 * t + q) * n;
-        double pv = xr[pidx[0]];
-#pragma unroll
-        for (int u = 1; u < LM1; ++u) pv = __dmul_rn(pv, xr[pidx[u]]);
-        const double v0 = __dmul_rn(pv, xr[a0]);
-        const double v1 = __dmul_rn(pv, xr[a1]);
-        s0 = __dadd_rn(s0, v0);  // row order, plain adds (moments.cpp:44)
-        s1 = __dadd_rn(s1, v1);
-        *reinterpret_cast<double2*>(as + t * 32 * ASTRIDE + q * ASTRIDE) = make_double2(v0, v1);
+    for (int t = 0; t < HSTEPS; ++t) {
+      if (t + 1 < HSTEPS) {
+        load(xst, t + 1, (t + 1) & 1);
+      } else if (c + 1 < g.chunks) {
+#if CSB_EXP & 128
+        uint64_t w0;
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(w0));
+        mbar_wait(g.xfull + nx.st, nx.ph);
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(q3));
+        q3 -= w0;
+#else
+        mbar_wait(g.xfull + nx.st, nx.ph);
+#endif
+        load(nxst, 0, (t + 1) & 1);
       }
-    mbar_arrive(afull + slot);  // every lane: its stores are released
-    release_chunk(P, g, c, st);
+      form(as, t, t & 1);
+    }
+#if CSB_EXP & 128
+    if (c >= 20 && c < 36) {
+      pt[c - 20][0] = q0;
+      pt[c - 20][1] = q1 - q0;
+      pt[c - 20][2] = q2 - q1;
+      pt[c - 20][3] = q3;
+    }
+#endif
+    // one arrival per warp: __syncwarp orders the lanes' A-ring stores
+    // before lane 0's (release) arrive
+    __syncwarp();
+    if (lane == 0) mbar_arrive(afull + slot);
+    release_chunk(P, g, c, cur.st);
     if (update && c + 1 == g.cpp) {  // end of the incoming pass
+      flush();
       in0 = __dmul_rn(s0, P.inv);
       in1 = __dmul_rn(s1, P.inv);
       s0 = s1 = 0.0;
     }
+    cur = nx;
+    xst = nxst;
   }
+  flush();
+#if CSB_EXP & 128
+  if (lane == 0 && (blockIdx.x % 53) == 0 && P.npass == 2)
+    for (int i = 1; i < 16; ++i)
+      printf("P %u %d %d %lld %lld %lld %lld\n", blockIdx.x, rs, i, (long long)(pt[i][0] - pt[i - 1][0]),
+             (long long)pt[i][1], (long long)pt[i][2], (long long)pt[i][3]);
+#endif
   // ---- order L = d-1: the row sums of this lane's two slots ----
   if (!do_low) return;
   const double cc = P.c;
@@ -255,7 +350,9 @@ __device__ __forceinline__ void produce(const MomParams& P, const MomTile& tile,
 // DMMA warp: row set rs, column tiles [ct0, ct0 + NC) of the CTA's range.
 // Lane (r, q): A fragment g = row slot (r, g) at k = q; B fragment c =
 // x[k = q][col + 8c + r]; accumulator (g, c, e) = row slot (r, g), column
-// col + 8c + 2q + e.
+// col + 8c + 2q + e.  The operand loads run one k4 step ahead across chunk
+// boundaries: the next chunk's barriers are checked and its first operands
+// loaded in the middle of the current chunk's last DMMA step.
 template <int NC, int N>
 __device__ __forceinline__ void consume(const MomParams& P, const MomTile& tile, const Ring& g, int rs, int ct0,
                                         int warp) {
@@ -268,47 +365,89 @@ __device__ __forceinline__ void consume(const MomParams& P, const MomTile& tile,
   const bool update = P.npass == 2;
   const size_t stage_elems = static_cast<size_t>(KC) * n;
   const double* aring = g.arings + static_cast<size_t>(rs) * ASLOTS * ASLOT + (r * 4 + q) * ASTRIDE;
+  const double* xlane = g.xs + static_cast<size_t>(q) * n + colbase + r;
   uint64_t* afull = g.afull + rs * ASLOTS;
   uint64_t* aempty = g.aempty + rs * ASLOTS;
   // pass-0 means of this thread (64 doubles), in the CTA's scratch
-  double* stash = P.scratch + static_cast<size_t>(blockIdx.x) * (CWARPS * 32 * 64);
+  double* __restrict__ stash = P.scratch + static_cast<size_t>(blockIdx.x) * (CWARPS * 32 * 64);
   const int tid = warp * 32 + lane;
   double acc[8][NC][2];
 #pragma unroll
   for (int gg = 0; gg < 8; ++gg)
 #pragma unroll
     for (int c = 0; c < NC; ++c) acc[gg][c][0] = acc[gg][c][1] = 0.0;
-  Cursor cur;
-  for (uint32_t c = 0; c < g.chunks; ++c, cur.next(g.stages)) {
-    const uint32_t st = cur.st;
-    const uint32_t slot = c % ASLOTS;
-    mbar_wait(g.xfull + st, cur.ph);
-    mbar_wait(afull + slot, (c / ASLOTS) & 1u);
-    const double* as = aring + slot * ASLOT;
-    const double* xb = g.xs + st * stage_elems + static_cast<size_t>(q) * n + colbase + r;
-    double a[2][8], bb[2][NC];
-    auto load = [&](int t, int buf) {
-      const double2* ap = reinterpret_cast<const double2*>(as + t * 32 * ASTRIDE);
+  double a[2][8], bb[2][NC];
+  auto load = [&](const double* as, const double* xb, int t, int buf) {
+    const double2* ap = reinterpret_cast<const double2*>(as + t * 32 * ASTRIDE);
 #pragma unroll
-      for (int s2 = 0; s2 < 4; ++s2) {
-        const double2 v = ap[s2];
-        a[buf][2 * s2] = v.x;
-        a[buf][2 * s2 + 1] = v.y;
-      }
-#pragma unroll
-      for (int cc = 0; cc < NC; ++cc) bb[buf][cc] = xb[static_cast<size_t>(4 * t) * n + 8 * cc];
-    };
-    load(0, 0);
-#pragma unroll
-    for (int t = 0; t < HSTEPS; ++t) {
-      if (t + 1 < HSTEPS) load(t + 1, (t + 1) & 1);
-#pragma unroll
-      for (int cc = 0; cc < NC; ++cc)
-#pragma unroll
-        for (int gg = 0; gg < 8; ++gg) dmma(acc[gg][cc][0], acc[gg][cc][1], a[t & 1][gg], bb[t & 1][cc]);
+    for (int s2 = 0; s2 < 4; ++s2) {
+      const double2 v = ap[s2];
+      a[buf][2 * s2] = v.x;
+      a[buf][2 * s2 + 1] = v.y;
     }
-    mbar_arrive(aempty + slot);  // every lane has consumed the slot
-    release_chunk(P, g, c, st);
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc) bb[buf][cc] = xb[static_cast<size_t>(4 * t) * n + 8 * cc];
+  };
+  auto mma_rows = [&](int buf, int g0, int g1) {
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+      for (int gg = g0; gg < g1; ++gg) dmma(acc[gg][cc][0], acc[gg][cc][1], a[buf][gg], bb[buf][cc]);
+  };
+#if CSB_EXP & 128
+  uint64_t tl[16][3], rl[16];
+#endif
+  // The x stage of a chunk is complete once its A slot is: the producer
+  // arrives on afull only after its own wait on the stage's TMA barrier.
+  Cursor cur;  // stage of chunk c
+  uint32_t slot = 0, aph = 0;
+  mbar_wait(afull, 0);
+  const double* as = aring;
+  const double* xb = xlane;
+  load(as, xb, 0, 0);
+  for (uint32_t c = 0; c < g.chunks; ++c) {
+    Cursor nx = cur;
+    nx.next(g.stages);
+    const uint32_t nslot = slot + 1 == ASLOTS ? 0 : slot + 1;
+    const uint32_t naph = nslot == 0 ? aph ^ 1u : aph;
+    const double* nas = aring + nslot * ASLOT;
+    const double* nxb = xlane + nx.st * stage_elems;
+#pragma unroll
+    for (int t = 0; t < HSTEPS - 1; ++t) {
+      load(as, xb, t + 1, (t + 1) & 1);
+      mma_rows(t & 1, 0, 8);
+    }
+    constexpr int LB = (HSTEPS - 1) & 1;
+    mma_rows(LB, 0, 4);
+    if (c + 1 < g.chunks) {
+#if CSB_EXP & 128  // timing experiment: per-chunk wait timeline of one warp
+      uint64_t t0, t1, t2;
+      asm volatile("mov.u64 %0, %%clock64;" : "=l"(t0));
+      asm volatile("mov.u64 %0, %%clock64;" : "=l"(t1));
+      mbar_wait(afull + nslot, naph);
+      asm volatile("mov.u64 %0, %%clock64;" : "=l"(t2));
+      if (c >= 20 && c < 36) {
+        tl[c - 20][0] = t0;
+        tl[c - 20][1] = t1;
+        tl[c - 20][2] = t2;
+      }
+#else
+      mbar_wait(afull + nslot, naph);
+#endif
+      load(nas, nxb, 0, LB ^ 1);
+    }
+    mma_rows(LB, 4, 8);
+#if CSB_EXP & 128
+    uint64_t r0, r1;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(r0));
+#endif
+    __syncwarp();  // every lane has consumed the slot
+    if (lane == 0) mbar_arrive(aempty + slot);
+    release_chunk(P, g, c, cur.st);
+#if CSB_EXP & 128
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(r1));
+    if (c >= 20 && c < 36) rl[c - 20] = r1 - r0;
+#endif
     if (update && c + 1 == g.cpp) {
       // end of the incoming pass: stash its means, restart the accumulators
 #pragma unroll
@@ -322,62 +461,108 @@ __device__ __forceinline__ void consume(const MomParams& P, const MomTile& tile,
             acc[gg][cc][e] = 0.0;
           }
     }
+    cur = nx;
+    slot = nslot;
+    aph = naph;
+    as = nas;
+    xb = nxb;
   }
 
+#if CSB_EXP & 128
+  if (lane == 0 && (blockIdx.x % 53) == 0 && P.npass == 2)
+    for (int i = 1; i < 16; ++i)
+      printf("C %u %d %d %d %lld %lld %lld %lld\n", blockIdx.x, warp, NC, i, (long long)(tl[i][0] - tl[i - 1][2]),
+             (long long)(tl[i][1] - tl[i][0]), (long long)(tl[i][2] - tl[i][1]), (long long)rl[i]);
+#endif
   // ---- epilogue: canonical entries only ----
   // Entries of blocks with equal neighbouring coordinates have symmetric
   // copies; for those the update's delta is also written to the delta
   // buffer at the canonical position and mirror_kernel applies it to every
-  // other stored copy (or copies the value, for an assignment).
-  const double cc = P.c;
+  // other stored copy (or copies the value, for an assignment).  Loads are
+  // batched (slot metadata, then the stash, then the old values per half)
+  // so each round trip to memory is paid a few times, not per slot.
+  const PrefixRow* __restrict__ rows = P.rows + static_cast<size_t>(set) * SLOTS_PER_SET + r * 8;
+  uint64_t tb[8];
+  uint32_t vp[8], po[8];
+  int il[8];
+  bool runs[8];
 #pragma unroll
   for (int gg = 0; gg < 8; ++gg) {
-    const PrefixRow& pr = P.rows[static_cast<size_t>(set) * SLOTS_PER_SET + r * 8 + gg];
-    if (pr.vprime == 0) continue;  // masked slot
-    const int iL = pr.idx[P.L - 1];
-    const bool row_runs = (pr.idx[7] & 1u) != 0;  // runs among (j_1..j_L)
-    const int J = iL / b;
-    size_t off[NC][2];
-    double val[NC][2];
-    bool ok[NC][2], diag[NC][2];
+    const uint4* pr = reinterpret_cast<const uint4*>(rows + gg);
+    const uint4 w0 = __ldg(pr), w1 = __ldg(pr + 1), w2 = __ldg(pr + 2);
+    const uint32_t li = static_cast<uint32_t>(P.L - 1);
+    const uint32_t word = li < 2 ? w0.x : li < 4 ? w0.y : li < 6 ? w0.z : w0.w;
+    il[gg] = static_cast<int>((li & 1) ? (word >> 16) : (word & 0xffffu));
+    runs[gg] = ((w0.w >> 16) & 1u) != 0;  // idx[7] bit 0: runs among (j_1..j_L)
+    tb[gg] = static_cast<uint64_t>(w1.x) | (static_cast<uint64_t>(w1.y) << 32);
+    vp[gg] = w2.x;
+    po[gg] = w2.y;
+  }
+  if (update) {
 #pragma unroll
-    for (int c = 0; c < NC; ++c)
+    for (int gg = 0; gg < 8; ++gg)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int col = colbase + 8 * c + 2 * q + e;
-        const int jd = col / b;
-        ok[c][e] = col < n && col >= iL;
-        diag[c][e] = row_runs || jd == J;
-        off[c][e] = pr.top_base + static_cast<uint64_t>(pr.vprime) * b * (jd - J) +
-                    static_cast<uint64_t>(pr.poff) * ext_of(jd, n, b) + (col - jd * b);
-        if (update) {
+      for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
           const size_t ix = static_cast<size_t>((gg * NC + c) * 2 + e) * (CWARPS * 32) + tid;
-          val[c][e] = __dsub_rn(stash[ix], __dmul_rn(acc[gg][c][e], P.inv));  // a - b
-        } else {
-          val[c][e] = __dmul_rn(acc[gg][c][e], P.inv);
+          acc[gg][c][e] = __dsub_rn(stash[ix], __dmul_rn(acc[gg][c][e], P.inv));  // a - b
         }
-      }
+  } else {
+#pragma unroll
+    for (int gg = 0; gg < 8; ++gg)
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) acc[gg][c][e] = __dmul_rn(acc[gg][c][e], P.inv);
+  }
+  double* __restrict__ top = P.top;
+  double* __restrict__ dtop = P.dtop;
+  const double cc = P.c;
+  // batches of GB slots: offsets are recomputed at the stores rather than
+  // kept live next to the loaded old values
+  constexpr int GB = NC >= 3 ? 2 : 4;
+  auto offset = [&](int gg, int c, int e, bool& ok, bool& diag) -> size_t {
+    const int col = colbase + 8 * c + 2 * q + e;
+    const int jd = col / b;
+    const int J = il[gg] / b;
+    ok = vp[gg] != 0 && col < n && col >= il[gg];
+    diag = runs[gg] || jd == J;
+    return tb[gg] + static_cast<uint64_t>(vp[gg]) * b * (jd - J) + static_cast<uint64_t>(po[gg]) * ext_of(jd, n, b) +
+           (col - jd * b);
+  };
+#pragma unroll
+  for (int g0 = 0; g0 < 8; g0 += GB) {
+    double old[GB][NC][2];
     if (update) {
-      double old[NC][2];
 #pragma unroll
-      for (int c = 0; c < NC; ++c)
+      for (int h = 0; h < GB; ++h)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) old[c][e] = ok[c][e] ? P.top[off[c][e]] : 0.0;
+        for (int c = 0; c < NC; ++c)
 #pragma unroll
-      for (int c = 0; c < NC; ++c)
-#pragma unroll
-        for (int e = 0; e < 2; ++e)
-          if (ok[c][e]) {
-            P.top[off[c][e]] = __fma_rn(cc, val[c][e], old[c][e]);
-            if (diag[c][e]) P.dtop[off[c][e]] = val[c][e];
+          for (int e = 0; e < 2; ++e) {
+            bool ok, diag;
+            const size_t o = offset(g0 + h, c, e, ok, diag);
+            old[h][c][e] = ok ? top[o] : 0.0;
           }
-    } else {
+    }
+#pragma unroll
+    for (int h = 0; h < GB; ++h)
 #pragma unroll
       for (int c = 0; c < NC; ++c)
 #pragma unroll
-        for (int e = 0; e < 2; ++e)
-          if (ok[c][e]) P.top[off[c][e]] = val[c][e];
-    }
+        for (int e = 0; e < 2; ++e) {
+          bool ok, diag;
+          const size_t o = offset(g0 + h, c, e, ok, diag);
+          if (!ok) continue;
+          const double v = acc[g0 + h][c][e];
+          if (update) {
+            top[o] = __fma_rn(cc, v, old[h][c][e]);
+            if (diag) dtop[o] = v;
+          } else {
+            top[o] = v;
+          }
+        }
   }
 }
 
@@ -388,6 +573,10 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t bars[MAX_STAGES + 2 * PWARPS * ASLOTS];
   __shared__ uint32_t rel[MAX_STAGES];
+#if CSB_EXP & 64
+  uint64_t t_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
   const MomTile tile = P.tiles[blockIdx.x];
   const int R = static_cast<int>(tile.pad0);    // row-set slots of this CTA: 1, 2, 4
   const int nrs = static_cast<int>(tile.nrows); // live row sets (<= R)
@@ -406,7 +595,11 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
   g.chunks = g.cpp * P.npass;  // incoming pass, then outgoing pass
   const int warp = threadIdx.x >> 5;
   // active warps: DMMA warps whose row set is live, one producer per live row set
+#if CSB_EXP & 16  // timing experiment: producers exit at once
+  int active = 0;
+#else
   int active = nrs;
+#endif
   for (int w = 0; w < CWARPS; ++w) active += (w % R) < nrs;
   g.active = static_cast<uint32_t>(active);
   if (threadIdx.x == 0) {
@@ -415,8 +608,8 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
       rel[s] = 0;
     }
     for (int s = 0; s < PWARPS * ASLOTS; ++s) {
-      mbar_init(g.afull + s, 32);
-      mbar_init(g.aempty + s, 32 * C);
+      mbar_init(g.afull + s, 1);
+      mbar_init(g.aempty + s, C);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (uint32_t i = 0; i < g.chunks && i < g.stages; ++i) issue_chunk(P, g, i, i);
@@ -424,7 +617,7 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
   __syncthreads();
   if (warp >= CWARPS) {
     const int rs = warp - CWARPS;
-    if (rs >= nrs) return;
+    if (rs >= nrs || (CSB_EXP & 16)) return;
     switch (P.L) {
       case 2: produce<1, N>(P, tile, g, rs); break;
       case 3: produce<2, N>(P, tile, g, rs); break;
@@ -446,6 +639,17 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
     case 4: consume<4, N>(P, tile, g, rs, ct0, warp); break;
     default: break;
   }
+#if CSB_EXP & 64  // timing experiment: per-CTA timeline of consumer warps
+  {
+    uint64_t t_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    if ((threadIdx.x & 31) == 0 && P.npass == 2)
+      printf("T %u %u %d %d %d %d %llu %llu\n", blockIdx.x, smid, warp, R, nrs, ct1 - ct0,
+             (unsigned long long)t_start, (unsigned long long)t_end);
+  }
+#endif
 }
 
 // Symmetric copies of the canonical entries written above, one CTA per

@@ -15,6 +15,7 @@ def main():
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--label", default="")
+    ap.add_argument("--p", type=int, default=0, help="override rows per step (experiments)")
     args = ap.parse_args()
     import torch
 
@@ -22,6 +23,9 @@ def main():
     from paper_1701_06446_b200.synth import CONFIGS, StreamGen
 
     cfg = CONFIGS[args.config]
+    if args.p:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, p=args.p)
     g = StreamGen(cfg)
     st = capi.Stream(cfg.n, cfg.d, cfg.T, cfg.p, cfg.b, g.window(), resync_every=0)
     xs = [torch.from_numpy(g.batch(1 + k % cfg.steps)).cuda() for k in range(args.steps + 3)]
