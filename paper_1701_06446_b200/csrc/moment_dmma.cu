@@ -49,11 +49,25 @@ namespace {
 constexpr int CWARPS = 4;                 // DMMA consumer warps
 constexpr int PWARPS = 4;                 // producer warps (one per row set)
 constexpr int THREADS = (CWARPS + PWARPS) * 32;
-constexpr int HSTEPS = 4;                 // k4 steps per chunk
-constexpr int KC = 4 * HSTEPS;            // data rows per chunk / stage
-constexpr int ASTRIDE = 10;               // doubles per (r, q) entry: 8 used, bank-conflict free
-constexpr int ASLOT = HSTEPS * 32 * ASTRIDE;
-constexpr int ASLOTS = 3;                 // A-ring slots per row set
+// Chunk geometry: HS k4 steps (4 HS data rows) per chunk, stage and A slot;
+// HS is a kernel template parameter (8, 6 or 4, whichever leaves >= 5 stages).
+constexpr int ASTRIDE = 8;                // doubles per (r, q) A-ring entry (swizzled, see apos)
+constexpr int ASLOTS = 2;                 // A-ring slots per row set
+template <int HS>
+struct Geo {
+  static constexpr int KC = 4 * HS;                  // data rows per chunk
+  static constexpr int ASLOT = HS * 32 * ASTRIDE;    // doubles per A slot
+};
+
+// A-ring entry e = 4 r + q holds the 8 fragments (16-byte chunks s = 0..3)
+// of row slots (r, 0..7) at one data row.  Entries are permuted and their
+// chunks XOR-swizzled so that both the producers' stores (fixed q, lanes
+// (r, gp)) and the DMMA warps' loads (fixed s, lanes (r, q)) are free of
+// shared-memory bank conflicts.
+__device__ __forceinline__ int apos(int e, int s) {
+  const int pe = e ^ ((e >> 2) & 1);
+  return pe * ASTRIDE + 2 * (s ^ ((pe >> 1) & 3));
+}
 constexpr int MAX_STAGES = 12;
 constexpr int SLOTS_PER_SET = 64;         // prefix rows per row set
 
@@ -131,7 +145,7 @@ struct Ring {
   uint32_t* rel;       // per stage: release counter (active warps per round)
   uint64_t* afull;     // per row set and slot: producer lanes stored
   uint64_t* aempty;    // per row set and slot: DMMA lanes consumed
-  uint32_t stages;
+  uint32_t stages, kc;   // stages, data rows per chunk
   uint32_t active;       // warps that consume the staged chunks
   uint32_t chunks, cpp;  // chunks in total, per pass
 };
@@ -143,13 +157,13 @@ __device__ __forceinline__ void issue_chunk(const MomParams& P, const Ring& g, u
   const uint32_t rb = static_cast<uint32_t>(n) * 8u;
   const uint32_t pass = i >= g.cpp ? 1u : 0u;
   const RowSource& src = P.src[pass];
+  const uint32_t KC = g.kc;
   const uint32_t a0 = (i - pass * g.cpp) * KC;
-  const uint32_t kc = min(static_cast<uint32_t>(KC), K - a0);
+  const uint32_t kc = min(KC, K - a0);
   double* dst = g.xs + st * static_cast<size_t>(KC) * n;
-  mbar_expect_tx(g.xfull + st, static_cast<uint32_t>(KC) * rb);
+  mbar_expect_tx(g.xfull + st, KC * rb);
   // rows past the end of the pass are zero rows: they add exact zeros
-  if (kc < static_cast<uint32_t>(KC))
-    bulk_g2s(dst + static_cast<size_t>(kc) * n, P.zeros, (KC - kc) * rb, g.xfull + st);
+  if (kc < KC) bulk_g2s(dst + static_cast<size_t>(kc) * n, P.zeros, (KC - kc) * rb, g.xfull + st);
   if (a0 + kc <= src.len0 || a0 >= src.len0) {
     bulk_g2s(dst, row_ptr(src, a0, n), kc * rb, g.xfull + st);
   } else {  // across the ring's wrap
@@ -191,8 +205,9 @@ __device__ __forceinline__ void release_chunk(const MomParams& P, const Ring& g,
 // Ring layout: aring[slot][t][(r * 4 + q) * ASTRIDE + g] holds the value of
 // row slot (r, g) at data row k = 4t + q of the chunk, so a DMMA lane
 // (r, q) loads its 8 fragments with 4 x LDS.128.
-template <int LM1, int N>
+template <int LM1, int N, int HS>
 __device__ __forceinline__ void produce(const MomParams& P, const MomTile& tile, const Ring& g, int rs) {
+  constexpr int HSTEPS = HS, KC = Geo<HS>::KC, ASLOT = Geo<HS>::ASLOT;
   const int n = N ? N : P.n;
   const int lane = threadIdx.x & 31;
   const uint32_t set = tile.row0 + rs;
@@ -207,7 +222,7 @@ __device__ __forceinline__ void produce(const MomParams& P, const MomTile& tile,
   double* aring = g.arings + static_cast<size_t>(rs) * ASLOTS * ASLOT;
   uint64_t* afull = g.afull + rs * ASLOTS;
   uint64_t* aempty = g.aempty + rs * ASLOTS;
-  const int wofs = ((lane >> 2) * 4) * ASTRIDE + 2 * (lane & 3);
+  const int pr_r = lane >> 2, pr_gp = lane & 3;
   double s0 = 0.0, s1 = 0.0, in0 = 0.0, in1 = 0.0;
   // Explicit software pipeline: the operands of the next k4 step (4 data
   // rows; across the chunk boundary too) are loaded before this step's
@@ -245,7 +260,7 @@ __device__ __forceinline__ void produce(const MomParams& P, const MomTile& tile,
       s1 = __dadd_rn(s1, h1[q]);
       h0[q] = v0;
       h1[q] = v1;
-      *reinterpret_cast<double2*>(as + t * 32 * ASTRIDE + q * ASTRIDE) = make_double2(v0, v1);
+      *reinterpret_cast<double2*>(as + t * 32 * ASTRIDE + apos(pr_r * 4 + q, pr_gp)) = make_double2(v0, v1);
 #endif
     }
   };
@@ -281,7 +296,7 @@ __device__ __forceinline__ void produce(const MomParams& P, const MomTile& tile,
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(q2));
     q3 = 0;
 #endif
-    double* as = aring + slot * ASLOT + wofs;
+    double* as = aring + slot * ASLOT;
 #pragma unroll
     for (int t = 0; t < HSTEPS; ++t) {
       if (t + 1 < HSTEPS) {
@@ -353,9 +368,10 @@ __device__ __forceinline__ void produce(const MomParams& P, const MomTile& tile,
 // col + 8c + 2q + e.  The operand loads run one k4 step ahead across chunk
 // boundaries: the next chunk's barriers are checked and its first operands
 // loaded in the middle of the current chunk's last DMMA step.
-template <int NC, int N>
+template <int NC, int N, int HS>
 __device__ __forceinline__ void consume(const MomParams& P, const MomTile& tile, const Ring& g, int rs, int ct0,
                                         int warp) {
+  constexpr int HSTEPS = HS, KC = Geo<HS>::KC, ASLOT = Geo<HS>::ASLOT;
   const int n = N ? N : P.n;
   const int b = P.b;
   const int lane = threadIdx.x & 31;
@@ -364,7 +380,7 @@ __device__ __forceinline__ void consume(const MomParams& P, const MomTile& tile,
   const int colbase = static_cast<int>(tile.col0) + 8 * ct0;
   const bool update = P.npass == 2;
   const size_t stage_elems = static_cast<size_t>(KC) * n;
-  const double* aring = g.arings + static_cast<size_t>(rs) * ASLOTS * ASLOT + (r * 4 + q) * ASTRIDE;
+  const double* aring = g.arings + static_cast<size_t>(rs) * ASLOTS * ASLOT;
   const double* xlane = g.xs + static_cast<size_t>(q) * n + colbase + r;
   uint64_t* afull = g.afull + rs * ASLOTS;
   uint64_t* aempty = g.aempty + rs * ASLOTS;
@@ -378,10 +394,10 @@ __device__ __forceinline__ void consume(const MomParams& P, const MomTile& tile,
     for (int c = 0; c < NC; ++c) acc[gg][c][0] = acc[gg][c][1] = 0.0;
   double a[2][8], bb[2][NC];
   auto load = [&](const double* as, const double* xb, int t, int buf) {
-    const double2* ap = reinterpret_cast<const double2*>(as + t * 32 * ASTRIDE);
+    const double* ap = as + t * 32 * ASTRIDE;
 #pragma unroll
     for (int s2 = 0; s2 < 4; ++s2) {
-      const double2 v = ap[s2];
+      const double2 v = *reinterpret_cast<const double2*>(ap + apos(lane, s2));
       a[buf][2 * s2] = v.x;
       a[buf][2 * s2 + 1] = v.y;
     }
@@ -568,8 +584,9 @@ __device__ __forceinline__ void consume(const MomParams& P, const MomTile& tile,
 
 // N: compile-time row length (0: runtime P.n) -- with it every shared-memory
 // address of the inner loops is a register plus an immediate
-template <int N>
+template <int N, int HS>
 __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomParams P) {
+  constexpr int KC = Geo<HS>::KC;
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t bars[MAX_STAGES + 2 * PWARPS * ASLOTS];
   __shared__ uint32_t rel[MAX_STAGES];
@@ -591,6 +608,7 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
   g.rel = rel;
   g.afull = bars + MAX_STAGES;
   g.aempty = g.afull + PWARPS * ASLOTS;
+  g.kc = KC;
   g.cpp = (P.K + KC - 1) / KC;
   g.chunks = g.cpp * P.npass;  // incoming pass, then outgoing pass
   const int warp = threadIdx.x >> 5;
@@ -619,10 +637,10 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
     const int rs = warp - CWARPS;
     if (rs >= nrs || (CSB_EXP & 16)) return;
     switch (P.L) {
-      case 2: produce<1, N>(P, tile, g, rs); break;
-      case 3: produce<2, N>(P, tile, g, rs); break;
-      case 4: produce<3, N>(P, tile, g, rs); break;
-      case 5: produce<4, N>(P, tile, g, rs); break;
+      case 2: produce<1, N, HS>(P, tile, g, rs); break;
+      case 3: produce<2, N, HS>(P, tile, g, rs); break;
+      case 4: produce<3, N, HS>(P, tile, g, rs); break;
+      case 5: produce<4, N, HS>(P, tile, g, rs); break;
       default: break;
     }
     return;
@@ -633,10 +651,10 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
   const int nct = static_cast<int>(tile.ncols);
   const int ct0 = nct * part / C, ct1 = nct * (part + 1) / C;
   switch (ct1 - ct0) {
-    case 1: consume<1, N>(P, tile, g, rs, ct0, warp); break;
-    case 2: consume<2, N>(P, tile, g, rs, ct0, warp); break;
-    case 3: consume<3, N>(P, tile, g, rs, ct0, warp); break;
-    case 4: consume<4, N>(P, tile, g, rs, ct0, warp); break;
+    case 1: consume<1, N, HS>(P, tile, g, rs, ct0, warp); break;
+    case 2: consume<2, N, HS>(P, tile, g, rs, ct0, warp); break;
+    case 3: consume<3, N, HS>(P, tile, g, rs, ct0, warp); break;
+    case 4: consume<4, N, HS>(P, tile, g, rs, ct0, warp); break;
     default: break;
   }
 #if CSB_EXP & 64  // timing experiment: per-CTA timeline of consumer warps
@@ -701,17 +719,24 @@ __global__ void __launch_bounds__(256) mirror_kernel(double* __restrict__ m, con
   }
 }
 
-size_t smem_bytes(int n, int stages) {
-  return sizeof(double) * (static_cast<size_t>(stages) * KC * n + 64 + PWARPS * ASLOTS * ASLOT);
+size_t smem_bytes(int n, int stages, int hs) {
+  return sizeof(double) * (static_cast<size_t>(stages) * 4 * hs * n + 64 + static_cast<size_t>(PWARPS) * ASLOTS * hs * 32 * ASTRIDE);
 }
 
 // leaves room for a co-resident low-order CTA (1 KB reserved shared memory per CTA)
 constexpr size_t kSmemLimit = 224 * 1024;
 
-int stages_for(int n) {
+int stages_for(int n, int hs) {
   int s = MAX_STAGES;
-  while (s > 0 && smem_bytes(n, s) > kSmemLimit) --s;
+  while (s > 0 && smem_bytes(n, s, hs) > kSmemLimit) --s;
   return s;
+}
+
+// the longest chunk that still leaves >= 5 stages (>= 2 at worst)
+int chunk_steps(int n) {
+  for (int hs : {8, 6, 4})
+    if (stages_for(n, hs) >= 5) return hs;
+  return 4;
 }
 
 }  // namespace
@@ -723,7 +748,7 @@ bool dmma_supported(const MomParams& p) {
   // instantiated for orders 3..6 (L = 2..5); rows must be 16-byte aligned
   // for the bulk copies, and at least two stages must fit
   if (p.n % 2 != 0 || p.L < 2 || p.L > 5) return false;
-  return stages_for(p.n) >= 2;
+  return stages_for(p.n, 4) >= 2;
 }
 
 void launch_mirror(int S, double* m, const double* delta, const LayoutDev& lay, const uint32_t* blocks,
@@ -743,14 +768,19 @@ void launch_mirror(int S, double* m, const double* delta, const LayoutDev& lay, 
 void launch_moment_top_dmma(const MomParams& p_in, int ntiles, cudaStream_t st) {
   if (ntiles <= 0) return;
   MomParams p = p_in;
-  p.stages = stages_for(p.n);
+  const int hs = chunk_steps(p.n);
+  p.stages = stages_for(p.n, hs);
   if (p.stages < 2) fail(CSB_EINVAL, "moment_top_dmma: rows too wide for the staging ring");
-  const size_t smem = smem_bytes(p.n, p.stages);
-  auto kern = p.n == 96 ? moment_top_dmma_kernel<96>
-            : p.n == 48 ? moment_top_dmma_kernel<48>
-            : p.n == 24 ? moment_top_dmma_kernel<24>
-            : p.n == 256 ? moment_top_dmma_kernel<256>
-                         : moment_top_dmma_kernel<0>;
+  const size_t smem = smem_bytes(p.n, p.stages, hs);
+  using K = void (*)(MomParams);
+  K kern = nullptr;
+  if (p.n == 96 && hs == 6) kern = moment_top_dmma_kernel<96, 6>;
+  else if (p.n == 48 && hs == 8) kern = moment_top_dmma_kernel<48, 8>;
+  else if (p.n == 24 && hs == 8) kern = moment_top_dmma_kernel<24, 8>;
+  else if (p.n == 256 && hs == 4) kern = moment_top_dmma_kernel<256, 4>;
+  else if (hs == 8) kern = moment_top_dmma_kernel<0, 8>;
+  else if (hs == 6) kern = moment_top_dmma_kernel<0, 6>;
+  else kern = moment_top_dmma_kernel<0, 4>;
   CSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   kern<<<ntiles, THREADS, smem, st>>>(p);
   CSB_CUDA(cudaGetLastError());
