@@ -34,6 +34,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstdio>
 
 #include "kernels.cuh"
@@ -734,6 +735,12 @@ int stages_for(int n, int hs) {
 
 // the longest chunk that still leaves >= 5 stages (>= 2 at worst)
 int chunk_steps(int n) {
+  static const int forced = [] {  // CSB_HS=4|6|8 (experiments)
+    const char* e = std::getenv("CSB_HS");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (forced == 4 || forced == 6 || forced == 8)
+    if (stages_for(n, forced) >= 2) return forced;
   for (int hs : {8, 6, 4})
     if (stages_for(n, hs) >= 5) return hs;
   return 4;
@@ -775,6 +782,7 @@ void launch_moment_top_dmma(const MomParams& p_in, int ntiles, cudaStream_t st) 
   using K = void (*)(MomParams);
   K kern = nullptr;
   if (p.n == 96 && hs == 6) kern = moment_top_dmma_kernel<96, 6>;
+  else if (p.n == 96 && hs == 8) kern = moment_top_dmma_kernel<96, 8>;
   else if (p.n == 48 && hs == 8) kern = moment_top_dmma_kernel<48, 8>;
   else if (p.n == 24 && hs == 8) kern = moment_top_dmma_kernel<24, 8>;
   else if (p.n == 256 && hs == 4) kern = moment_top_dmma_kernel<256, 4>;
