@@ -98,52 +98,43 @@ __global__ void __launch_bounds__(256) moms2cums_v2(const M2CParams P) {
   const uint64_t boff = LS.offset[blk];
   const uint32_t vol = static_cast<uint32_t>(LS.offset[blk + 1] - boff);
 
-  if (threadIdx.x == 0) {
+  // sub-block geometry: one mask per thread (offsets precomputed on the
+  // host, MomentPlan-style, instead of ranking them here)
+  const uint64_t* subs = P.subs + blk * (NM - 1);
+  for (int m = 1 + static_cast<int>(threadIdx.x); m < NM; m += blockDim.x) {
+    uint32_t stride = 1;
+#pragma unroll
+    for (int k = S - 1; k >= 0; --k) {
+      if (m >> k & 1) {
+        sstride[m][k] = stride;
+        stride *= static_cast<uint32_t>(e[k]);
+      } else {
+        sstride[m][k] = 0;
+      }
+    }
+    if (!STAGED) sbase[m] = subs[m - 1];
+  }
+  if (STAGED && threadIdx.x == 0) {
     uint32_t soff = 0;
     for (int m = 1; m < NM; ++m) {
-      int sub[S], cnt = 0;
       uint32_t svol = 1;
       for (int k = 0; k < S; ++k)
-        if (m >> k & 1) {
-          sub[cnt++] = j[k];
-          svol *= static_cast<uint32_t>(e[k]);
-        }
-      const LayoutDev& Lq = P.lay[cnt - 1];
-      const uint64_t g = Lq.offset[rank_dev(Lq, sub, cnt)];
-      uint32_t stride = 1;
-      for (int k = S - 1; k >= 0; --k) {
-        if (m >> k & 1) {
-          sstride[m][k] = stride;
-          stride *= static_cast<uint32_t>(e[k]);
-        } else {
-          sstride[m][k] = 0;
-        }
-      }
-      if (STAGED) {
-        sbase[m] = soff;  // offset of the staged copy in shared memory
-        soff += svol;
-      } else {
-        sbase[m] = g;     // offset in C_|m|
-      }
+        if (m >> k & 1) svol *= static_cast<uint32_t>(e[k]);
+      sbase[m] = soff;  // offset of the staged copy in shared memory
+      soff += svol;
     }
   }
   __syncthreads();
   if (STAGED) {
     // copy every needed sub-block into shared memory (coalesced per subset)
-    uint32_t soff = 0;
     for (int m = 1; m < NM; ++m) {
-      int sub[S], cnt = 0;
       uint32_t svol = 1;
 #pragma unroll
       for (int k = 0; k < S; ++k)
-        if (m >> k & 1) {
-          sub[cnt++] = j[k];
-          svol *= static_cast<uint32_t>(e[k]);
-        }
-      const LayoutDev& Lq = P.lay[cnt - 1];
-      const double* src = P.lower[cnt - 1] + Lq.offset[rank_dev(Lq, sub, cnt)];
-      for (uint32_t t = threadIdx.x; t < svol; t += blockDim.x) sfac[soff + t] = src[t];
-      soff += svol;
+        if (m >> k & 1) svol *= static_cast<uint32_t>(e[k]);
+      const double* src = P.lower[popcount_c(m) - 1] + subs[m - 1];
+      double* dst = sfac + sbase[m];
+      for (uint32_t t = threadIdx.x; t < svol; t += blockDim.x) dst[t] = src[t];
     }
     __syncthreads();
   }

@@ -48,6 +48,7 @@ struct M2CParams {
   LayoutDev lay[kMaxOrder];         // layouts of orders 1..S (index s-1)
   int n = 0, b = 0;
   uint64_t blk0 = 0;                // first block of the shard
+  const uint64_t* subs = nullptr;   // per block, masks 1..2^S-2: offset of the sub-block in C_|mask|
   double* partial = nullptr;        // per block: sum over stored entries of v*v
 };
 

@@ -64,6 +64,7 @@ struct Device {
   std::map<std::tuple<int, int, int, int>, std::shared_ptr<MomentPlan>> plans;
   std::map<std::tuple<int, int, int>, std::shared_ptr<DevBuf<LowerElem>>> lower;
   std::map<std::tuple<int, int, int>, std::shared_ptr<DevBuf<LowerThread>>> lower2;
+  std::map<std::tuple<int, int, int>, std::shared_ptr<DevBuf<uint64_t>>> subs;
   std::map<std::tuple<int, int, int, int>, std::shared_ptr<ShardPlan>> shards;
   void* comm = nullptr;  // NCCL communicator (csb_comm_init)
   int nranks = 1, rank = 0;
@@ -217,6 +218,34 @@ std::shared_ptr<DevBuf<LowerElem>> get_lower_elems(Device& dev, int s, int n, in
     }
     auto buf = std::make_shared<DevBuf<LowerElem>>(v.size());
     h2d_sync(buf->ptr, v.data(), buf->bytes());
+    slot = buf;
+  }
+  return slot;
+}
+
+// Sub-block offsets for moms2cums of order S: for every block j and every
+// proper non-empty subset m of its positions, the offset in C_|m| of the
+// block (j_k : k in m) (cumulants.cpp:163-171 reads C_|P|[i_P] there).
+std::shared_ptr<DevBuf<uint64_t>> get_subs(Device& dev, int S, int n, int b) {
+  std::vector<std::shared_ptr<DevLayout>> lays;
+  for (int k = 1; k <= S; ++k) lays.push_back(get_layout(dev, k, n, b));
+  std::lock_guard<std::mutex> lk(dev.mu);
+  auto& slot = dev.subs[{S, n, b}];
+  if (!slot) {
+    const Layout& LS = lays[S - 1]->host;
+    const int NM = (1 << S) - 1;
+    std::vector<uint64_t> v(LS.nblocks * static_cast<uint64_t>(NM - 1));
+    int sub[kMaxOrder];
+    for (uint64_t r = 0; r < LS.nblocks; ++r)
+      for (int m = 1; m < NM; ++m) {
+        int cnt = 0;
+        for (int k = 0; k < S; ++k)
+          if (m >> k & 1) sub[cnt++] = LS.index[r * S + k];
+        const Layout& Lq = lays[cnt - 1]->host;
+        v[r * (NM - 1) + (m - 1)] = Lq.offset[Lq.rank(sub)];
+      }
+    auto buf = std::make_shared<DevBuf<uint64_t>>(v.size());
+    if (!v.empty()) h2d_sync(buf->ptr, v.data(), buf->bytes());
     slot = buf;
   }
   return slot;
@@ -553,6 +582,7 @@ void run_moms2cums(const csb_series* m, csb_series* c, NormScratch& ns, cudaStre
     for (int k = 1; k <= s; ++k) p.lay[k - 1] = m->lay[k - 1]->view();
     p.n = m->n;
     p.b = m->b;
+    p.subs = get_subs(*m->dev, s, m->n, m->b)->ptr;
     if (s == d && sh.active()) {
       // C_d only for the owned blocks; the other partials stay zero so a
       // sum over ranks reproduces the unsharded partial array exactly
