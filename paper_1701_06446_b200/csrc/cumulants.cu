@@ -139,25 +139,61 @@ __global__ void __launch_bounds__(256) moms2cums_v2(const M2CParams P) {
     __syncthreads();
   }
 
-  // phase 1: canonical entries
-  for (uint32_t pos = threadIdx.x; pos < vol; pos += blockDim.x) {
-    int o[S];
-    decode<S>(pos, e, o);
-    if (!canonical<S>(j, o)) continue;
-    double f[NM];
+  // phase 1: canonical entries.  Full blocks (all extents b) walk the
+  // precomputed canonical positions of their run pattern -- no lane idles
+  // on the non-canonical copies of diagonal blocks -- and address a factor
+  // in its staged sub-block with compile-time powers of b; edge blocks test
+  // every position.
+  bool full = true;
 #pragma unroll
-    for (int m = 1; m < NM; ++m) {
-      uint32_t a = 0;
+  for (int k = 0; k < S; ++k) full &= e[k] == b;
+  if (STAGED && full && P.canon) {
+    uint32_t pat = 0;
 #pragma unroll
-      for (int k = 0; k < S; ++k)
-        if (m >> k & 1) a += static_cast<uint32_t>(o[k]) * sstride[m][k];
-      if (STAGED)
+    for (int k = 1; k < S; ++k) pat |= static_cast<uint32_t>(j[k] == j[k - 1]) << (k - 1);
+    const uint32_t* list = P.canon + P.canon_off[pat];
+    const uint32_t cnt = P.canon_off[pat + 1] - P.canon_off[pat];
+    uint32_t bp[S];  // b^0 .. b^(S-1)
+    bp[0] = 1;
+#pragma unroll
+    for (int k = 1; k < S; ++k) bp[k] = bp[k - 1] * static_cast<uint32_t>(b);
+    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+      const uint32_t pos = __ldg(list + i);
+      int o[S];
+      decode<S>(pos, e, o);
+      double f[NM];
+#pragma unroll
+      for (int m = 1; m < NM; ++m) {
+        uint32_t a = 0;
+        int after = 0;  // positions of m after k (compile-time after unrolling)
+#pragma unroll
+        for (int k = S - 1; k >= 0; --k)
+          if (m >> k & 1) a += static_cast<uint32_t>(o[k]) * bp[after++];
         f[m] = sfac[sbase[m] + a];
-      else
-        f[m] = P.lower[popcount_c(m) - 1][sbase[m] + a];
+      }
+      const double corr = partition_correction<S>(f);
+      P.c[boff + pos] = __dsub_rn(P.m[boff + pos], corr);
     }
-    const double corr = partition_correction<S>(f);
-    P.c[boff + pos] = __dsub_rn(P.m[boff + pos], corr);
+  } else {
+    for (uint32_t pos = threadIdx.x; pos < vol; pos += blockDim.x) {
+      int o[S];
+      decode<S>(pos, e, o);
+      if (!canonical<S>(j, o)) continue;
+      double f[NM];
+#pragma unroll
+      for (int m = 1; m < NM; ++m) {
+        uint32_t a = 0;
+#pragma unroll
+        for (int k = 0; k < S; ++k)
+          if (m >> k & 1) a += static_cast<uint32_t>(o[k]) * sstride[m][k];
+        if (STAGED)
+          f[m] = sfac[sbase[m] + a];
+        else
+          f[m] = P.lower[popcount_c(m) - 1][sbase[m] + a];
+      }
+      const double corr = partition_correction<S>(f);
+      P.c[boff + pos] = __dsub_rn(P.m[boff + pos], corr);
+    }
   }
   __syncthreads();  // canonical entries of this block are visible to the CTA
 

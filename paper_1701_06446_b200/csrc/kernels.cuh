@@ -49,6 +49,10 @@ struct M2CParams {
   int n = 0, b = 0;
   uint64_t blk0 = 0;                // first block of the shard
   const uint64_t* subs = nullptr;   // per block, masks 1..2^S-2: offset of the sub-block in C_|mask|
+  // canonical positions of a full block (all extents b) per run pattern
+  // (bit k-1: j_k == j_{k-1}): canon[canon_off[pat] .. canon_off[pat + 1])
+  const uint32_t* canon = nullptr;
+  const uint32_t* canon_off = nullptr;
   double* partial = nullptr;        // per block: sum over stored entries of v*v
 };
 

@@ -65,6 +65,7 @@ struct Device {
   std::map<std::tuple<int, int, int>, std::shared_ptr<DevBuf<LowerElem>>> lower;
   std::map<std::tuple<int, int, int>, std::shared_ptr<DevBuf<LowerThread>>> lower2;
   std::map<std::tuple<int, int, int>, std::shared_ptr<DevBuf<uint64_t>>> subs;
+  std::map<std::pair<int, int>, std::pair<std::shared_ptr<DevBuf<uint32_t>>, std::shared_ptr<DevBuf<uint32_t>>>> canon;
   std::map<std::tuple<int, int, int, int>, std::shared_ptr<ShardPlan>> shards;
   void* comm = nullptr;  // NCCL communicator (csb_comm_init)
   int nranks = 1, rank = 0;
@@ -249,6 +250,42 @@ std::shared_ptr<DevBuf<uint64_t>> get_subs(Device& dev, int S, int n, int b) {
     slot = buf;
   }
   return slot;
+}
+
+// Canonical in-block positions of a full order-S block (extents b) for each
+// run pattern (bit k-1 set: j_k == j_{k-1}): offsets non-decreasing within
+// runs (cumulants.cpp:163-168), C-order positions, ascending.
+std::pair<const uint32_t*, const uint32_t*> get_canon(Device& dev, int S, int b) {
+  std::lock_guard<std::mutex> lk(dev.mu);
+  auto& slot = dev.canon[{S, b}];
+  if (!slot.first) {
+    uint64_t vol = 1;
+    for (int k = 0; k < S; ++k) vol *= static_cast<uint64_t>(b);
+    std::vector<uint32_t> list, off;
+    const uint32_t npat = 1u << (S - 1);
+    int o[kMaxOrder];
+    for (uint32_t pat = 0; pat < npat; ++pat) {
+      off.push_back(static_cast<uint32_t>(list.size()));
+      for (uint64_t pos = 0; pos < vol; ++pos) {
+        uint64_t rem = pos;
+        for (int k = S - 1; k >= 0; --k) {
+          o[k] = static_cast<int>(rem % static_cast<uint64_t>(b));
+          rem /= static_cast<uint64_t>(b);
+        }
+        bool ok = true;
+        for (int k = 1; k < S; ++k)
+          if ((pat >> (k - 1) & 1) && o[k] < o[k - 1]) ok = false;
+        if (ok) list.push_back(static_cast<uint32_t>(pos));
+      }
+    }
+    off.push_back(static_cast<uint32_t>(list.size()));
+    auto l = std::make_shared<DevBuf<uint32_t>>(list.size());
+    auto o2 = std::make_shared<DevBuf<uint32_t>>(off.size());
+    h2d_sync(l->ptr, list.data(), l->bytes());
+    h2d_sync(o2->ptr, off.data(), o2->bytes());
+    slot = {l, o2};
+  }
+  return {slot.first->ptr, slot.second->ptr};
 }
 
 // Thread table of the staged low-order kernel for orders 1..ST: the
@@ -583,6 +620,15 @@ void run_moms2cums(const csb_series* m, csb_series* c, NormScratch& ns, cudaStre
     p.n = m->n;
     p.b = m->b;
     p.subs = get_subs(*m->dev, s, m->n, m->b)->ptr;
+    {
+      uint64_t vol = 1;
+      for (int k = 0; k < s; ++k) vol *= static_cast<uint64_t>(m->b);
+      if (vol <= (1ull << 20)) {  // canonical-position lists for full blocks
+        auto cl = get_canon(*m->dev, s, m->b);
+        p.canon = cl.first;
+        p.canon_off = cl.second;
+      }
+    }
     if (s == d && sh.active()) {
       // C_d only for the owned blocks; the other partials stay zero so a
       // sum over ranks reproduces the unsharded partial array exactly
