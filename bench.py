@@ -318,9 +318,18 @@ def main() -> None:
     tr_path = os.path.join(ROOT, "profiles", "moment_top_traffic.json")
     if os.path.exists(tr_path):
         try:
-            traffic = json.load(open(tr_path)).get("bytes_per_launch")
+            tr = json.load(open(tr_path))
+            if tr.get("workload") == cfg.name:
+                traffic = tr.get("bytes_per_launch")
         except (OSError, ValueError):
             traffic = None
+    hbm_peak = None
+    try:
+        hbm_peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs")
+    except (OSError, ValueError):
+        hbm_peak = None
+    if not hbm_peak:
+        hbm_peak = 6650.0  # profiling recipe fallback
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -339,10 +348,14 @@ def main() -> None:
                        "step": "exchange + moments_update(M1..M4) + moms2cums(C1..C4) + report(nu3, nu4)"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "kernel": "moment_pair_kernel<true> (orders 4 and 3)",
+                         "kernel": f"moment_top_dmma_kernel (orders {cfg.d} and {cfg.d - 1}, FP64 DMMA)",
                          "flops_per_launch": flops["F_top_launch"], "avg_launch_ms": top_avg_s * 1e3,
                          "launches": top_n, "peak_source": peak_src,
-                         "note": "FP64 path: bound is the FP64 pipe (DFMA/DMMA), not bf16 tensor"},
+                         "note": "FP64 path: bound is the FP64 pipe (DFMA/DMMA), not bf16 tensor",
+                         "hbm": ({"traffic_bytes": traffic, "achieved_gbs": traffic / top_avg_s / 1e9,
+                                  "peak_gbs": hbm_peak, "frac": traffic / top_avg_s / 1e9 / hbm_peak,
+                                  "source": "ncu dram__bytes_read+write of one launch (profiles/moment_top_traffic.json)"}
+                                 if traffic and top_n else None)},
             "step_flops": {"F_alg": flops["F_alg"], "F_mom": flops["F_mom"], "F_m2c": flops["F_m2c"],
                            "alg_tflops_per_s": flops["F_alg"] / (dev_s / args.steps) / 1e12},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": cfg.p * cfg.n * 8,
