@@ -47,9 +47,10 @@ namespace csb {
 
 namespace {
 
-constexpr int CWARPS = 4;                 // DMMA consumer warps
+constexpr int CWARPS = 8;                 // DMMA consumer warps (two per SM sub-partition)
 constexpr int PWARPS = 4;                 // producer warps (one per row set)
 constexpr int THREADS = (CWARPS + PWARPS) * 32;
+constexpr int MAXNC = 2;                  // column tiles per DMMA warp
 // Chunk geometry: HS k4 steps (4 HS data rows) per chunk, stage and A slot;
 // HS is a kernel template parameter (8, 6 or 4, whichever leaves >= 5 stages).
 constexpr int ASTRIDE = 8;                // doubles per (r, q) A-ring entry (swizzled, see apos)
@@ -386,7 +387,7 @@ __device__ __forceinline__ void consume(const MomParams& P, const MomTile& tile,
   uint64_t* afull = g.afull + rs * ASLOTS;
   uint64_t* aempty = g.aempty + rs * ASLOTS;
   // pass-0 means of this thread (64 doubles), in the CTA's scratch
-  double* __restrict__ stash = P.scratch + static_cast<size_t>(blockIdx.x) * (CWARPS * 32 * 64);
+  double* __restrict__ stash = P.scratch + static_cast<size_t>(blockIdx.x) * (CWARPS * 32 * 16 * MAXNC);
   const int tid = warp * 32 + lane;
   double acc[8][NC][2];
 #pragma unroll
@@ -598,7 +599,9 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
   const MomTile tile = P.tiles[blockIdx.x];
   const int R = static_cast<int>(tile.pad0);    // row-set slots of this CTA: 1, 2, 4
   const int nrs = static_cast<int>(tile.nrows); // live row sets (<= R)
-  const int C = CWARPS / R;                     // column ranges
+  const int C = CWARPS / R;                     // column ranges per row set
+  const int nct = static_cast<int>(tile.ncols);
+  const int cparts = nct < C ? nct : C;          // non-empty column ranges
   Ring g;
   g.stages = static_cast<uint32_t>(P.stages);
   g.xs = smem;
@@ -619,7 +622,10 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
 #else
   int active = nrs;
 #endif
-  for (int w = 0; w < CWARPS; ++w) active += (w % R) < nrs;
+  for (int w = 0; w < CWARPS; ++w) {
+    const int part = w / R;
+    active += (w % R) < nrs && nct * (part + 1) / C > nct * part / C;
+  }
   g.active = static_cast<uint32_t>(active);
   if (threadIdx.x == 0) {
     for (uint32_t s = 0; s < g.stages; ++s) {
@@ -628,7 +634,7 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
     }
     for (int s = 0; s < PWARPS * ASLOTS; ++s) {
       mbar_init(g.afull + s, 1);
-      mbar_init(g.aempty + s, C);
+      mbar_init(g.aempty + s, cparts);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (uint32_t i = 0; i < g.chunks && i < g.stages; ++i) issue_chunk(P, g, i, i);
@@ -649,13 +655,11 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
   const int rs = warp % R;
   if (rs >= nrs) return;
   const int part = warp / R;
-  const int nct = static_cast<int>(tile.ncols);
   const int ct0 = nct * part / C, ct1 = nct * (part + 1) / C;
+  static_assert(MAXNC == 2, "column tiles per DMMA warp");
   switch (ct1 - ct0) {
     case 1: consume<1, N, HS>(P, tile, g, rs, ct0, warp); break;
     case 2: consume<2, N, HS>(P, tile, g, rs, ct0, warp); break;
-    case 3: consume<3, N, HS>(P, tile, g, rs, ct0, warp); break;
-    case 4: consume<4, N, HS>(P, tile, g, rs, ct0, warp); break;
     default: break;
   }
 #if CSB_EXP & 64  // timing experiment: per-CTA timeline of consumer warps
@@ -749,7 +753,7 @@ int chunk_steps(int n) {
 }  // namespace
 
 // per tile: the incoming pass's means (64 values per consumer thread)
-size_t dmma_scratch_per_tile() { return static_cast<size_t>(CWARPS) * 32 * 64; }
+size_t dmma_scratch_per_tile() { return static_cast<size_t>(CWARPS) * 32 * 16 * MAXNC; }
 
 bool dmma_supported(const MomParams& p) {
   // instantiated for orders 3..6 (L = 2..5); rows must be 16-byte aligned
