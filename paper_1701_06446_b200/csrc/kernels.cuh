@@ -28,8 +28,8 @@ struct MomParams {
   double* scratch = nullptr;  // pass-0 stash (DMMA: per tile)
   const double* zeros = nullptr;  // DMMA: >= 16 x n zero doubles (tail rows of a pass)
   int stages = 0;                 // DMMA: row-chunk stages in shared memory
-  double* dtop = nullptr;         // DMMA update: canonical deltas of M_S (diagonal blocks)
-  double* dlow = nullptr;         // DMMA update: canonical deltas of M_{S-1}
+  int ones4 = 0;                  // DMMA: row sums on the DMMA pipe in R = 4 windows with <= ones4 column tiles
+  bool ones_r12 = false;          // DMMA: ... and in spare sub-partition slots of R = 1 / 2 tiles
   double c = 0.0;             // p / T        (moments.cpp:287)
   double inv = 1.0;           // 1.0 / rows   (moments.cpp:148)
 };
@@ -137,7 +137,9 @@ bool dmma_supported(const MomParams& p);
 size_t dmma_scratch_per_tile();
 void launch_moment_top_dmma(const MomParams& p, int ntiles, cudaStream_t st);
 // copies of canonical entries in blocks with runs (after the DMMA kernel)
-void launch_mirror(int S, double* m, const double* delta, const LayoutDev& lay, const uint32_t* blocks,
-                   uint32_t nblocks, int n, int b, bool update, double c, cudaStream_t st);
+// symmetric copies of the canonical entries of the listed stored blocks
+// (lists: per run pattern (dst, src) pairs of a full block, or nullptr)
+void launch_mirror(int S, double* m, const LayoutDev& lay, const uint32_t* blocks, uint32_t nblocks, int n, int b,
+                   const uint2* lists, const uint32_t* list_off, cudaStream_t st);
 
 }  // namespace csb

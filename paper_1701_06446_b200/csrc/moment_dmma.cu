@@ -33,6 +33,7 @@
 // the canonical entries (mirror_kernel then fixes the symmetric copies).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <cstdio>
@@ -148,6 +149,7 @@ struct Ring {
   uint64_t* afull;     // per row set and slot: producer lanes stored
   uint64_t* aempty;    // per row set and slot: DMMA lanes consumed
   uint32_t stages, kc;   // stages, data rows per chunk
+  uint32_t aslots, alog;  // A-ring slots per live row set (PWARPS x ASLOTS / R) and log2
   uint32_t active;       // warps that consume the staged chunks
   uint32_t chunks, cpp;  // chunks in total, per pass
 };
@@ -207,7 +209,7 @@ __device__ __forceinline__ void release_chunk(const MomParams& P, const Ring& g,
 // Ring layout: aring[slot][t][(r * 4 + q) * ASTRIDE + g] holds the value of
 // row slot (r, g) at data row k = 4t + q of the chunk, so a DMMA lane
 // (r, q) loads its 8 fragments with 4 x LDS.128.
-template <int LM1, int N, int HS>
+template <int LM1, int N, int HS, bool SUMS>
 __device__ __forceinline__ void produce(const MomParams& P, const MomTile& tile, const Ring& g, int rs) {
   constexpr int HSTEPS = HS, KC = Geo<HS>::KC, ASLOT = Geo<HS>::ASLOT;
   const int n = N ? N : P.n;
@@ -219,11 +221,10 @@ __device__ __forceinline__ void produce(const MomParams& P, const MomTile& tile,
   for (int t = 0; t < LM1; ++t) pidx[t] = pr.pidx[t];
   const int a0 = pr.a0, a1 = pr.a1;
   const bool update = P.npass == 2;
-  const bool do_low = P.low != nullptr && tile.low;
   const size_t stage_elems = static_cast<size_t>(KC) * n;
-  double* aring = g.arings + static_cast<size_t>(rs) * ASLOTS * ASLOT;
-  uint64_t* afull = g.afull + rs * ASLOTS;
-  uint64_t* aempty = g.aempty + rs * ASLOTS;
+  double* aring = g.arings + static_cast<size_t>(rs) * g.aslots * ASLOT;
+  uint64_t* afull = g.afull + rs * g.aslots;
+  uint64_t* aempty = g.aempty + rs * g.aslots;
   const int pr_r = lane >> 2, pr_gp = lane & 3;
   double s0 = 0.0, s1 = 0.0, in0 = 0.0, in1 = 0.0;
   // Explicit software pipeline: the operands of the next k4 step (4 data
@@ -258,15 +259,18 @@ __device__ __forceinline__ void produce(const MomParams& P, const MomTile& tile,
       for (int u = 1; u < LM1; ++u) pv = __dmul_rn(pv, xv[buf][q][u]);
       const double v0 = __dmul_rn(pv, xv[buf][q][LM1]);
       const double v1 = __dmul_rn(pv, xv[buf][q][LM1 + 1]);
-      s0 = __dadd_rn(s0, h0[q]);  // row order, plain adds (moments.cpp:44)
-      s1 = __dadd_rn(s1, h1[q]);
-      h0[q] = v0;
-      h1[q] = v1;
+      if (SUMS) {
+        s0 = __dadd_rn(s0, h0[q]);  // row order, plain adds (moments.cpp:44)
+        s1 = __dadd_rn(s1, h1[q]);
+        h0[q] = v0;
+        h1[q] = v1;
+      }
       *reinterpret_cast<double2*>(as + t * 32 * ASTRIDE + apos(pr_r * 4 + q, pr_gp)) = make_double2(v0, v1);
 #endif
     }
   };
   auto flush = [&]() {  // add the held products (end of a pass)
+    if (!SUMS) return;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       s0 = __dadd_rn(s0, h0[q]);
@@ -276,6 +280,10 @@ __device__ __forceinline__ void produce(const MomParams& P, const MomTile& tile,
   };
   Cursor cur;
   mbar_wait(g.xfull, 0);
+#if CSB_EXP & 64
+  long long pwait_e = 0, pwait_x = 0;
+  const long long pl0 = clock64();
+#endif
   const double* xst = g.xs;
   load(xst, 0, 0);
 #if CSB_EXP & 128
@@ -289,11 +297,19 @@ __device__ __forceinline__ void produce(const MomParams& P, const MomTile& tile,
     Cursor nx = cur;
     nx.next(g.stages);
     const double* nxst = g.xs + nx.st * stage_elems;
-    const uint32_t slot = c % ASLOTS;
+    const uint32_t slot = c & (g.aslots - 1);
 #if CSB_EXP & 128
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(q1));
 #endif
-    if (c >= ASLOTS) mbar_wait(aempty + slot, ((c / ASLOTS) - 1) & 1u);
+#if CSB_EXP & 64
+    {
+      const long long w0 = clock64();
+      if (c >= g.aslots) mbar_wait(aempty + slot, ((c >> g.alog) - 1) & 1u);
+      pwait_e += clock64() - w0;
+    }
+#else
+    if (c >= g.aslots) mbar_wait(aempty + slot, ((c >> g.alog) - 1) & 1u);
+#endif
 #if CSB_EXP & 128
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(q2));
     q3 = 0;
@@ -310,6 +326,12 @@ __device__ __forceinline__ void produce(const MomParams& P, const MomTile& tile,
         mbar_wait(g.xfull + nx.st, nx.ph);
         asm volatile("mov.u64 %0, %%clock64;" : "=l"(q3));
         q3 -= w0;
+#elif CSB_EXP & 64
+        {
+          const long long w0 = clock64();
+          mbar_wait(g.xfull + nx.st, nx.ph);
+          pwait_x += clock64() - w0;
+        }
 #else
         mbar_wait(g.xfull + nx.st, nx.ph);
 #endif
@@ -340,6 +362,10 @@ __device__ __forceinline__ void produce(const MomParams& P, const MomTile& tile,
     xst = nxst;
   }
   flush();
+#if CSB_EXP & 64
+  if (lane == 0 && P.npass == 2)
+    printf("P %u %d %lld %lld %lld\n", blockIdx.x, rs, pwait_e, pwait_x, clock64() - pl0);
+#endif
 #if CSB_EXP & 128
   if (lane == 0 && (blockIdx.x % 53) == 0 && P.npass == 2)
     for (int i = 1; i < 16; ++i)
@@ -347,7 +373,7 @@ __device__ __forceinline__ void produce(const MomParams& P, const MomTile& tile,
              (long long)pt[i][1], (long long)pt[i][2], (long long)pt[i][3]);
 #endif
   // ---- order L = d-1: the row sums of this lane's two slots ----
-  if (!do_low) return;
+  if (!SUMS) return;
   const double cc = P.c;
 #pragma unroll
   for (int e = 0; e < 2; ++e) {
@@ -357,12 +383,21 @@ __device__ __forceinline__ void produce(const MomParams& P, const MomTile& tile,
     if (update) {
       const double delta = __dsub_rn(e ? in1 : in0, __dmul_rn(s, P.inv));  // a - b
       P.low[row.low_off] = __fma_rn(cc, delta, P.low[row.low_off]);
-      if (row.idx[7] & 1u) P.dlow[row.low_off] = delta;
     } else {
       P.low[row.low_off] = __dmul_rn(s, P.inv);
     }
   }
 }
+
+#if CSB_EXP & 64
+__shared__ uint64_t exp_t[2][CWARPS];  // per DMMA warp: first A slot ready, main loop done
+__shared__ uint64_t exp_w[CWARPS + PWARPS][2];  // per warp: clock64 cycles waiting (A slot / stage), loop cycles
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
 
 // DMMA warp: row set rs, column tiles [ct0, ct0 + NC) of the CTA's range.
 // Lane (r, q): A fragment g = row slot (r, g) at k = q; B fragment c =
@@ -370,22 +405,31 @@ __device__ __forceinline__ void produce(const MomParams& P, const MomTile& tile,
 // col + 8c + 2q + e.  The operand loads run one k4 step ahead across chunk
 // boundaries: the next chunk's barriers are checked and its first operands
 // loaded in the middle of the current chunk's last DMMA step.
-template <int NC, int N, int HS>
+// ONES: the warp's last tile is the row-sum tile: B = 1.0 in every column,
+// so its accumulators are the order-(d-1) row sums -- each DMMA output is
+// the sequential fma(A, 1.0, acc) = acc + A chain, i.e. exactly the
+// reference's row-ordered plain adds (moments.cpp:44) -- and the producer
+// skips its own adds.  Used where a sub-partition has a spare tile slot.
+template <int NC, int N, int HS, int B, bool ONES>
 __device__ __forceinline__ void consume(const MomParams& P, const MomTile& tile, const Ring& g, int rs, int ct0,
                                         int warp) {
   constexpr int HSTEPS = HS, KC = Geo<HS>::KC, ASLOT = Geo<HS>::ASLOT;
   const int n = N ? N : P.n;
-  const int b = P.b;
+  const int b = B ? B : P.b;  // compile-time block size where instantiated
   const int lane = threadIdx.x & 31;
   const int r = lane >> 2, q = lane & 3;
   const uint32_t set = tile.row0 + rs;
   const int colbase = static_cast<int>(tile.col0) + 8 * ct0;
   const bool update = P.npass == 2;
   const size_t stage_elems = static_cast<size_t>(KC) * n;
-  const double* aring = g.arings + static_cast<size_t>(rs) * ASLOTS * ASLOT;
+  const double* aring = g.arings + static_cast<size_t>(rs) * g.aslots * ASLOT;
+#if CSB_EXP & 8  // timing experiment: conflict-free (wrong) B addresses
+  const double* xlane = g.xs + static_cast<size_t>(q) * (n + 4) + colbase + r;
+#else
   const double* xlane = g.xs + static_cast<size_t>(q) * n + colbase + r;
-  uint64_t* afull = g.afull + rs * ASLOTS;
-  uint64_t* aempty = g.aempty + rs * ASLOTS;
+#endif
+  uint64_t* afull = g.afull + rs * g.aslots;
+  uint64_t* aempty = g.aempty + rs * g.aslots;
   // pass-0 means of this thread (64 doubles), in the CTA's scratch
   double* __restrict__ stash = P.scratch + static_cast<size_t>(blockIdx.x) * (CWARPS * 32 * 16 * MAXNC);
   const int tid = warp * 32 + lane;
@@ -404,29 +448,48 @@ __device__ __forceinline__ void consume(const MomParams& P, const MomTile& tile,
       a[buf][2 * s2 + 1] = v.y;
     }
 #pragma unroll
-    for (int cc = 0; cc < NC; ++cc) bb[buf][cc] = xb[static_cast<size_t>(4 * t) * n + 8 * cc];
+    for (int cc = 0; cc < NC; ++cc)
+      bb[buf][cc] = (ONES && cc == NC - 1) ? 1.0 : xb[static_cast<size_t>(4 * t) * n + 8 * cc];
   };
   auto mma_rows = [&](int buf, int g0, int g1) {
 #pragma unroll
     for (int cc = 0; cc < NC; ++cc)
 #pragma unroll
-      for (int gg = g0; gg < g1; ++gg) dmma(acc[gg][cc][0], acc[gg][cc][1], a[buf][gg], bb[buf][cc]);
+      for (int gg = g0; gg < g1; ++gg) {
+#if CSB_EXP & 4  // timing experiment: no DMMAs (operands still loaded)
+        asm volatile("" ::"d"(a[buf][gg]), "d"(bb[buf][cc]));
+#else
+        dmma(acc[gg][cc][0], acc[gg][cc][1], a[buf][gg], bb[buf][cc]);
+#endif
+      }
   };
 #if CSB_EXP & 128
   uint64_t tl[16][3], rl[16];
 #endif
   // The x stage of a chunk is complete once its A slot is: the producer
   // arrives on afull only after its own wait on the stage's TMA barrier.
+#ifdef CSB_STAGGER  // timing experiment: the second DMMA warp of each SM sub-partition starts late
+  if (warp & 4) {
+    const long long t0 = clock64();
+    while (clock64() - t0 < CSB_STAGGER) {
+    }
+  }
+#endif
   Cursor cur;  // stage of chunk c
   uint32_t slot = 0, aph = 0;
   mbar_wait(afull, 0);
+#if CSB_EXP & 64
+  exp_t[0][warp] = gtimer();
+  long long cwait = 0;
+  const long long cl0 = clock64();
+#endif
   const double* as = aring;
   const double* xb = xlane;
   load(as, xb, 0, 0);
   for (uint32_t c = 0; c < g.chunks; ++c) {
     Cursor nx = cur;
     nx.next(g.stages);
-    const uint32_t nslot = slot + 1 == ASLOTS ? 0 : slot + 1;
+    const uint32_t nslot = slot + 1 == g.aslots ? 0 : slot + 1;
     const uint32_t naph = nslot == 0 ? aph ^ 1u : aph;
     const double* nas = aring + nslot * ASLOT;
     const double* nxb = xlane + nx.st * stage_elems;
@@ -448,6 +511,12 @@ __device__ __forceinline__ void consume(const MomParams& P, const MomTile& tile,
         tl[c - 20][0] = t0;
         tl[c - 20][1] = t1;
         tl[c - 20][2] = t2;
+      }
+#elif CSB_EXP & 64
+      {
+        const long long w0 = clock64();
+        mbar_wait(afull + nslot, naph);
+        cwait += clock64() - w0;
       }
 #else
       mbar_wait(afull + nslot, naph);
@@ -492,6 +561,12 @@ __device__ __forceinline__ void consume(const MomParams& P, const MomTile& tile,
       printf("C %u %d %d %d %lld %lld %lld %lld\n", blockIdx.x, warp, NC, i, (long long)(tl[i][0] - tl[i - 1][2]),
              (long long)(tl[i][1] - tl[i][0]), (long long)(tl[i][2] - tl[i][1]), (long long)rl[i]);
 #endif
+#if CSB_EXP & 64
+  exp_t[1][warp] = gtimer();
+  exp_w[warp][0] = cwait;
+  exp_w[warp][1] = clock64() - cl0;
+  const long long e0 = clock64();
+#endif
   // ---- epilogue: canonical entries only ----
   // Entries of blocks with equal neighbouring coordinates have symmetric
   // copies; for those the update's delta is also written to the delta
@@ -503,7 +578,6 @@ __device__ __forceinline__ void consume(const MomParams& P, const MomTile& tile,
   uint64_t tb[8];
   uint32_t vp[8], po[8];
   int il[8];
-  bool runs[8];
 #pragma unroll
   for (int gg = 0; gg < 8; ++gg) {
     const uint4* pr = reinterpret_cast<const uint4*>(rows + gg);
@@ -511,10 +585,28 @@ __device__ __forceinline__ void consume(const MomParams& P, const MomTile& tile,
     const uint32_t li = static_cast<uint32_t>(P.L - 1);
     const uint32_t word = li < 2 ? w0.x : li < 4 ? w0.y : li < 6 ? w0.z : w0.w;
     il[gg] = static_cast<int>((li & 1) ? (word >> 16) : (word & 0xffffu));
-    runs[gg] = ((w0.w >> 16) & 1u) != 0;  // idx[7] bit 0: runs among (j_1..j_L)
     tb[gg] = static_cast<uint64_t>(w1.x) | (static_cast<uint64_t>(w1.y) << 32);
     vp[gg] = w2.x;
     po[gg] = w2.y;
+  }
+  auto offset = [&](int gg, int c, int e, bool& ok) -> size_t {
+    const int col = colbase + 8 * c + 2 * q + e;
+    const int jd = col / b;
+    const int J = il[gg] / b;
+    ok = vp[gg] != 0 && col < n && col >= il[gg];
+    return tb[gg] + static_cast<uint64_t>(vp[gg]) * b * (jd - J) + static_cast<uint64_t>(po[gg]) * ext_of(jd, n, b) +
+           (col - jd * b);
+  };
+  if (update) {
+    // the old values are read after the stash round trip: start them toward L2 now
+#pragma unroll
+    for (int gg = 0; gg < 8; ++gg)
+#pragma unroll
+      for (int c = 0; c < NC - (ONES ? 1 : 0); ++c) {
+        bool ok;
+        const size_t o = offset(gg, c, 0, ok);
+        if (ok) asm volatile("prefetch.global.L2 [%0];" ::"l"(P.top + o));
+      }
   }
   if (update) {
 #pragma unroll
@@ -534,59 +626,85 @@ __device__ __forceinline__ void consume(const MomParams& P, const MomTile& tile,
 #pragma unroll
         for (int e = 0; e < 2; ++e) acc[gg][c][e] = __dmul_rn(acc[gg][c][e], P.inv);
   }
+#if CSB_EXP & 64
+  const long long e1 = clock64();
+#endif
   double* __restrict__ top = P.top;
-  double* __restrict__ dtop = P.dtop;
   const double cc = P.c;
   // batches of GB slots: offsets are recomputed at the stores rather than
   // kept live next to the loaded old values
-  constexpr int GB = NC >= 3 ? 2 : 4;
-  auto offset = [&](int gg, int c, int e, bool& ok, bool& diag) -> size_t {
-    const int col = colbase + 8 * c + 2 * q + e;
-    const int jd = col / b;
-    const int J = il[gg] / b;
-    ok = vp[gg] != 0 && col < n && col >= il[gg];
-    diag = runs[gg] || jd == J;
-    return tb[gg] + static_cast<uint64_t>(vp[gg]) * b * (jd - J) + static_cast<uint64_t>(po[gg]) * ext_of(jd, n, b) +
-           (col - jd * b);
-  };
+  constexpr int GB = NC >= 2 ? 2 : 4;
+  constexpr int NCD = ONES ? NC - 1 : NC;  // data-column tiles
+  if (ONES && q == 0) {
+    // row sums: lane (r, 0) holds slots (r, 0..7) in column 0 of the tile
+    double* __restrict__ low = P.low;
+#pragma unroll
+    for (int gg = 0; gg < 8; ++gg) {
+      if (vp[gg] == 0) continue;
+      const uint64_t lo = rows[gg].low_off;
+      const double v = acc[gg][NC - 1][0];
+      if (update) {
+        low[lo] = __fma_rn(cc, v, low[lo]);
+      } else {
+        low[lo] = v;
+      }
+    }
+  }
 #pragma unroll
   for (int g0 = 0; g0 < 8; g0 += GB) {
-    double old[GB][NC][2];
+    double old[GB][NCD > 0 ? NCD : 1][2];
     if (update) {
 #pragma unroll
       for (int h = 0; h < GB; ++h)
 #pragma unroll
-        for (int c = 0; c < NC; ++c)
+        for (int c = 0; c < NCD; ++c)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            bool ok, diag;
-            const size_t o = offset(g0 + h, c, e, ok, diag);
+            bool ok;
+            const size_t o = offset(g0 + h, c, e, ok);
             old[h][c][e] = ok ? top[o] : 0.0;
           }
     }
 #pragma unroll
     for (int h = 0; h < GB; ++h)
 #pragma unroll
-      for (int c = 0; c < NC; ++c)
+      for (int c = 0; c < NCD; ++c)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          bool ok, diag;
-          const size_t o = offset(g0 + h, c, e, ok, diag);
+          bool ok;
+          const size_t o = offset(g0 + h, c, e, ok);
           if (!ok) continue;
           const double v = acc[g0 + h][c][e];
           if (update) {
             top[o] = __fma_rn(cc, v, old[h][c][e]);
-            if (diag) dtop[o] = v;
           } else {
             top[o] = v;
           }
         }
   }
+#if CSB_EXP & 64
+  if (lane == 0 && P.npass == 2 && (blockIdx.x % 7) == 0)
+    printf("E %u %d %d %lld %lld\n", blockIdx.x, warp, NC, e1 - e0, clock64() - e1);
+#endif
+}
+
+// Column tiles [ct0, ct1) of DMMA warp w in a CTA with R row-set slots and
+// nct column tiles.  Warp w runs on SM sub-partition w % 4 and serves row
+// set w % R; a row set's tiles are split evenly over its 4/R sub-partitions
+// first, then over the two warps of each, so every sub-partition's DMMA pipe
+// gets the same share (ceil(nct R / 4) tiles at most).
+__device__ __forceinline__ void warp_tiles(int w, int R, int nct, int& ct0, int& ct1) {
+  const int ns = 4 / R;             // sub-partitions per row set
+  const int si = (w & 3) / R;       // this warp's among them
+  const int s0 = nct * si / ns, s1 = nct * (si + 1) / ns;
+  const int h = w >> 2;             // first or second warp of the sub-partition
+  ct0 = s0 + (s1 - s0) * h / 2;
+  ct1 = s0 + (s1 - s0) * (h + 1) / 2;
 }
 
 // N: compile-time row length (0: runtime P.n) -- with it every shared-memory
 // address of the inner loops is a register plus an immediate
-template <int N, int HS>
+template <int N, int HS, int B>
 __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomParams P) {
   constexpr int KC = Geo<HS>::KC;
   extern __shared__ __align__(128) double smem[];
@@ -599,19 +717,29 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
   const MomTile tile = P.tiles[blockIdx.x];
   const int R = static_cast<int>(tile.pad0);    // row-set slots of this CTA: 1, 2, 4
   const int nrs = static_cast<int>(tile.nrows); // live row sets (<= R)
-  const int C = CWARPS / R;                     // column ranges per row set
-  const int nct = static_cast<int>(tile.ncols);
-  const int cparts = nct < C ? nct : C;          // non-empty column ranges
+  const int nct0 = static_cast<int>(tile.ncols);
+  // Optionally (P.ones_r12 / P.ones4, off by default: measured slower on
+  // B200 -- the extra DMMAs slow the producer sharing the FP64 pipe more
+  // than its adds cost) the order-(d-1) row sums run on the DMMA pipe as
+  // an extra all-ones column tile where a sub-partition has a spare tile
+  // slot (R = 1: nct not a multiple of 4, R = 2: nct odd) or in the
+  // thinnest windows (R = 4, nct <= P.ones4).  Bit-identical either way.
+  const bool sums = P.low != nullptr && tile.low;
+  const bool ones = sums && ((P.ones_r12 && ((R == 1 && (nct0 & 3) != 0) || (R == 2 && (nct0 & 1) != 0))) ||
+                             (R == 4 && nct0 <= P.ones4));
+  const int nct = nct0 + (ones ? 1 : 0);
   Ring g;
   g.stages = static_cast<uint32_t>(P.stages);
   g.xs = smem;
   // reads past row n of the last stage (B fragments of the last column
   // tile) land in this padding and only feed outputs that are never stored
   g.arings = smem + static_cast<size_t>(g.stages) * KC * P.n + 64;
+  g.aslots = static_cast<uint32_t>(ASLOTS * PWARPS / R);
+  g.alog = 31 - __clz(g.aslots);
   g.xfull = bars;
   g.rel = rel;
   g.afull = bars + MAX_STAGES;
-  g.aempty = g.afull + PWARPS * ASLOTS;
+  g.aempty = g.afull + PWARPS * ASLOTS;  // aslots x (live row sets <= R) <= PWARPS x ASLOTS
   g.kc = KC;
   g.cpp = (P.K + KC - 1) / KC;
   g.chunks = g.cpp * P.npass;  // incoming pass, then outgoing pass
@@ -622,9 +750,12 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
 #else
   int active = nrs;
 #endif
+  int cparts = 0;  // DMMA warps with tiles per row set (the same for every row set)
   for (int w = 0; w < CWARPS; ++w) {
-    const int part = w / R;
-    active += (w % R) < nrs && nct * (part + 1) / C > nct * part / C;
+    int c0, c1;
+    warp_tiles(w, R, nct, c0, c1);
+    active += (w % R) < nrs && c1 > c0;
+    cparts += (w % R) == 0 && c1 > c0;
   }
   g.active = static_cast<uint32_t>(active);
   if (threadIdx.x == 0) {
@@ -643,23 +774,31 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
   if (warp >= CWARPS) {
     const int rs = warp - CWARPS;
     if (rs >= nrs || (CSB_EXP & 16)) return;
+    const bool psums = sums && !ones;
+#define CSB_PRODUCE(LM1)                                       \
+  if (psums) produce<LM1, N, HS, true>(P, tile, g, rs);        \
+  else produce<LM1, N, HS, false>(P, tile, g, rs);
     switch (P.L) {
-      case 2: produce<1, N, HS>(P, tile, g, rs); break;
-      case 3: produce<2, N, HS>(P, tile, g, rs); break;
-      case 4: produce<3, N, HS>(P, tile, g, rs); break;
-      case 5: produce<4, N, HS>(P, tile, g, rs); break;
+      case 2: CSB_PRODUCE(1) break;
+      case 3: CSB_PRODUCE(2) break;
+      case 4: CSB_PRODUCE(3) break;
+      case 5: CSB_PRODUCE(4) break;
       default: break;
     }
+#undef CSB_PRODUCE
     return;
   }
   const int rs = warp % R;
   if (rs >= nrs) return;
-  const int part = warp / R;
-  const int ct0 = nct * part / C, ct1 = nct * (part + 1) / C;
+  int ct0, ct1;
+  warp_tiles(warp, R, nct, ct0, ct1);
   static_assert(MAXNC == 2, "column tiles per DMMA warp");
-  switch (ct1 - ct0) {
-    case 1: consume<1, N, HS>(P, tile, g, rs, ct0, warp); break;
-    case 2: consume<2, N, HS>(P, tile, g, rs, ct0, warp); break;
+  const bool wones = ones && ct1 == nct;  // this warp's last tile is the row-sum tile
+  switch ((ct1 - ct0) * 2 + (wones ? 1 : 0)) {
+    case 2: consume<1, N, HS, B, false>(P, tile, g, rs, ct0, warp); break;
+    case 3: consume<1, N, HS, B, true>(P, tile, g, rs, ct0, warp); break;
+    case 4: consume<2, N, HS, B, false>(P, tile, g, rs, ct0, warp); break;
+    case 5: consume<2, N, HS, B, true>(P, tile, g, rs, ct0, warp); break;
     default: break;
   }
 #if CSB_EXP & 64  // timing experiment: per-CTA timeline of consumer warps
@@ -669,29 +808,52 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
     uint32_t smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     if ((threadIdx.x & 31) == 0 && P.npass == 2)
-      printf("T %u %u %d %d %d %d %llu %llu\n", blockIdx.x, smid, warp, R, nrs, ct1 - ct0,
-             (unsigned long long)t_start, (unsigned long long)t_end);
+      printf("T %u %u %d %d %d %d %llu %llu %llu %llu\n", blockIdx.x, smid, warp, R, nrs, ct1 - ct0,
+             (unsigned long long)t_start, (unsigned long long)t_end, (unsigned long long)exp_t[0][warp],
+             (unsigned long long)exp_t[1][warp]);
+    if ((threadIdx.x & 31) == 0 && P.npass == 2 && ct1 > ct0)
+      printf("W %u %d %d %lld %lld\n", blockIdx.x, warp, ct1 - ct0, (long long)exp_w[warp][0], (long long)exp_w[warp][1]);
   }
 #endif
 }
 
 // Symmetric copies of the canonical entries written above, one CTA per
 // stored block with equal neighbouring coordinates (symten.cpp:195-220):
-// entry o of block j is a copy of the entry with o sorted within each run
-// of equal j; an update applies the canonical delta to the copy's own old
-// value (moments.cpp:294-299 RMWs every stored entry), an assignment copies.
+// entry o of block j holds the value of the entry with o sorted within each
+// run of equal j.  The reference RMWs every stored copy with the same
+// fma(c, a - b, old) as its canonical entry (moments.cpp:294-299); the
+// copies enter every step bit-identical to the canonical entry (prime
+// scatters one value into all of them), so after the update they equal the
+// canonical entry's new value, and a copy is exactly that: m[dst] = m[src].
+// Full blocks (every extent b) stream a host-built (dst, src) list of their
+// run pattern; edge blocks sort each position's offsets in place.
 template <int S>
-__global__ void __launch_bounds__(256) mirror_kernel(double* __restrict__ m, const double* __restrict__ delta,
-                                                     LayoutDev lay, const uint32_t* __restrict__ blocks, int n,
-                                                     int b, bool update, double c) {
+__global__ void __launch_bounds__(256) mirror_kernel(double* __restrict__ m, LayoutDev lay,
+                                                     const uint32_t* __restrict__ blocks, int n, int b,
+                                                     const uint2* __restrict__ lists,
+                                                     const uint32_t* __restrict__ list_off) {
   const uint32_t blk = blocks[blockIdx.x];
   int j[S], e[S];
+  bool full = true;
 #pragma unroll
   for (int k = 0; k < S; ++k) {
     j[k] = lay.index[static_cast<size_t>(blk) * S + k];
     e[k] = ext_of(j[k], n, b);
+    full &= e[k] == b;
   }
   const uint64_t base = lay.offset[blk];
+  double* __restrict__ mb = m + base;
+  if (full && lists) {
+    uint32_t pat = 0;
+#pragma unroll
+    for (int k = 1; k < S; ++k) pat |= static_cast<uint32_t>(j[k] == j[k - 1]) << (k - 1);
+    const uint32_t i1 = list_off[pat + 1];
+    for (uint32_t i = list_off[pat] + threadIdx.x; i < i1; i += blockDim.x) {
+      const uint2 pr = __ldg(lists + i);
+      mb[pr.x] = mb[pr.y];
+    }
+    return;
+  }
   const uint64_t vol = lay.offset[blk + 1] - base;
   for (uint64_t pos = threadIdx.x; pos < vol; pos += blockDim.x) {
     int o[S];
@@ -701,12 +863,12 @@ __global__ void __launch_bounds__(256) mirror_kernel(double* __restrict__ m, con
       o[k] = static_cast<int>(rem % e[k]);
       rem /= e[k];
     }
-    // sort within runs (bubble passes over a tiny array, fully unrolled)
     bool canonical = true;
 #pragma unroll
     for (int k = 1; k < S; ++k)
       if (j[k] == j[k - 1] && o[k] < o[k - 1]) canonical = false;
     if (canonical) continue;
+    // sort within runs (bubble passes over a tiny array, fully unrolled)
 #pragma unroll
     for (int pass = 0; pass < S - 1; ++pass)
 #pragma unroll
@@ -719,8 +881,7 @@ __global__ void __launch_bounds__(256) mirror_kernel(double* __restrict__ m, con
     uint64_t src = 0;
 #pragma unroll
     for (int k = 0; k < S; ++k) src = src * e[k] + o[k];
-    double* p = m + base + pos;
-    *p = update ? __fma_rn(c, delta[base + src], *p) : m[base + src];
+    mb[pos] = mb[src];
   }
 }
 
@@ -762,12 +923,12 @@ bool dmma_supported(const MomParams& p) {
   return stages_for(p.n, 4) >= 2;
 }
 
-void launch_mirror(int S, double* m, const double* delta, const LayoutDev& lay, const uint32_t* blocks,
-                   uint32_t nblocks, int n, int b, bool update, double c, cudaStream_t st) {
+void launch_mirror(int S, double* m, const LayoutDev& lay, const uint32_t* blocks, uint32_t nblocks, int n, int b,
+                   const uint2* lists, const uint32_t* list_off, cudaStream_t st) {
   if (!nblocks) return;
   switch (S) {
 #define CSB_MIRROR(SS) \
-  case SS: mirror_kernel<SS><<<nblocks, 256, 0, st>>>(m, delta, lay, blocks, n, b, update, c); break;
+  case SS: mirror_kernel<SS><<<nblocks, 256, 0, st>>>(m, lay, blocks, n, b, lists, list_off); break;
     CSB_MIRROR(2) CSB_MIRROR(3) CSB_MIRROR(4) CSB_MIRROR(5) CSB_MIRROR(6) CSB_MIRROR(7) CSB_MIRROR(8)
 #undef CSB_MIRROR
     default: fail(CSB_EINVAL, "mirror: order out of range");
@@ -781,18 +942,29 @@ void launch_moment_top_dmma(const MomParams& p_in, int ntiles, cudaStream_t st) 
   MomParams p = p_in;
   const int hs = chunk_steps(p.n);
   p.stages = stages_for(p.n, hs);
+  static const int ones4 = [] {  // CSB_ONES4=0..3: row-sum tile in R = 4 windows of <= k column tiles
+    const char* e = std::getenv("CSB_ONES4");
+    return e ? std::max(0, std::min(3, std::atoi(e))) : 0;
+  }();
+  static const bool ones_r12 = [] {  // CSB_ONES=1: row-sum tile in spare R = 1 / 2 slots
+    const char* e = std::getenv("CSB_ONES");
+    return e && e[0] == '1';
+  }();
+  p.ones4 = ones4;
+  p.ones_r12 = ones_r12;
   if (p.stages < 2) fail(CSB_EINVAL, "moment_top_dmma: rows too wide for the staging ring");
   const size_t smem = smem_bytes(p.n, p.stages, hs);
   using K = void (*)(MomParams);
   K kern = nullptr;
-  if (p.n == 96 && hs == 6) kern = moment_top_dmma_kernel<96, 6>;
-  else if (p.n == 96 && hs == 8) kern = moment_top_dmma_kernel<96, 8>;
-  else if (p.n == 48 && hs == 8) kern = moment_top_dmma_kernel<48, 8>;
-  else if (p.n == 24 && hs == 8) kern = moment_top_dmma_kernel<24, 8>;
-  else if (p.n == 256 && hs == 4) kern = moment_top_dmma_kernel<256, 4>;
-  else if (hs == 8) kern = moment_top_dmma_kernel<0, 8>;
-  else if (hs == 6) kern = moment_top_dmma_kernel<0, 6>;
-  else kern = moment_top_dmma_kernel<0, 4>;
+  // specialised (row length, chunk, block size) of the BASELINE configs; generic otherwise
+  if (p.n == 96 && hs == 6 && p.b == 8) kern = moment_top_dmma_kernel<96, 6, 8>;
+  else if (p.n == 96 && hs == 8 && p.b == 8) kern = moment_top_dmma_kernel<96, 8, 8>;
+  else if (p.n == 48 && hs == 8 && p.b == 4) kern = moment_top_dmma_kernel<48, 8, 4>;
+  else if (p.n == 24 && hs == 8 && p.b == 3) kern = moment_top_dmma_kernel<24, 8, 3>;
+  else if (p.n == 256 && hs == 4 && p.b == 16) kern = moment_top_dmma_kernel<256, 4, 16>;
+  else if (hs == 8) kern = moment_top_dmma_kernel<0, 8, 0>;
+  else if (hs == 6) kern = moment_top_dmma_kernel<0, 6, 0>;
+  else kern = moment_top_dmma_kernel<0, 4, 0>;
   CSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   kern<<<ntiles, THREADS, smem, st>>>(p);
   CSB_CUDA(cudaGetLastError());

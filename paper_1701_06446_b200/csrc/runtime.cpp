@@ -66,6 +66,7 @@ struct Device {
   std::map<std::tuple<int, int, int>, std::shared_ptr<DevBuf<LowerThread>>> lower2;
   std::map<std::tuple<int, int, int>, std::shared_ptr<DevBuf<uint64_t>>> subs;
   std::map<std::pair<int, int>, std::pair<std::shared_ptr<DevBuf<uint32_t>>, std::shared_ptr<DevBuf<uint32_t>>>> canon;
+  std::map<std::pair<int, int>, std::pair<std::shared_ptr<DevBuf<uint2>>, std::shared_ptr<DevBuf<uint32_t>>>> mirror;
   std::map<std::tuple<int, int, int, int>, std::shared_ptr<ShardPlan>> shards;
   void* comm = nullptr;  // NCCL communicator (csb_comm_init)
   int nranks = 1, rank = 0;
@@ -288,6 +289,51 @@ std::pair<const uint32_t*, const uint32_t*> get_canon(Device& dev, int S, int b)
   return {slot.first->ptr, slot.second->ptr};
 }
 
+// (dst, src) pairs of the symmetric copies of a full order-S block (all
+// extents b) per run pattern (bit k-1: j_k == j_{k-1}): dst a non-canonical
+// position, src its offsets sorted within runs (symten.cpp:195-220).  Not
+// built for large blocks (the mirror kernel then sorts in place).
+std::pair<const uint2*, const uint32_t*> get_mirror_lists(Device& dev, int S, int b) {
+  std::lock_guard<std::mutex> lk(dev.mu);
+  auto& slot = dev.mirror[{S, b}];
+  if (!slot.first) {
+    uint64_t vol = 1;
+    for (int k = 0; k < S; ++k) vol *= static_cast<uint64_t>(b);
+    const uint32_t npat = 1u << (S - 1);
+    if (vol * npat > (1ull << 20)) return {nullptr, nullptr};
+    std::vector<uint2> list;
+    std::vector<uint32_t> off;
+    int o[kMaxOrder];
+    for (uint32_t pat = 0; pat < npat; ++pat) {
+      off.push_back(static_cast<uint32_t>(list.size()));
+      for (uint64_t pos = 0; pos < vol; ++pos) {
+        uint64_t rem = pos;
+        for (int k = S - 1; k >= 0; --k) {
+          o[k] = static_cast<int>(rem % static_cast<uint64_t>(b));
+          rem /= static_cast<uint64_t>(b);
+        }
+        bool canonical = true;
+        for (int k = 1; k < S; ++k)
+          if ((pat >> (k - 1) & 1) && o[k] < o[k - 1]) canonical = false;
+        if (canonical) continue;
+        for (int pass = 0; pass < S - 1; ++pass)
+          for (int k = 1; k < S; ++k)
+            if ((pat >> (k - 1) & 1) && o[k] < o[k - 1]) std::swap(o[k], o[k - 1]);
+        uint64_t src = 0;
+        for (int k = 0; k < S; ++k) src = src * static_cast<uint64_t>(b) + static_cast<uint64_t>(o[k]);
+        list.push_back(make_uint2(static_cast<uint32_t>(pos), static_cast<uint32_t>(src)));
+      }
+    }
+    off.push_back(static_cast<uint32_t>(list.size()));
+    auto l = std::make_shared<DevBuf<uint2>>(std::max<size_t>(1, list.size()));
+    auto o2 = std::make_shared<DevBuf<uint32_t>>(off.size());
+    if (!list.empty()) h2d_sync(l->ptr, list.data(), list.size() * sizeof(uint2));
+    h2d_sync(o2->ptr, off.data(), o2->bytes());
+    slot = {l, o2};
+  }
+  return {slot.first->ptr, slot.second->ptr};
+}
+
 // Thread table of the staged low-order kernel for orders 1..ST: the
 // order-ST tuples in lexicographic order, cut into runs of <= W sharing
 // their (ST-1)-prefix pi; a prefix's first run also represents the tuples
@@ -414,12 +460,6 @@ struct Scratch {
     return buf.ptr;
   }
   DevBuf<double> zeros;
-  DevBuf<double> dtop, dlow;
-  DevBuf<double> dlower[4];
-  double* get_delta(DevBuf<double>& d, uint64_t count) {
-    if (d.count < count) d.alloc(count);
-    return d.ptr;
-  }
   const double* get_zeros(uint64_t count) {
     if (zeros.count < count) {
       zeros.alloc(count);
@@ -551,22 +591,23 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
     p.pairs = plan->d_pairs.ptr;
     const uint64_t ntiles = plan->tiles.size();
     if (npass == 2 || use_dmma) p.scratch = sc.get(ntiles * plan->scratch_per_tile);
-    ProfScope ps("moment_top", st);
     if (use_dmma) {
       p.zeros = sc.get_zeros(32ull * m->n);
-      if (npass == 2) {
-        p.dtop = sc.get_delta(sc.dtop, m->lay[S - 1]->host.stored);
-        if (p.low) p.dlow = sc.get_delta(sc.dlow, m->lay[S - 2]->host.stored);
+      {
+        ProfScope ps("moment_top", st);  // the DMMA kernel alone (bench roofline)
+        launch_moment_top_dmma(p, static_cast<int>(ntiles), st);
       }
-      launch_moment_top_dmma(p, static_cast<int>(ntiles), st);
+      ProfScope pm("mirror", st);
       const auto& LT = m->lay[S - 1];
       auto rt = sharded ? LT->diag_range(sh.lo(0), sh.hi(0)) : std::make_pair(0u, LT->ndiag);
-      launch_mirror(S, p.top, p.dtop, LT->view(), LT->diag.ptr + rt.first, rt.second, m->n, m->b, npass == 2, c, st);
+      auto ml = get_mirror_lists(*m->dev, S, m->b);
+      launch_mirror(S, p.top, LT->view(), LT->diag.ptr + rt.first, rt.second, m->n, m->b, ml.first, ml.second, st);
       if (p.low) {
         const auto& LL = m->lay[S - 2];
         auto rl = sharded ? LL->diag_range(sh.lo(1), sh.hi(1)) : std::make_pair(0u, LL->ndiag);
-        launch_mirror(S - 1, p.low, p.dlow, LL->view(), LL->diag.ptr + rl.first, rl.second, m->n, m->b, npass == 2,
-                      c, st);
+        auto ml1 = get_mirror_lists(*m->dev, S - 1, m->b);
+        launch_mirror(S - 1, p.low, LL->view(), LL->diag.ptr + rl.first, rl.second, m->n, m->b, ml1.first, ml1.second,
+                      st);
         if (sharded && sh.comm) {
           // collective C2: every rank needs all of M_{d-1} (its own blocks
           // were just updated, the rest arrive from their owners)
@@ -580,6 +621,7 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
         }
       }
     } else {
+      ProfScope ps("moment_top", st);
       launch_moment_pair(p, static_cast<int>(ntiles), true, st);
     }
   }

@@ -220,13 +220,16 @@ int main() {
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   double* out;
   CK(cudaMalloc(&out, 64));
-  for (int w : {1}) {
-    run<1, 2>(w, out, sms);
-    run<2, 2>(w, out, sms);
-    run<4, 2>(w, out, sms);
+  for (int w : {1, 2}) {
     run<1, 0>(w, out, sms);
     run<2, 0>(w, out, sms);
     run<4, 0>(w, out, sms);
+    run<1, 1>(w, out, sms);
+    run<2, 1>(w, out, sms);
+    run<2, 2>(w, out, sms);
+    run<2, 0, 3>(w, out, sms);
+    run<2, 0, 4>(w, out, sms);
+    run<2, 0, 1>(w, out, sms);
   }
   return 0;
 }
