@@ -18,9 +18,11 @@
 // exactly as the reference's upper levels (moments.cpp:55-57).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "kernels.cuh"
+#include "ptx.cuh"
 #include "partitions_gen.cuh"
 
 namespace csb {
@@ -573,6 +575,143 @@ __global__ void __launch_bounds__(LOW2_THREADS, 8) moment_lower_side_kernel(cons
       default: break;
     }
   }
+}
+
+// Orders <= d-2 when they are few (cfg1: 4,656 + 96 elements): one thread
+// per order-ST element (and the lower-order tuples it represents), the
+// pass's rows streamed through a shared-memory ring by TMA bulk copies
+// (one producer warp, full/empty mbarriers), so each thread's row-ordered
+// chain of plain adds (moments.cpp:44) runs at the DADD latency instead of
+// waiting on L2 for every few rows.
+constexpr int LOWT_THREADS = 256;
+constexpr int LOWT_MAXST = 8;
+
+template <int ST>
+__global__ void __launch_bounds__(LOWT_THREADS + 32) moment_lower_tma_kernel(const Lower2Params P, int stages, int kr) {
+  extern __shared__ __align__(128) double xs[];  // stages x kr x n
+  __shared__ __align__(8) uint64_t full[LOWT_MAXST], empty[LOWT_MAXST];
+  constexpr int NP = ST - 1;
+  constexpr int NR = NP > 0 ? NP : 1;
+  const int n = P.n;
+  const uint32_t K = P.K;
+  const uint32_t cpp = (K + kr - 1) / kr;
+  const uint32_t chunks = cpp * P.npass;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      ptx::mbar_init(full + s, 1);
+      ptx::mbar_init(empty + s, LOWT_THREADS / 32);
+    }
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x >= LOWT_THREADS) {  // producer warp: one lane issues the copies
+    if (threadIdx.x != LOWT_THREADS) return;
+    const uint32_t rb = static_cast<uint32_t>(n) * 8u;
+    for (uint32_t c = 0; c < chunks; ++c) {
+      const uint32_t st = c % stages;
+      if (c >= static_cast<uint32_t>(stages)) ptx::mbar_wait(empty + st, ((c / stages) - 1) & 1u);
+      const uint32_t pass = c >= cpp ? 1u : 0u;
+      const RowSource src = P.src[pass];
+      const uint32_t a0 = (c - pass * cpp) * kr;
+      const uint32_t kc = min(static_cast<uint32_t>(kr), K - a0);
+      double* dst = xs + static_cast<size_t>(st) * kr * n;
+      ptx::mbar_expect_tx(full + st, kc * rb);
+      auto rowp = [&](uint32_t k) {
+        return k < src.len0 ? src.seg0 + static_cast<size_t>(k) * n : src.seg1 + static_cast<size_t>(k - src.len0) * n;
+      };
+      if (a0 + kc <= src.len0 || a0 >= src.len0) {
+        ptx::bulk_g2s(dst, rowp(a0), kc * rb, full + st);
+      } else {  // across the ring's wrap
+        const uint32_t k1 = src.len0 - a0;
+        ptx::bulk_g2s(dst, rowp(a0), k1 * rb, full + st);
+        ptx::bulk_g2s(dst + static_cast<size_t>(k1) * n, src.seg1, (kc - k1) * rb, full + st);
+      }
+    }
+    return;
+  }
+  const uint32_t tid = blockIdx.x * LOWT_THREADS + threadIdx.x;
+  const bool live = tid < P.nthreads;
+  const LowerThread T = P.threads[live ? tid : 0];
+  int pidx[NR];
+#pragma unroll
+  for (int k = 0; k < NR; ++k) pidx[k] = NP > 0 ? T.pidx[k] : 0;
+  const int col = T.t0;
+  bool rep[NR];
+#pragma unroll
+  for (int k = 0; k < NR; ++k) rep[k] = NP > 0 && T.rep[k] != 0xffffffffu;
+  double res[2][1 + NR];
+  double acc[1 + NR];
+#pragma unroll
+  for (int w = 0; w < 1 + NR; ++w) acc[w] = 0.0;
+  for (uint32_t c = 0; c < chunks; ++c) {
+    const uint32_t st = c % stages;
+    ptx::mbar_wait(full + st, (c / stages) & 1u);
+    const uint32_t pass = c >= cpp ? 1u : 0u;
+    const uint32_t kc = min(static_cast<uint32_t>(kr), K - (c - pass * cpp) * kr);
+    const double* xb = xs + static_cast<size_t>(st) * kr * n;
+#pragma unroll 8
+    for (uint32_t r = 0; r < kc; ++r) {
+      const double* x = xb + r * n;
+      double pv = 1.0;
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        pv = k == 0 ? x[pidx[0]] : __dmul_rn(pv, x[pidx[k]]);
+        if (rep[k]) acc[1 + k] = __dadd_rn(acc[1 + k], pv);
+      }
+      acc[0] = __dadd_rn(acc[0], NP > 0 ? __dmul_rn(pv, x[col]) : x[col]);
+    }
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) ptx::mbar_arrive(empty + st);
+    if (c + 1 == cpp || c + 1 == chunks) {  // end of a pass
+#pragma unroll
+      for (int w = 0; w < 1 + NR; ++w) {
+        res[pass][w] = __dmul_rn(acc[w], P.inv);
+        acc[w] = 0.0;
+      }
+    }
+  }
+  if (!live) return;
+  const bool update = P.npass == 2;
+  {
+    const double v = update ? __dsub_rn(res[0][0], res[1][0]) : res[0][0];
+    write_copies<ST>(P.m[ST - 1], P.elems[ST - 1][T.e0], n, P.b, update, P.c, v);
+  }
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    if (!rep[k]) continue;
+    const double v = update ? __dsub_rn(res[0][1 + k], res[1][1 + k]) : res[0][1 + k];
+    switch (k) {
+      case 0: write_copies<1>(P.m[0], P.elems[0][T.rep[0]], n, P.b, update, P.c, v); break;
+      case 1: write_copies<(ST > 2 ? 2 : 1)>(P.m[1], P.elems[1][T.rep[1]], n, P.b, update, P.c, v); break;
+      case 2: write_copies<(ST > 3 ? 3 : 1)>(P.m[2], P.elems[2][T.rep[2]], n, P.b, update, P.c, v); break;
+      default: break;
+    }
+  }
+}
+
+bool lower_tma_supported(const Lower2Params& p) { return p.n % 2 == 0 && p.n <= 4096; }
+
+void launch_moment_lower_tma(int ST, const Lower2Params& p, cudaStream_t st) {
+  if (!p.nthreads) return;
+  const unsigned g = (p.nthreads + LOWT_THREADS - 1) / LOWT_THREADS;
+  const int kr = 32;
+  const size_t stage_bytes = static_cast<size_t>(kr) * p.n * sizeof(double);
+  int stages = static_cast<int>(std::min<size_t>(LOWT_MAXST, (200u << 10) / stage_bytes));
+  if (stages < 2) fail(CSB_EINVAL, "moment_lower_tma: rows too wide");
+  const size_t sm = stages * stage_bytes;
+  switch (ST) {
+#define CSB_LOWT(SS)                                                                                          \
+  case SS:                                                                                                    \
+    CSB_CUDA(cudaFuncSetAttribute(moment_lower_tma_kernel<SS>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                  static_cast<int>(sm)));                                                     \
+    moment_lower_tma_kernel<SS><<<g, LOWT_THREADS + 32, sm, st>>>(p, stages, kr);                             \
+    break;
+    CSB_LOWT(1) CSB_LOWT(2) CSB_LOWT(3) CSB_LOWT(4)
+#undef CSB_LOWT
+    default: fail(CSB_EINVAL, "moment_lower_tma: order out of range");
+  }
+  CSB_CUDA(cudaGetLastError());
+  count_launch();
 }
 
 void launch_moment_lower_side(int ST, const Lower2Params& p, cudaStream_t st) {

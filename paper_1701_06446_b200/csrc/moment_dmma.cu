@@ -847,10 +847,22 @@ __global__ void __launch_bounds__(256) mirror_kernel(double* __restrict__ m, Lay
     uint32_t pat = 0;
 #pragma unroll
     for (int k = 1; k < S; ++k) pat |= static_cast<uint32_t>(j[k] == j[k - 1]) << (k - 1);
-    const uint32_t i1 = list_off[pat + 1];
-    for (uint32_t i = list_off[pat] + threadIdx.x; i < i1; i += blockDim.x) {
-      const uint2 pr = __ldg(lists + i);
-      mb[pr.x] = mb[pr.y];
+    const uint32_t i0 = list_off[pat], i1 = list_off[pat + 1];
+    // four independent copies in flight per thread (latency-bound otherwise)
+    constexpr uint32_t U = 4;
+    for (uint32_t i = i0 + threadIdx.x; i < i1; i += U * blockDim.x) {
+      uint2 pr[U];
+      double v[U];
+#pragma unroll
+      for (uint32_t u = 0; u < U; ++u) {
+        const uint32_t k = i + u * blockDim.x;
+        pr[u] = k < i1 ? __ldg(lists + k) : make_uint2(0u, 0u);
+      }
+#pragma unroll
+      for (uint32_t u = 0; u < U; ++u) v[u] = mb[pr[u].y];
+#pragma unroll
+      for (uint32_t u = 0; u < U; ++u)
+        if (i + u * blockDim.x < i1) mb[pr[u].x] = v[u];
     }
     return;
   }

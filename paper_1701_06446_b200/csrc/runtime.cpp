@@ -11,6 +11,7 @@
 #include <map>
 #include <unordered_map>
 #include <memory>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <tuple>
@@ -482,6 +483,16 @@ const bool g_low_side = [] {
   const char* e = std::getenv("CSB_LOW_INLINE");
   return !(e && e[0] == '1');
 }();
+// CSB_LOW_KERNEL=side: the register-only low-order kernel instead of the
+// TMA-staged one; CSB_LOW_DEFER=0: launch it before the top kernel (A/B)
+const bool g_low_tma = [] {
+  const char* e = std::getenv("CSB_LOW_KERNEL");
+  return !(e && std::strcmp(e, "side") == 0);
+}();
+const bool g_low_defer = [] {
+  const char* e = std::getenv("CSB_LOW_DEFER");
+  return !(e && e[0] == '0');
+}();
 const bool g_use_dmma = [] {
   const char* e = std::getenv("CSB_NO_DMMA");
   return !(e && e[0] == '1');
@@ -535,8 +546,15 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
   // latency bound and hides under the top pair); else staged, in line
   const bool side = lower && d - 2 <= 4 && use_dmma && g_low_side && multiset_count(m->n, d - 2) <= 60000;
   bool joined = true;
+  // The side-stream launch is deferred until the top kernel is queued: the
+  // block scheduler hands SMs to the top kernel's CTAs first and the few
+  // low-order CTAs (TMA-staged rows) run as SMs free up in its last wave.
+  // Launched first, the old register-only kernel held ~1/4 of the SMs for
+  // ~180 us and cost cfg1's top kernel 31 us (measured; CSB_LOW_DEFER=0).
+  std::function<void()> side_launch;
   if (lower && d - 2 <= 4) {
-    ProfScope ps("moment_low", side ? dev.side : st);
+    std::unique_ptr<ProfScope> ps;
+    if (!side) ps = std::make_unique<ProfScope>("moment_low", st);
     const int ST = d - 2;
     const int W = side ? 1 : multiset_count(m->n, ST) > 60000 ? 4 : 1;
     auto th = get_lower2_threads(dev, ST, m->n, W);
@@ -556,11 +574,21 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
     lp.c = c;
     lp.inv = 1.0 / static_cast<double>(K);
     if (side) {
-      std::lock_guard<std::mutex> lk(dev.mu);
-      CSB_CUDA(cudaEventRecord(dev.fork, st));
-      CSB_CUDA(cudaStreamWaitEvent(dev.side, dev.fork, 0));
-      launch_moment_lower_side(ST, lp, dev.side);
-      CSB_CUDA(cudaEventRecord(dev.join, dev.side));
+      CSB_CUDA(cudaEventRecord(dev.fork, st));  // the low orders depend only on work queued so far
+      side_launch = [&dev, ST, lp]() {
+        std::lock_guard<std::mutex> lk(dev.mu);
+        CSB_CUDA(cudaStreamWaitEvent(dev.side, dev.fork, 0));
+        ProfScope pl("moment_low", dev.side);
+        if (g_low_tma && lower_tma_supported(lp))
+          launch_moment_lower_tma(ST, lp, dev.side);
+        else
+          launch_moment_lower_side(ST, lp, dev.side);
+        CSB_CUDA(cudaEventRecord(dev.join, dev.side));
+      };
+      if (!g_low_defer) {
+        side_launch();
+        side_launch = nullptr;
+      }
       joined = false;
     } else {
       launch_moment_lower2(ST, W, lp, st);
@@ -597,6 +625,7 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
         ProfScope ps("moment_top", st);  // the DMMA kernel alone (bench roofline)
         launch_moment_top_dmma(p, static_cast<int>(ntiles), st);
       }
+      if (side_launch) side_launch();
       ProfScope pm("mirror", st);
       const auto& LT = m->lay[S - 1];
       auto rt = sharded ? LT->diag_range(sh.lo(0), sh.hi(0)) : std::make_pair(0u, LT->ndiag);
