@@ -81,8 +81,16 @@ __device__ __forceinline__ uint32_t source_of(const int (&j)[S], int (&o)[S], co
   return src;
 }
 
-template <int S, bool STAGED>
-__global__ void __launch_bounds__(256) moms2cums_v2(const M2CParams P) {
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+
+// B: compile-time block size (0: runtime) -- full blocks then decode
+// positions and address factors with constant divisions and powers
+template <int S, bool STAGED, int B>
+__global__ void __launch_bounds__(256, 2) moms2cums_v2(const M2CParams P) {
   constexpr int NM = (1 << S) - 1;  // masks 1..NM-1: proper non-empty subsets
   extern __shared__ __align__(16) double sfac[];  // staged sub-blocks (STAGED)
   __shared__ uint64_t sbase[NM];                  // global (or smem) base per subset
@@ -90,7 +98,7 @@ __global__ void __launch_bounds__(256) moms2cums_v2(const M2CParams P) {
   __shared__ double red[8];
   const uint64_t blk = P.blk0 + blockIdx.x;
   const LayoutDev& LS = P.lay[S - 1];
-  const int n = P.n, b = P.b;
+  const int n = P.n, b = B ? B : P.b;
   int j[S], e[S];
 #pragma unroll
   for (int k = 0; k < S; ++k) {
@@ -127,8 +135,19 @@ __global__ void __launch_bounds__(256) moms2cums_v2(const M2CParams P) {
     }
   }
   __syncthreads();
+  bool full = true;
+#pragma unroll
+  for (int k = 0; k < S; ++k) full &= e[k] == b;
+  // a full block is assembled in shared memory: M staged, C computed in
+  // place (each canonical position by the thread that reads it), copies
+  // filled from the pattern list, then written out coalesced
+  const bool inblk = STAGED && full && P.canon && P.mlist;
+  double* cblk = sfac + P.cblk;
   if (STAGED) {
-    // copy every needed sub-block into shared memory (coalesced per subset)
+    if (inblk)
+      for (uint32_t t = threadIdx.x; t < vol; t += blockDim.x) cp_async8(cblk + t, P.m + boff + t);
+    // copy every needed sub-block into shared memory (coalesced per subset;
+    // asynchronous, so all subsets' loads are in flight at once)
     for (int m = 1; m < NM; ++m) {
       uint32_t svol = 1;
 #pragma unroll
@@ -136,8 +155,12 @@ __global__ void __launch_bounds__(256) moms2cums_v2(const M2CParams P) {
         if (m >> k & 1) svol *= static_cast<uint32_t>(e[k]);
       const double* src = P.lower[popcount_c(m) - 1] + subs[m - 1];
       double* dst = sfac + sbase[m];
-      for (uint32_t t = threadIdx.x; t < svol; t += blockDim.x) dst[t] = src[t];
+      if (inblk)
+        for (uint32_t t = threadIdx.x; t < svol; t += blockDim.x) cp_async8(dst + t, src + t);
+      else
+        for (uint32_t t = threadIdx.x; t < svol; t += blockDim.x) dst[t] = src[t];
     }
+    if (inblk) asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
     __syncthreads();
   }
 
@@ -146,9 +169,6 @@ __global__ void __launch_bounds__(256) moms2cums_v2(const M2CParams P) {
   // on the non-canonical copies of diagonal blocks -- and address a factor
   // in its staged sub-block with compile-time powers of b; edge blocks test
   // every position.
-  bool full = true;
-#pragma unroll
-  for (int k = 0; k < S; ++k) full &= e[k] == b;
   if (STAGED && full && P.canon) {
     uint32_t pat = 0;
 #pragma unroll
@@ -162,7 +182,16 @@ __global__ void __launch_bounds__(256) moms2cums_v2(const M2CParams P) {
     for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
       const uint32_t pos = __ldg(list + i);
       int o[S];
-      decode<S>(pos, e, o);
+      if (B) {
+        uint32_t r = pos;
+#pragma unroll
+        for (int k = S - 1; k >= 0; --k) {
+          o[k] = static_cast<int>(r % static_cast<uint32_t>(B ? B : 1));
+          r /= static_cast<uint32_t>(B ? B : 1);
+        }
+      } else {
+        decode<S>(pos, e, o);
+      }
       double f[NM];
 #pragma unroll
       for (int m = 1; m < NM; ++m) {
@@ -174,7 +203,10 @@ __global__ void __launch_bounds__(256) moms2cums_v2(const M2CParams P) {
         f[m] = sfac[sbase[m] + a];
       }
       const double corr = partition_correction<S>(f);
-      P.c[boff + pos] = __dsub_rn(P.m[boff + pos], corr);
+      if (inblk)
+        cblk[pos] = __dsub_rn(cblk[pos], corr);
+      else
+        P.c[boff + pos] = __dsub_rn(P.m[boff + pos], corr);
     }
   } else {
     for (uint32_t pos = threadIdx.x; pos < vol; pos += blockDim.x) {
@@ -201,7 +233,23 @@ __global__ void __launch_bounds__(256) moms2cums_v2(const M2CParams P) {
 
   // phase 2: copies + the block's sum of squares (fixed order)
   double part = 0.0;
-  for (uint32_t pos = threadIdx.x; pos < vol; pos += blockDim.x) {
+  if (inblk) {
+    uint32_t pat = 0;
+#pragma unroll
+    for (int k = 1; k < S; ++k) pat |= static_cast<uint32_t>(j[k] == j[k - 1]) << (k - 1);
+    const uint32_t i1 = P.mlist_off[pat + 1];
+    for (uint32_t i = P.mlist_off[pat] + threadIdx.x; i < i1; i += blockDim.x) {
+      const uint2 pr = __ldg(P.mlist + i);
+      cblk[pr.x] = cblk[pr.y];
+    }
+    __syncthreads();
+    for (uint32_t pos = threadIdx.x; pos < vol; pos += blockDim.x) {
+      const double v = cblk[pos];
+      P.c[boff + pos] = v;
+      part = __fma_rn(v, v, part);
+    }
+  }
+  for (uint32_t pos = threadIdx.x; !inblk && pos < vol; pos += blockDim.x) {
     int o[S];
     decode<S>(pos, e, o);
     double v;
@@ -350,12 +398,6 @@ __global__ void __launch_bounds__(128) moment_lower_kernel(const LowerParams P) 
 constexpr int LOW2_KC = 32;
 constexpr int LOW2_THREADS = 128;
 
-__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
-               "l"(src)
-               : "memory");
-}
-
 template <int ST, int W>
 __global__ void __launch_bounds__(LOW2_THREADS) moment_lower2_kernel(const Lower2Params P) {
   extern __shared__ double xs[];  // 2 x LOW2_KC x n
@@ -475,21 +517,44 @@ size_t moms2cums_stage_bytes(int S, int n, int b) {
 void launch_moms2cums_v2(int S, const M2CParams& p, uint64_t nblocks, cudaStream_t st) {
   if (nblocks == 0) return;
   const unsigned g = static_cast<unsigned>(nblocks);
-  const size_t sm = moms2cums_stage_bytes(S, p.n, p.b);
-  const bool staged = sm <= 160 * 1024;
+  const size_t sm0 = moms2cums_stage_bytes(S, p.n, p.b);
+  const bool staged = sm0 <= 160 * 1024;
+  // one full block of C_S beside the staged sub-blocks, when it fits
+  size_t vol = 1;
+  for (int k = 0; k < S; ++k) vol *= static_cast<size_t>(p.b < p.n ? p.b : p.n);
+  M2CParams q = p;
+  size_t sm = sm0;
+  if (staged && q.mlist && sm0 + vol * sizeof(double) <= 64 * 1024) {
+    q.cblk = static_cast<uint32_t>(sm0 / sizeof(double));
+    sm = sm0 + vol * sizeof(double);
+  } else {
+    q.mlist = nullptr;
+  }
+  const int bb = p.b < p.n ? p.b : p.n;
   switch (S) {
-#define CSB_M2C(SS)                                                                                   \
-  case SS:                                                                                            \
-    if (staged) {                                                                                     \
-      CSB_CUDA(cudaFuncSetAttribute(moms2cums_v2<SS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                    static_cast<int>(sm)));                                           \
-      moms2cums_v2<SS, true><<<g, 256, sm, st>>>(p);                                                  \
-    } else {                                                                                          \
-      moms2cums_v2<SS, false><<<g, 256, 0, st>>>(p);                                                  \
-    }                                                                                                 \
+#define CSB_M2C_B(SS, BB)                                                                                  \
+  CSB_CUDA(cudaFuncSetAttribute(moms2cums_v2<SS, true, BB>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                                static_cast<int>(sm)));                                                   \
+  moms2cums_v2<SS, true, BB><<<g, 256, sm, st>>>(q);
+#define CSB_M2C(SS)                                                                                         \
+  case SS:                                                                                                  \
+    if (staged) {                                                                                           \
+      if (bb == 4) {                                                                                        \
+        CSB_M2C_B(SS, 4)                                                                                    \
+      } else if (bb == 8) {                                                                                 \
+        CSB_M2C_B(SS, 8)                                                                                    \
+      } else if (bb == 16) {                                                                                \
+        CSB_M2C_B(SS, 16)                                                                                   \
+      } else {                                                                                              \
+        CSB_M2C_B(SS, 0)                                                                                    \
+      }                                                                                                     \
+    } else {                                                                                                \
+      moms2cums_v2<SS, false, 0><<<g, 256, 0, st>>>(q);                                                     \
+    }                                                                                                       \
     break;
     CSB_M2C(2) CSB_M2C(3) CSB_M2C(4) CSB_M2C(5) CSB_M2C(6)
 #undef CSB_M2C
+#undef CSB_M2C_B
     default: fail(CSB_EINVAL, "moms2cums: device path supports orders <= 6");
   }
   CSB_CUDA(cudaGetLastError());

@@ -48,6 +48,12 @@ struct M2CParams {
   LayoutDev lay[kMaxOrder];         // layouts of orders 1..S (index s-1)
   int n = 0, b = 0;
   uint64_t blk0 = 0;                // first block of the shard
+  // (dst, src) symmetric-copy pairs of a full block per run pattern (or
+  // nullptr); with them a full block is assembled in shared memory at
+  // cblk (doubles past the staged sub-blocks) and written out coalesced
+  const uint2* mlist = nullptr;
+  const uint32_t* mlist_off = nullptr;
+  uint32_t cblk = 0;
   const uint64_t* subs = nullptr;   // per block, masks 1..2^S-2: offset of the sub-block in C_|mask|
   // canonical positions of a full block (all extents b) per run pattern
   // (bit k-1: j_k == j_{k-1}): canon[canon_off[pat] .. canon_off[pat + 1])

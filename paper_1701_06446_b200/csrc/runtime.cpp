@@ -698,6 +698,9 @@ void run_moms2cums(const csb_series* m, csb_series* c, NormScratch& ns, cudaStre
         auto cl = get_canon(*m->dev, s, m->b);
         p.canon = cl.first;
         p.canon_off = cl.second;
+        auto ml = get_mirror_lists(*m->dev, s, m->b);
+        p.mlist = ml.first;
+        p.mlist_off = ml.second;
       }
     }
     if (s == d && sh.active()) {
@@ -715,6 +718,8 @@ void run_moms2cums(const csb_series* m, csb_series* c, NormScratch& ns, cudaStre
     } else {
       p.blk0 = 0;
       p.partial = ns.partial[s - 1].ptr;
+      static const char* const tags[] = {"m2c_1", "m2c_2", "m2c_3", "m2c_4", "m2c_5", "m2c_6", "m2c_7", "m2c_8"};
+      ProfScope po(tags[s - 1], st);
       launch_moms2cums_v2(s, p, m->lay[s - 1]->host.nblocks, st);
     }
   }
