@@ -19,8 +19,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CASES = [  # (n, d, b, T, p, steps, seed)
     (96, 4, 8, 300, 60, 2, 11),    # cfg1 geometry: windows of 12..1 column tiles
     (130, 3, 16, 200, 50, 2, 12),  # > 16 column tiles: split column ranges, edge blocks
-    (48, 6, 4, 60, 12, 2, 13),     # cfg2 geometry (order 6)
-    (72, 5, 8, 60, 20, 1, 14),     # order 5, full and edge blocks
+    (48, 6, 4, 24, 8, 2, 13),      # cfg2 geometry (order 6)
+    (72, 5, 8, 40, 10, 1, 14),     # order 5, full and edge blocks
 ]
 
 
