@@ -162,6 +162,18 @@ __global__ void __launch_bounds__(256, 2) moms2cums_v2(const M2CParams P) {
     }
     if (inblk) asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
     __syncthreads();
+    if (inblk && P.mfix) {
+      // M's symmetric copies from the staged block (before C overwrites it)
+      uint32_t pat = 0;
+#pragma unroll
+      for (int k = 1; k < S; ++k) pat |= static_cast<uint32_t>(j[k] == j[k - 1]) << (k - 1);
+      const uint32_t i1 = P.mlist_off[pat + 1];
+      for (uint32_t i = P.mlist_off[pat] + threadIdx.x; i < i1; i += blockDim.x) {
+        const uint2 pr = __ldg(P.mlist + i);
+        P.mfix[boff + pr.x] = cblk[pr.y];
+      }
+      __syncthreads();
+    }
   }
 
   // phase 1: canonical entries.  Full blocks (all extents b) walk the
@@ -514,21 +526,37 @@ size_t moms2cums_stage_bytes(int S, int n, int b) {
   return tot * sizeof(double);
 }
 
+namespace {
+constexpr size_t kM2cInblkLimit = 64 * 1024;  // staged sub-blocks + one block: >= 3 CTAs per SM
+size_t m2c_block_vol(int S, int n, int b) {
+  size_t vol = 1;
+  for (int k = 0; k < S; ++k) vol *= static_cast<size_t>(b < n ? b : n);
+  return vol;
+}
+}  // namespace
+
+bool m2c_fuse_ok(int S, int n, int b) {
+  if (S < 2 || S > 6 || n % b != 0) return false;  // every block full
+  const size_t sm0 = moms2cums_stage_bytes(S, n, b);
+  const size_t vol = m2c_block_vol(S, n, b);
+  return sm0 <= 160 * 1024 && vol <= (1u << 20) && sm0 + vol * sizeof(double) <= kM2cInblkLimit;
+}
+
 void launch_moms2cums_v2(int S, const M2CParams& p, uint64_t nblocks, cudaStream_t st) {
   if (nblocks == 0) return;
   const unsigned g = static_cast<unsigned>(nblocks);
   const size_t sm0 = moms2cums_stage_bytes(S, p.n, p.b);
   const bool staged = sm0 <= 160 * 1024;
   // one full block of C_S beside the staged sub-blocks, when it fits
-  size_t vol = 1;
-  for (int k = 0; k < S; ++k) vol *= static_cast<size_t>(p.b < p.n ? p.b : p.n);
+  const size_t vol = m2c_block_vol(S, p.n, p.b);
   M2CParams q = p;
   size_t sm = sm0;
-  if (staged && q.mlist && sm0 + vol * sizeof(double) <= 64 * 1024) {
+  if (staged && q.mlist && sm0 + vol * sizeof(double) <= kM2cInblkLimit) {
     q.cblk = static_cast<uint32_t>(sm0 / sizeof(double));
     sm = sm0 + vol * sizeof(double);
   } else {
     q.mlist = nullptr;
+    if (q.mfix) fail(CSB_ERUNTIME, "moms2cums: deferred mirror without an in-block pass");
   }
   const int bb = p.b < p.n ? p.b : p.n;
   switch (S) {

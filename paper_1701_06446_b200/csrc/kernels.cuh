@@ -54,6 +54,7 @@ struct M2CParams {
   const uint2* mlist = nullptr;
   const uint32_t* mlist_off = nullptr;
   uint32_t cblk = 0;
+  double* mfix = nullptr;  // M_S itself: also write its symmetric copies from the staged block
   const uint64_t* subs = nullptr;   // per block, masks 1..2^S-2: offset of the sub-block in C_|mask|
   // canonical positions of a full block (all extents b) per run pattern
   // (bit k-1: j_k == j_{k-1}): canon[canon_off[pat] .. canon_off[pat + 1])
@@ -117,6 +118,9 @@ struct NormParams {
 
 void launch_moment_pair(const MomParams& p, int ntiles, bool top_fma, cudaStream_t st);
 void launch_moms2cums(int S, const M2CParams& p, uint64_t nblocks, cudaStream_t st);
+// whether moms2cums of order S assembles every block in shared memory
+// (then it can also fill M_S's symmetric copies: MomentPlan's deferred mirror)
+bool m2c_fuse_ok(int S, int n, int b);
 void launch_moms2cums_v2(int S, const M2CParams& p, uint64_t nblocks, cudaStream_t st);
 void launch_moment_lower(int S, const LowerParams& p, cudaStream_t st);
 void launch_moment_lower2(int ST, int W, const Lower2Params& p, cudaStream_t st);

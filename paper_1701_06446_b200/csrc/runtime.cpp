@@ -423,6 +423,9 @@ struct csb_series {
   Device* dev = nullptr;
   std::vector<std::shared_ptr<DevLayout>> lay;  // orders 1..d
   std::vector<DevBuf<double>> data;
+  // orders (bit s-1) whose symmetric copies the next run_moms2cums fills
+  // from its staged blocks instead of a mirror kernel (stream step only)
+  mutable uint32_t mirror_defer = 0;
 };
 
 namespace csb {
@@ -518,7 +521,7 @@ struct ShardCtx {
 };
 
 void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, double c,
-                 cudaStream_t st, int only_order = 0, const ShardCtx& sh = ShardCtx{}) {
+                 cudaStream_t st, int only_order = 0, const ShardCtx& sh = ShardCtx{}, bool defer_mirror = false) {
   Device& dev = *m->dev;
   const int d = m->d;
   const int S = only_order ? only_order : d;
@@ -629,14 +632,23 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
       ProfScope pm("mirror", st);
       const auto& LT = m->lay[S - 1];
       auto rt = sharded ? LT->diag_range(sh.lo(0), sh.hi(0)) : std::make_pair(0u, LT->ndiag);
+      // in a stream step the next moms2cums stages these blocks anyway and
+      // writes their copies (same values, one pass less over M)
+      const bool fuse = defer_mirror && !sharded;
       auto ml = get_mirror_lists(*m->dev, S, m->b);
-      launch_mirror(S, p.top, LT->view(), LT->diag.ptr + rt.first, rt.second, m->n, m->b, ml.first, ml.second, st);
+      if (fuse && ml.first && m2c_fuse_ok(S, m->n, m->b))
+        m->mirror_defer |= 1u << (S - 1);
+      else
+        launch_mirror(S, p.top, LT->view(), LT->diag.ptr + rt.first, rt.second, m->n, m->b, ml.first, ml.second, st);
       if (p.low) {
         const auto& LL = m->lay[S - 2];
         auto rl = sharded ? LL->diag_range(sh.lo(1), sh.hi(1)) : std::make_pair(0u, LL->ndiag);
         auto ml1 = get_mirror_lists(*m->dev, S - 1, m->b);
-        launch_mirror(S - 1, p.low, LL->view(), LL->diag.ptr + rl.first, rl.second, m->n, m->b, ml1.first, ml1.second,
-                      st);
+        if (fuse && ml1.first && m2c_fuse_ok(S - 1, m->n, m->b))
+          m->mirror_defer |= 1u << (S - 2);
+        else
+          launch_mirror(S - 1, p.low, LL->view(), LL->diag.ptr + rl.first, rl.second, m->n, m->b, ml1.first,
+                        ml1.second, st);
         if (sharded && sh.comm) {
           // collective C2: every rank needs all of M_{d-1} (its own blocks
           // were just updated, the rest arrive from their owners)
@@ -702,6 +714,10 @@ void run_moms2cums(const csb_series* m, csb_series* c, NormScratch& ns, cudaStre
         p.mlist = ml.first;
         p.mlist_off = ml.second;
       }
+    }
+    if (m->mirror_defer >> (s - 1) & 1u) {
+      p.mfix = m->data[s - 1].ptr;  // write M_s's copies too (run_moments deferred them)
+      m->mirror_defer &= ~(1u << (s - 1));
     }
     if (s == d && sh.active()) {
       // C_d only for the owned blocks; the other partials stay zero so a
@@ -915,7 +931,7 @@ void stream_exchange_and_update(csb_stream* s, const double* x_dev) {
     src[0].seg0 = x_dev;
     src[0].len0 = static_cast<uint32_t>(p);
     src[1] = out;
-    run_moments(s->M.get(), src, 2, p, static_cast<double>(p) / static_cast<double>(T), s->st, 0, s->sh);
+    run_moments(s->M.get(), src, 2, p, static_cast<double>(p) / static_cast<double>(T), s->st, 0, s->sh, true);
     g_rows_read.fetch_add(2 * p, std::memory_order_relaxed);
   }
   // incoming rows take the outgoing slots
