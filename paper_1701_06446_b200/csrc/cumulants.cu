@@ -96,6 +96,7 @@ __global__ void __launch_bounds__(256, 2) moms2cums_v2(const M2CParams P) {
   __shared__ uint64_t sbase[NM];                  // global (or smem) base per subset
   __shared__ uint32_t sstride[NM][S];
   __shared__ double red[8];
+  __shared__ __align__(8) uint64_t mbar;  // TMA staging of a full block (even b)
   const uint64_t blk = P.blk0 + blockIdx.x;
   const LayoutDev& LS = P.lay[S - 1];
   const int n = P.n, b = B ? B : P.b;
@@ -124,6 +125,17 @@ __global__ void __launch_bounds__(256, 2) moms2cums_v2(const M2CParams P) {
     }
     if (!STAGED) sbase[m] = subs[m - 1];
   }
+  bool full = true;
+#pragma unroll
+  for (int k = 0; k < S; ++k) full &= e[k] == b;
+  // a full block is assembled in shared memory: M staged, C computed in
+  // place (each canonical position by the thread that reads it), copies
+  // filled from the pattern list, then written out coalesced
+  const bool inblk = STAGED && full && P.canon && P.mlist;
+  double* cblk = sfac + P.cblk;
+  // full blocks of an even compile-time b: every sub-block and the M block
+  // are whole 16-byte-aligned blocks -> one TMA bulk copy each
+  const bool bulk = B != 0 && (B % 2) == 0 && inblk && n % b == 0;
   if (STAGED && threadIdx.x == 0) {
     uint32_t soff = 0;
     for (int m = 1; m < NM; ++m) {
@@ -133,17 +145,21 @@ __global__ void __launch_bounds__(256, 2) moms2cums_v2(const M2CParams P) {
       sbase[m] = soff;  // offset of the staged copy in shared memory
       soff += svol;
     }
+    if (bulk) {
+      ptx::mbar_init(&mbar, 1);
+      ptx::fence_mbar_init();
+      ptx::mbar_expect_tx(&mbar, static_cast<uint32_t>((soff + vol) * sizeof(double)));
+      ptx::bulk_g2s(cblk, P.m + boff, vol * sizeof(double), &mbar);
+      for (int m = 1; m < NM; ++m) {
+        const uint32_t svol = static_cast<uint32_t>((m + 1 < NM ? sbase[m + 1] : soff) - sbase[m]);
+        ptx::bulk_g2s(sfac + sbase[m], P.lower[popcount_c(m) - 1] + subs[m - 1], svol * sizeof(double), &mbar);
+      }
+    }
   }
   __syncthreads();
-  bool full = true;
-#pragma unroll
-  for (int k = 0; k < S; ++k) full &= e[k] == b;
-  // a full block is assembled in shared memory: M staged, C computed in
-  // place (each canonical position by the thread that reads it), copies
-  // filled from the pattern list, then written out coalesced
-  const bool inblk = STAGED && full && P.canon && P.mlist;
-  double* cblk = sfac + P.cblk;
-  if (STAGED) {
+  if (bulk) {
+    ptx::mbar_wait(&mbar, 0);
+  } else if (STAGED) {
     if (inblk)
       for (uint32_t t = threadIdx.x; t < vol; t += blockDim.x) cp_async8(cblk + t, P.m + boff + t);
     // copy every needed sub-block into shared memory (coalesced per subset;
@@ -162,6 +178,8 @@ __global__ void __launch_bounds__(256, 2) moms2cums_v2(const M2CParams P) {
     }
     if (inblk) asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
     __syncthreads();
+  }
+  if (STAGED) {
     if (inblk && P.mfix) {
       // M's symmetric copies from the staged block (before C overwrites it)
       uint32_t pat = 0;
@@ -191,6 +209,11 @@ __global__ void __launch_bounds__(256, 2) moms2cums_v2(const M2CParams P) {
     bp[0] = 1;
 #pragma unroll
     for (int k = 1; k < S; ++k) bp[k] = bp[k - 1] * static_cast<uint32_t>(b);
+    // staged sub-block bases in registers (32-bit shared-memory offsets)
+    constexpr int NB = S <= 5 ? NM : 1;
+    uint32_t sb[NB];
+#pragma unroll
+    for (int m = 1; m < NB; ++m) sb[m] = static_cast<uint32_t>(sbase[m]);
     for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
       const uint32_t pos = __ldg(list + i);
       int o[S];
@@ -212,7 +235,7 @@ __global__ void __launch_bounds__(256, 2) moms2cums_v2(const M2CParams P) {
 #pragma unroll
         for (int k = S - 1; k >= 0; --k)
           if (m >> k & 1) a += static_cast<uint32_t>(o[k]) * bp[after++];
-        f[m] = sfac[sbase[m] + a];
+        f[m] = sfac[(S <= 5 ? sb[m < NB ? m : 0] : static_cast<uint32_t>(sbase[m])) + a];
       }
       const double corr = partition_correction<S>(f);
       if (inblk)
