@@ -520,8 +520,12 @@ struct ShardCtx {
   uint64_t hi(int which) const { return (which ? plan->low_blk : plan->top_blk)[index + 1]; }
 };
 
+// side_tail: work that depends only on orders <= d-2, enqueued on the side
+// stream behind the low-order kernel (the stream step's C_1, C_2); returns
+// whether it ran there (else the caller does it in line)
 void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, double c,
-                 cudaStream_t st, int only_order = 0, const ShardCtx& sh = ShardCtx{}, bool defer_mirror = false) {
+                 cudaStream_t st, int only_order = 0, const ShardCtx& sh = ShardCtx{}, bool defer_mirror = false,
+                 const std::function<void(cudaStream_t)>& side_tail = nullptr, bool* side_tail_ran = nullptr) {
   Device& dev = *m->dev;
   const int d = m->d;
   const int S = only_order ? only_order : d;
@@ -578,14 +582,21 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
     lp.inv = 1.0 / static_cast<double>(K);
     if (side) {
       CSB_CUDA(cudaEventRecord(dev.fork, st));  // the low orders depend only on work queued so far
-      side_launch = [&dev, ST, lp]() {
+      side_launch = [&dev, ST, lp, &side_tail, side_tail_ran]() {
+        {
+          std::lock_guard<std::mutex> lk(dev.mu);
+          CSB_CUDA(cudaStreamWaitEvent(dev.side, dev.fork, 0));
+          ProfScope pl("moment_low", dev.side);
+          if (g_low_tma && lower_tma_supported(lp))
+            launch_moment_lower_tma(ST, lp, dev.side);
+          else
+            launch_moment_lower_side(ST, lp, dev.side);
+        }
+        if (side_tail) {  // takes dev.mu itself (plan/table caches)
+          side_tail(dev.side);
+          if (side_tail_ran) *side_tail_ran = true;
+        }
         std::lock_guard<std::mutex> lk(dev.mu);
-        CSB_CUDA(cudaStreamWaitEvent(dev.side, dev.fork, 0));
-        ProfScope pl("moment_low", dev.side);
-        if (g_low_tma && lower_tma_supported(lp))
-          launch_moment_lower_tma(ST, lp, dev.side);
-        else
-          launch_moment_lower_side(ST, lp, dev.side);
         CSB_CUDA(cudaEventRecord(dev.join, dev.side));
       };
       if (!g_low_defer) {
@@ -683,18 +694,23 @@ struct NormScratch {
   std::vector<double> host;
 };
 
+// orders [first, last] of moms2cums (C_1 is a copy of M_1), with per-block
+// partial squared norms; the stream step may run the low orders early on
+// the side stream (run_moments' side_tail) and the rest here
 void run_moms2cums(const csb_series* m, csb_series* c, NormScratch& ns, cudaStream_t st,
-                   const ShardCtx& sh = ShardCtx{}) {
+                   const ShardCtx& sh = ShardCtx{}, int first = 1, int last = 0) {
   const int d = m->d;
+  if (last <= 0) last = d;
   if (ns.partial.size() != static_cast<size_t>(d)) {
     ns.partial.clear();
     for (int s = 1; s <= d; ++s) ns.partial.emplace_back(m->lay[s - 1]->host.nblocks);
   }
   ProfScope ps("moms2cums", st);
   const auto& L1 = m->lay[0];
-  launch_copy_c1(m->data[0].ptr, c->data[0].ptr, ns.partial[0].ptr, L1->view(), L1->host.nblocks,
-                 L1->host.stored, st);
-  for (int s = 2; s <= d; ++s) {
+  if (first <= 1)
+    launch_copy_c1(m->data[0].ptr, c->data[0].ptr, ns.partial[0].ptr, L1->view(), L1->host.nblocks,
+                   L1->host.stored, st);
+  for (int s = std::max(2, first); s <= last; ++s) {
     M2CParams p;
     p.m = m->data[s - 1].ptr;
     p.c = c->data[s - 1].ptr;
@@ -886,6 +902,7 @@ struct csb_stream {
   uint64_t window = 0;
   uint64_t steps_since_resync = 0;
   NormScratch ns;
+  int early_m2c = 0;  // moms2cums orders already enqueued on the side stream this step
   bool norms_valid = false;
   std::shared_ptr<ShardPlan> splan;  // shard_count > 1
   ShardCtx sh;
@@ -931,8 +948,18 @@ void stream_exchange_and_update(csb_stream* s, const double* x_dev) {
     src[0].seg0 = x_dev;
     src[0].len0 = static_cast<uint32_t>(p);
     src[1] = out;
-    run_moments(s->M.get(), src, 2, p, static_cast<double>(p) / static_cast<double>(T), s->st, 0, s->sh, true);
+    // C_1, C_2 need only M_1, M_2 (the low-order kernel's): on the side stream
+    const int early = s->sh.active() ? 0 : std::min(2, cfg.max_order - 2);
+    std::function<void(cudaStream_t)> tail;
+    if (early >= 1)
+      tail = [s, early](cudaStream_t side) { run_moms2cums(s->M.get(), s->C.get(), s->ns, side, s->sh, 1, early); };
+    bool ran = false;
+    run_moments(s->M.get(), src, 2, p, static_cast<double>(p) / static_cast<double>(T), s->st, 0, s->sh, true,
+                tail, &ran);
+    s->early_m2c = ran ? early : 0;
     g_rows_read.fetch_add(2 * p, std::memory_order_relaxed);
+  } else {
+    s->early_m2c = 0;
   }
   // incoming rows take the outgoing slots
   CSB_CUDA(cudaMemcpyAsync(s->ring.ptr + s->head * n, x_dev, first * n * sizeof(double),
@@ -972,7 +999,7 @@ int stream_step_impl(csb_stream* s, const double* x, bool on_device, uint64_t ro
     CSB_CUDA(cudaEventRecord(s->ev[0], s->st));
     stream_exchange_and_update(s, xd);
     CSB_CUDA(cudaEventRecord(s->ev[1], s->st));
-    run_moms2cums(s->M.get(), s->C.get(), s->ns, s->st, s->sh);
+    run_moms2cums(s->M.get(), s->C.get(), s->ns, s->st, s->sh, 1 + s->early_m2c);
     CSB_CUDA(cudaEventRecord(s->ev[2], s->st));
     s->norms_valid = false;
     ++s->window;
