@@ -691,7 +691,27 @@ struct NormScratch {
   std::vector<DevBuf<double>> partial;  // per order
   DevBuf<double> diag;                  // gathered diagonal of a sharded C_d
   DevBuf<double> out;
-  std::vector<double> host;
+  // pinned: the report's D2H is a direct DMA, not a staged pageable copy
+  struct Pinned {
+    double* p = nullptr;
+    size_t n = 0;
+    Pinned() = default;
+    Pinned(const Pinned&) = delete;
+    Pinned& operator=(const Pinned&) = delete;
+    ~Pinned() {
+      if (p) cudaFreeHost(p);
+    }
+    void resize(size_t k) {
+      if (k <= n) return;
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      n = 0;
+      CSB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&p), k * sizeof(double)));
+      n = k;
+    }
+    double* data() { return p; }
+    const double* data() const { return p; }
+  } host;
 };
 
 // orders [first, last] of moms2cums (C_1 is a copy of M_1), with per-block
@@ -997,13 +1017,20 @@ int stream_step_impl(csb_stream* s, const double* x, bool on_device, uint64_t ro
       xd = s->staging.ptr;
     }
     CSB_CUDA(cudaEventRecord(s->ev[0], s->st));
-    stream_exchange_and_update(s, xd);
+    {
+      ProfScope pu("step_update", s->st);
+      stream_exchange_and_update(s, xd);
+    }
     CSB_CUDA(cudaEventRecord(s->ev[1], s->st));
-    run_moms2cums(s->M.get(), s->C.get(), s->ns, s->st, s->sh, 1 + s->early_m2c);
+    {
+      ProfScope pc("step_m2c", s->st);
+      run_moms2cums(s->M.get(), s->C.get(), s->ns, s->st, s->sh, 1 + s->early_m2c);
+    }
     CSB_CUDA(cudaEventRecord(s->ev[2], s->st));
     s->norms_valid = false;
     ++s->window;
     if (report) {
+      ProfScope pr("step_report", s->st);
       finalize_norms(s->C.get(), s->ns, s->st, s->sh);
       s->norms_valid = true;
       build_report(s->C.get(), s->ns, s->window, report);
