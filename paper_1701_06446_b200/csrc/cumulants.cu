@@ -131,11 +131,11 @@ __global__ void __launch_bounds__(256, 2) moms2cums_v2(const M2CParams P) {
   // a full block is assembled in shared memory: M staged, C computed in
   // place (each canonical position by the thread that reads it), copies
   // filled from the pattern list, then written out coalesced
-  const bool inblk = STAGED && full && P.canon && P.mlist;
+  const bool inblk = STAGED && full && P.canon && P.mlist && P.inblk;
   double* cblk = sfac + P.cblk;
   // full blocks of an even compile-time b: every sub-block and the M block
   // are whole 16-byte-aligned blocks -> one TMA bulk copy each
-  const bool bulk = B != 0 && (B % 2) == 0 && inblk && n % b == 0;
+  const bool bulk = B != 0 && (B % 2) == 0 && STAGED && full && n % b == 0;
   if (STAGED && threadIdx.x == 0) {
     uint32_t soff = 0;
     for (int m = 1; m < NM; ++m) {
@@ -148,8 +148,8 @@ __global__ void __launch_bounds__(256, 2) moms2cums_v2(const M2CParams P) {
     if (bulk) {
       ptx::mbar_init(&mbar, 1);
       ptx::fence_mbar_init();
-      ptx::mbar_expect_tx(&mbar, static_cast<uint32_t>((soff + vol) * sizeof(double)));
-      ptx::bulk_g2s(cblk, P.m + boff, vol * sizeof(double), &mbar);
+      ptx::mbar_expect_tx(&mbar, static_cast<uint32_t>((soff + (inblk ? vol : 0)) * sizeof(double)));
+      if (inblk) ptx::bulk_g2s(cblk, P.m + boff, vol * sizeof(double), &mbar);
       for (int m = 1; m < NM; ++m) {
         const uint32_t svol = static_cast<uint32_t>((m + 1 < NM ? sbase[m + 1] : soff) - sbase[m]);
         ptx::bulk_g2s(sfac + sbase[m], P.lower[popcount_c(m) - 1] + subs[m - 1], svol * sizeof(double), &mbar);
@@ -284,7 +284,25 @@ __global__ void __launch_bounds__(256, 2) moms2cums_v2(const M2CParams P) {
       part = __fma_rn(v, v, part);
     }
   }
-  for (uint32_t pos = threadIdx.x; !inblk && pos < vol; pos += blockDim.x) {
+  const bool listed = !inblk && STAGED && full && P.canon && P.mlist;
+  if (listed) {
+    // copies from the canonical entries this CTA just wrote (visible to the
+    // block after the barrier above), then the sum of squares in order
+    uint32_t pat = 0;
+#pragma unroll
+    for (int k = 1; k < S; ++k) pat |= static_cast<uint32_t>(j[k] == j[k - 1]) << (k - 1);
+    const uint32_t i1 = P.mlist_off[pat + 1];
+    for (uint32_t i = P.mlist_off[pat] + threadIdx.x; i < i1; i += blockDim.x) {
+      const uint2 pr = __ldg(P.mlist + i);
+      P.c[boff + pr.x] = P.c[boff + pr.y];
+    }
+    __syncthreads();
+    for (uint32_t pos = threadIdx.x; pos < vol; pos += blockDim.x) {
+      const double v = P.c[boff + pos];
+      part = __fma_rn(v, v, part);
+    }
+  }
+  for (uint32_t pos = threadIdx.x; !inblk && !listed && pos < vol; pos += blockDim.x) {
     int o[S];
     decode<S>(pos, e, o);
     double v;
@@ -576,9 +594,10 @@ void launch_moms2cums_v2(int S, const M2CParams& p, uint64_t nblocks, cudaStream
   size_t sm = sm0;
   if (staged && q.mlist && sm0 + vol * sizeof(double) <= kM2cInblkLimit) {
     q.cblk = static_cast<uint32_t>(sm0 / sizeof(double));
+    q.inblk = true;
     sm = sm0 + vol * sizeof(double);
   } else {
-    q.mlist = nullptr;
+    q.inblk = false;
     if (q.mfix) fail(CSB_ERUNTIME, "moms2cums: deferred mirror without an in-block pass");
   }
   const int bb = p.b < p.n ? p.b : p.n;

@@ -54,6 +54,7 @@ struct M2CParams {
   const uint2* mlist = nullptr;
   const uint32_t* mlist_off = nullptr;
   uint32_t cblk = 0;
+  bool inblk = false;  // launcher: the block fits beside the sub-blocks (cblk valid)
   double* mfix = nullptr;  // M_S itself: also write its symmetric copies from the staged block
   const uint64_t* subs = nullptr;   // per block, masks 1..2^S-2: offset of the sub-block in C_|mask|
   // canonical positions of a full block (all extents b) per run pattern
