@@ -551,7 +551,9 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
   // orders <= d-2 beside the DMMA top pair: a lean kernel on the side
   // stream (joined at the end of this call) when they are few (it is
   // latency bound and hides under the top pair); else staged, in line
-  const bool side = lower && d - 2 <= 4 && use_dmma && g_low_side && multiset_count(m->n, d - 2) <= 60000;
+  // (the TMA-staged kernel handles any count when rows are 16-byte multiples)
+  const bool side = lower && d - 2 <= 4 && use_dmma && g_low_side &&
+                    (multiset_count(m->n, d - 2) <= 60000 || (g_low_tma && m->n % 2 == 0));
   bool joined = true;
   // The side-stream launch is deferred until the top kernel is queued: the
   // block scheduler hands SMs to the top kernel's CTAs first and the few
