@@ -30,6 +30,14 @@ inline void cuda_check(cudaError_t e, const char* what) {
 }
 #define CSB_CUDA(call) ::csb::cuda_check((call), #call)
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel, device
+// and size (it costs microseconds of host time per call on the step path)
+void set_smem_attr(const void* kern, size_t bytes);
+template <class K>
+inline void ensure_smem(K kern, size_t bytes) {
+  set_smem_attr(reinterpret_cast<const void*>(kern), bytes);
+}
+
 // Owning device allocation (value-less; copying is explicit).
 template <class T>
 struct DevBuf {

@@ -603,8 +603,7 @@ void launch_moms2cums_v2(int S, const M2CParams& p, uint64_t nblocks, cudaStream
   const int bb = p.b < p.n ? p.b : p.n;
   switch (S) {
 #define CSB_M2C_B(SS, BB)                                                                                  \
-  CSB_CUDA(cudaFuncSetAttribute(moms2cums_v2<SS, true, BB>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
-                                static_cast<int>(sm)));                                                   \
+  ensure_smem(moms2cums_v2<SS, true, BB>, sm);                                                             \
   moms2cums_v2<SS, true, BB><<<g, 256, sm, st>>>(q);
 #define CSB_M2C(SS)                                                                                         \
   case SS:                                                                                                  \
@@ -837,8 +836,7 @@ void launch_moment_lower_tma(int ST, const Lower2Params& p, cudaStream_t st) {
   switch (ST) {
 #define CSB_LOWT(SS)                                                                                          \
   case SS:                                                                                                    \
-    CSB_CUDA(cudaFuncSetAttribute(moment_lower_tma_kernel<SS>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                  static_cast<int>(sm)));                                                     \
+    ensure_smem(moment_lower_tma_kernel<SS>, sm);                                                     \
     moment_lower_tma_kernel<SS><<<g, LOWT_THREADS + 32, sm, st>>>(p, stages, kr);                             \
     break;
     CSB_LOWT(1) CSB_LOWT(2) CSB_LOWT(3) CSB_LOWT(4)
@@ -870,8 +868,7 @@ void launch_moment_lower2(int ST, int W, const Lower2Params& p, cudaStream_t st)
   switch (ST * 8 + W) {
 #define CSB_LOW2(SS, WW)                                                                                  \
   case SS * 8 + WW:                                                                                       \
-    CSB_CUDA(cudaFuncSetAttribute(moment_lower2_kernel<SS, WW>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                  static_cast<int>(sm)));                                                 \
+    ensure_smem(moment_lower2_kernel<SS, WW>, sm);                                                      \
     moment_lower2_kernel<SS, WW><<<g, LOW2_THREADS, sm, st>>>(p);                                         \
     break;
     CSB_LOW2(1, 1) CSB_LOW2(1, 4) CSB_LOW2(2, 1) CSB_LOW2(2, 4) CSB_LOW2(3, 1) CSB_LOW2(3, 4) CSB_LOW2(4, 1)

@@ -478,12 +478,10 @@ void launch_moment_pair(const MomParams& p, int ntiles, bool top_fma, cudaStream
   const size_t smem = sizeof(double) * (KC * XS + KC * BS + KC * MAXROWS + MAXROWS) +
                       sizeof(uint16_t) * MAXROWS * 8;
   if (top_fma) {
-    CSB_CUDA(cudaFuncSetAttribute(moment_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
+    ensure_smem(moment_pair_kernel<true>, smem);
     moment_pair_kernel<true><<<ntiles, T, smem, st>>>(p);
   } else {
-    CSB_CUDA(cudaFuncSetAttribute(moment_pair_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
+    ensure_smem(moment_pair_kernel<false>, smem);
     moment_pair_kernel<false><<<ntiles, T, smem, st>>>(p);
   }
   CSB_CUDA(cudaGetLastError());

@@ -980,7 +980,7 @@ void launch_moment_top_dmma(const MomParams& p_in, int ntiles, cudaStream_t st) 
   else if (hs == 8) kern = moment_top_dmma_kernel<0, 8, 0>;
   else if (hs == 6) kern = moment_top_dmma_kernel<0, 6, 0>;
   else kern = moment_top_dmma_kernel<0, 4, 0>;
-  CSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  ensure_smem(kern, smem);
   kern<<<ntiles, THREADS, smem, st>>>(p);
   CSB_CUDA(cudaGetLastError());
   count_launch();

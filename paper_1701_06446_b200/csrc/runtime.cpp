@@ -167,7 +167,26 @@ std::shared_ptr<MomentPlan> get_plan(Device& dev, int S, int n, int b, bool dmma
   return slot;
 }
 
-// Optional per-launch event timing (csb_profile_enable).
+}  // namespace
+
+void set_smem_attr(const void* kern, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  CSB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& have = done[{kern, dev}];
+  if (have >= bytes) return;
+  CSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+  have = bytes;
+}
+
+namespace {
+
+// Optional per-launch event timing (csb_profile_enable); events are pooled
+// (created once, returned by csb_profile_read) to keep the host cost of a
+// profiled step small.
+
 struct Profiler {
   std::mutex mu;
   bool on = false;
@@ -175,6 +194,17 @@ struct Profiler {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
   };
   std::map<std::string, Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t get() {  // under mu
+    if (pool.empty()) {
+      cudaEvent_t e = nullptr;
+      CSB_CUDA(cudaEventCreate(&e));
+      return e;
+    }
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
 };
 Profiler g_prof;
 
@@ -184,8 +214,11 @@ struct ProfScope {
   const char* tag;
   ProfScope(const char* tag_, cudaStream_t st_) : st(st_), tag(tag_) {
     if (!g_prof.on) return;
-    CSB_CUDA(cudaEventCreate(&a));
-    CSB_CUDA(cudaEventCreate(&b));
+    {
+      std::lock_guard<std::mutex> lk(g_prof.mu);
+      a = g_prof.get();
+      b = g_prof.get();
+    }
     CSB_CUDA(cudaEventRecord(a, st));
   }
   ~ProfScope() {
@@ -1533,8 +1566,13 @@ int csb_profile_read(const char* tag, double* total_ms, uint64_t* launches) {
       float ms = 0.f;
       CSB_CUDA(cudaEventElapsedTime(&ms, a, b));
       tot += ms;
-      cudaEventDestroy(a);
-      cudaEventDestroy(b);
+    }
+    {
+      std::lock_guard<std::mutex> lk(g_prof.mu);
+      for (auto& [a, b] : ev) {
+        g_prof.pool.push_back(a);
+        g_prof.pool.push_back(b);
+      }
     }
     *total_ms = tot;
     *launches = ev.size();
