@@ -19,7 +19,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CASES = [  # (n, d, b, T, p, steps, seed)
     (96, 4, 8, 300, 60, 2, 11),    # cfg1 geometry: windows of 12..1 column tiles
     (130, 3, 16, 200, 50, 2, 12),  # > 16 column tiles: split column ranges, edge blocks
-    (48, 6, 4, 24, 8, 2, 13),      # cfg2 geometry (order 6)
+    (40, 6, 4, 24, 8, 2, 13),      # cfg2 geometry (order 6, R = 2 and 4 windows)
     (72, 5, 8, 40, 10, 1, 14),     # order 5, full and edge blocks
 ]
 
@@ -34,7 +34,7 @@ def test_row_sum_tile_modes_bitwise(env):
     """The optional all-ones DMMA tile for the order-(d-1) row sums (kernel
     switches read once per process, hence the subprocess) stays bit-exact."""
     e = dict(os.environ, **env)
-    for case in (CASES[0], CASES[2]):
+    for case in (CASES[0], (32, 6, 4, 16, 4, 1, 15)):
         r = subprocess.run([sys.executable, os.path.join(HERE, "wide_case.py"), *map(str, case)], env=e,
                            capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
