@@ -595,29 +595,33 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
   // ~180 us and cost cfg1's top kernel 31 us (measured; CSB_LOW_DEFER=0).
   std::function<void()> side_launch;
   if (lower && d - 2 <= 4) {
-    std::unique_ptr<ProfScope> ps;
-    if (!side) ps = std::make_unique<ProfScope>("moment_low", st);
     const int ST = d - 2;
-    const int W = side ? 1 : multiset_count(m->n, ST) > 60000 ? 4 : 1;
-    auto th = get_lower2_threads(dev, ST, m->n, W);
-    Lower2Params lp;
-    lp.src[0] = src[0];
-    lp.src[1] = src[1];
-    lp.npass = npass;
-    lp.K = static_cast<uint32_t>(K);
-    lp.n = m->n;
-    lp.b = m->b;
-    lp.threads = th->ptr;
-    lp.nthreads = static_cast<uint32_t>(th->count);
-    for (int s = 1; s <= ST; ++s) {
-      lp.elems[s - 1] = get_lower_elems(dev, s, m->n, m->b, m->lay[s - 1]->host)->ptr;
-      lp.m[s - 1] = m->data[s - 1].ptr;
-    }
-    lp.c = c;
-    lp.inv = 1.0 / static_cast<double>(K);
+    // the tables are looked up inside the launch: on the side path that
+    // runs after the top kernel is queued, keeping the host work before
+    // the step's first (and longest) kernel short
+    auto make_params = [&dev, m, ST, npass, K, c, src](int W) {
+      auto th = get_lower2_threads(dev, ST, m->n, W);
+      Lower2Params lp;
+      lp.src[0] = src[0];
+      lp.src[1] = src[1];
+      lp.npass = npass;
+      lp.K = static_cast<uint32_t>(K);
+      lp.n = m->n;
+      lp.b = m->b;
+      lp.threads = th->ptr;
+      lp.nthreads = static_cast<uint32_t>(th->count);
+      for (int s = 1; s <= ST; ++s) {
+        lp.elems[s - 1] = get_lower_elems(dev, s, m->n, m->b, m->lay[s - 1]->host)->ptr;
+        lp.m[s - 1] = m->data[s - 1].ptr;
+      }
+      lp.c = c;
+      lp.inv = 1.0 / static_cast<double>(K);
+      return lp;
+    };
     if (side) {
       CSB_CUDA(cudaEventRecord(dev.fork, st));  // the low orders depend only on work queued so far
-      side_launch = [&dev, ST, lp, &side_tail, side_tail_ran]() {
+      side_launch = [&dev, ST, make_params, &side_tail, side_tail_ran]() {
+        const Lower2Params lp = make_params(1);
         {
           std::lock_guard<std::mutex> lk(dev.mu);
           CSB_CUDA(cudaStreamWaitEvent(dev.side, dev.fork, 0));
@@ -640,7 +644,9 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
       }
       joined = false;
     } else {
-      launch_moment_lower2(ST, W, lp, st);
+      ProfScope ps("moment_low", st);
+      const int W = multiset_count(m->n, ST) > 60000 ? 4 : 1;
+      launch_moment_lower2(ST, W, make_params(W), st);
     }
   } else if (lower) {
     // orders <= d-2 of d > 6: element-parallel kernel
