@@ -1,5 +1,6 @@
 """Drop-in check: the reference's own doctest unit suites (test_symten,
-test_moments, test_cumulants, test_gauge, test_stream, test_partitions from
+test_moments, test_cumulants, test_gauge, test_stream, test_partitions,
+test_serialize from
 /root/reference/proj/tests, compiled in place -- never copied -- by
 `make -C paper_1701_06446_b200/cpp refsuite`) built against the
 cumstream_b200 C++ headers and linked to the B200 library."""
@@ -27,7 +28,7 @@ def run_suite():
 @pytest.mark.skipif(gpu_available(), reason="CPU-only expectations")
 def test_refsuite_host_cases_pass_without_gpu():
     res, total, passed, failed = run_suite()
-    assert total == 55
+    assert total == 59
     # the host-side utilities (layout, ranker, partitions, predictors, ring
     # buffer) pass; everything touching tensors needs the device
     assert passed >= 15
@@ -37,5 +38,5 @@ def test_refsuite_host_cases_pass_without_gpu():
 @pytest.mark.gpu
 def test_reference_unit_suites_pass_on_b200():
     res, total, passed, failed = run_suite()
-    assert total == 55
+    assert total == 59
     assert failed == 0, res.stderr[-4000:]
