@@ -388,16 +388,26 @@ __global__ void __launch_bounds__(256) moms2cums_kernel(const M2CParams P) {
 
 __global__ void copy_c1_kernel(const double* m1, double* c1, double* partial, LayoutDev lay,
                                uint64_t nblocks) {
-  // C_1 = M_1 (cumulants.cpp:139); one thread per block partial
-  const uint64_t blk = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  // C_1 = M_1 (cumulants.cpp:139), one CTA per block; the block's sum of
+  // squares is reduced exactly as knorm_partials_kernel does (same element
+  // order and association), so stream reports and knorm() agree bitwise
+  const uint64_t blk = blockIdx.x;
   if (blk >= nblocks) return;
+  __shared__ double red[8];
   double s = 0.0;
-  for (uint64_t i = lay.offset[blk]; i < lay.offset[blk + 1]; ++i) {
+  for (uint64_t i = lay.offset[blk] + threadIdx.x; i < lay.offset[blk + 1]; i += blockDim.x) {
     const double v = m1[i];
     c1[i] = v;
     s = __fma_rn(v, v, s);
   }
-  partial[blk] = s;
+  for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) a = __dadd_rn(a, red[w]);
+    partial[blk] = a;
+  }
 }
 
 __global__ void knorm_partials_kernel(const double* t, LayoutDev lay, uint64_t nblocks, double k,
@@ -505,8 +515,7 @@ void launch_moms2cums(int S, const M2CParams& p, uint64_t nblocks, cudaStream_t 
 
 void launch_copy_c1(const double* m1, double* c1, double* partial, const LayoutDev& lay,
                     uint64_t nblocks, uint64_t, cudaStream_t st) {
-  const unsigned g = static_cast<unsigned>((nblocks + 127) / 128);
-  copy_c1_kernel<<<g, 128, 0, st>>>(m1, c1, partial, lay, nblocks);
+  copy_c1_kernel<<<static_cast<unsigned>(nblocks), 256, 0, st>>>(m1, c1, partial, lay, nblocks);
   CSB_CUDA(cudaGetLastError());
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }
