@@ -529,6 +529,10 @@ const bool g_low_defer = [] {
   const char* e = std::getenv("CSB_LOW_DEFER");
   return !(e && e[0] == '0');
 }();
+const bool g_low_top = [] {
+  const char* e = std::getenv("CSB_LOW_TOP");
+  return e && e[0] == '1';
+}();
 const bool g_use_dmma = [] {
   const char* e = std::getenv("CSB_NO_DMMA");
   return !(e && e[0] == '1');
@@ -587,6 +591,10 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
   // (the TMA-staged kernel handles any count when rows are 16-byte multiples)
   const bool side = lower && d - 2 <= 4 && use_dmma && g_low_side &&
                     (multiset_count(m->n, d - 2) <= 60000 || (g_low_tma && m->n % 2 == 0));
+  // CSB_LOW_TOP=1: order d-1 too in the side-stream kernel, so the top
+  // kernel's producers carry no row sums (A/B: see DESIGN.md)
+  const bool low_top = side && g_low_tma && g_low_top && !sharded && d - 1 <= 4 && m->n % 2 == 0;
+  if (low_top) p.low = nullptr;
   bool joined = true;
   // The side-stream launch is deferred until the top kernel is queued: the
   // block scheduler hands SMs to the top kernel's CTAs first and the few
@@ -595,7 +603,7 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
   // ~180 us and cost cfg1's top kernel 31 us (measured; CSB_LOW_DEFER=0).
   std::function<void()> side_launch;
   if (lower && d - 2 <= 4) {
-    const int ST = d - 2;
+    const int ST = low_top ? d - 1 : d - 2;
     // the tables are looked up inside the launch: on the side path that
     // runs after the top kernel is queued, keeping the host work before
     // the step's first (and longest) kernel short
