@@ -16,6 +16,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--label", default="")
     ap.add_argument("--p", type=int, default=0, help="override rows per step (experiments)")
+    ap.add_argument("--resync", action="store_true", help="every step a full recompute (resync_every=1)")
     args = ap.parse_args()
     import torch
 
@@ -27,7 +28,7 @@ def main():
         import dataclasses
         cfg = dataclasses.replace(cfg, p=args.p)
     g = StreamGen(cfg)
-    st = capi.Stream(cfg.n, cfg.d, cfg.T, cfg.p, cfg.b, g.window(), resync_every=0)
+    st = capi.Stream(cfg.n, cfg.d, cfg.T, cfg.p, cfg.b, g.window(), resync_every=1 if args.resync else 0)
     xs = [torch.from_numpy(g.batch(1 + k % cfg.steps)).cuda() for k in range(args.steps + 3)]
     for k in range(3):
         st.step_dev(xs[k].data_ptr(), cfg.p, cfg.n, report=True)
