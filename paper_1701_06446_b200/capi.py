@@ -346,9 +346,12 @@ class Stream:
         except Exception:
             pass
 
-    def step(self, x: np.ndarray, report: bool = True) -> dict | None:
+    def step(self, x: np.ndarray, report: bool = True, timing: bool = False) -> dict | None:
+        """One window update from host rows (csb_stream_step); with timing,
+        self.timing holds the update / moms2cums split (StepTiming)."""
         x = np.ascontiguousarray(x, dtype=np.float64)
-        check(lib().csb_stream_step(self.h, _dptr(x), x.shape[0], x.shape[1], C.byref(self.timing),
+        check(lib().csb_stream_step(self.h, _dptr(x), x.shape[0], x.shape[1],
+                                    C.byref(self.timing) if timing else None,
                                     C.byref(self.rep) if report else None))
         return self.rep.as_dict() if report else None
 

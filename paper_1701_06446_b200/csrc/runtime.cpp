@@ -1065,17 +1065,17 @@ int stream_step_impl(csb_stream* s, const double* x, bool on_device, uint64_t ro
       CSB_CUDA(cudaMemcpyAsync(s->staging.ptr, x, rows * cols * sizeof(double), cudaMemcpyHostToDevice, s->st));
       xd = s->staging.ptr;
     }
-    CSB_CUDA(cudaEventRecord(s->ev[0], s->st));
+    if (timing) CSB_CUDA(cudaEventRecord(s->ev[0], s->st));  // StepTiming only when asked
     {
       ProfScope pu("step_update", s->st);
       stream_exchange_and_update(s, xd);
     }
-    CSB_CUDA(cudaEventRecord(s->ev[1], s->st));
+    if (timing) CSB_CUDA(cudaEventRecord(s->ev[1], s->st));
     {
       ProfScope pc("step_m2c", s->st);
       run_moms2cums(s->M.get(), s->C.get(), s->ns, s->st, s->sh, 1 + s->early_m2c);
     }
-    CSB_CUDA(cudaEventRecord(s->ev[2], s->st));
+    if (timing) CSB_CUDA(cudaEventRecord(s->ev[2], s->st));
     s->norms_valid = false;
     ++s->window;
     if (report) {
