@@ -309,8 +309,20 @@ void MomentPlan::build_dmma(int S_, int n_, int b_, const Layout& top, const Lay
     if (!nrs) continue;
     // R row sets x 4/R column ranges of at most 4 column tiles per DMMA warp
     const int ncg = (n - 8 * h + 7) / 8;
-    const int R = ncg <= 4 ? 4 : ncg <= 8 ? 2 : 1;
-    const int per_cta = 4 * (4 / R);
+    // R row sets per CTA, up to kMaxNc column tiles per DMMA warp (8 warps):
+    // each row set's tiles spread over 4/R sub-partitions; the choice keeps
+    // the busiest sub-partition's share per row set smallest
+    constexpr int kMaxNc = 3;
+    static const int r4max = [] {  // CSB_R4_MAX / CSB_R2_MAX: thresholds (experiments)
+      const char* e = std::getenv("CSB_R4_MAX");
+      return e ? std::atoi(e) : 6;
+    }();
+    static const int r2max = [] {
+      const char* e = std::getenv("CSB_R2_MAX");
+      return e ? std::atoi(e) : 12;
+    }();
+    const int R = ncg <= std::min(r4max, 6) ? 4 : ncg <= std::min(r2max, 12) ? 2 : 1;
+    const int per_cta = kMaxNc * 8 / R;
     const int nranges = (ncg + per_cta - 1) / per_cta;
     for (int q = 0; q < nranges; ++q) {
       const int c0 = q * ncg / nranges, c1 = (q + 1) * ncg / nranges;

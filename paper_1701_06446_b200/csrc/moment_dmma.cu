@@ -51,7 +51,10 @@ namespace {
 constexpr int CWARPS = 8;                 // DMMA consumer warps (two per SM sub-partition)
 constexpr int PWARPS = 4;                 // producer warps (one per row set)
 constexpr int THREADS = (CWARPS + PWARPS) * 32;
-constexpr int MAXNC = 2;                  // column tiles per DMMA warp
+#ifndef CSB_MAXNC
+#define CSB_MAXNC 3
+#endif
+constexpr int MAXNC = CSB_MAXNC;          // column tiles per DMMA warp
 // Chunk geometry: HS k4 steps (4 HS data rows) per chunk, stage and A slot;
 // HS is a kernel template parameter (8, 6 or 4, whichever leaves >= 5 stages).
 constexpr int ASTRIDE = 8;                // doubles per (r, q) A-ring entry (swizzled, see apos)
@@ -795,13 +798,17 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
   if (rs >= nrs) return;
   int ct0, ct1;
   warp_tiles(warp, R, nct, ct0, ct1);
-  static_assert(MAXNC == 2, "column tiles per DMMA warp");
+  static_assert(MAXNC == 2 || MAXNC == 3, "column tiles per DMMA warp");
   const bool wones = ones && ct1 == nct;  // this warp's last tile is the row-sum tile
   switch ((ct1 - ct0) * 2 + (wones ? 1 : 0)) {
     case 2: consume<1, N, HS, B, false>(P, tile, g, rs, ct0, warp); break;
     case 3: consume<1, N, HS, B, true>(P, tile, g, rs, ct0, warp); break;
     case 4: consume<2, N, HS, B, false>(P, tile, g, rs, ct0, warp); break;
     case 5: consume<2, N, HS, B, true>(P, tile, g, rs, ct0, warp); break;
+#if CSB_MAXNC >= 3
+    case 6: consume<3, N, HS, B, false>(P, tile, g, rs, ct0, warp); break;
+    case 7: consume<3, N, HS, B, true>(P, tile, g, rs, ct0, warp); break;
+#endif
     default: break;
   }
 #if CSB_EXP & 64  // timing experiment: per-CTA timeline of consumer warps
