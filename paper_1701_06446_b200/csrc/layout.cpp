@@ -344,17 +344,15 @@ void MomentPlan::build_dmma(int S_, int n_, int b_, const Layout& top, const Lay
   auto width = [](const MomTile& t) { return (t.ncols + (4 / t.pad0) - 1) / (4 / t.pad0); };
   std::stable_sort(tiles.begin(), tiles.end(),
                    [&](const MomTile& a, const MomTile& c) { return width(a) > width(c); });
-  // Narrow tiles stream the most row bytes per DMMA (every tile stages
-  // whole rows): interleave them with wide ones so the L2 -> SM demand is
-  // spread over the launch instead of piling up at its end.  The last
-  // sixth keeps longest-first order for the tail.
+  // (CSB_TILE_ORDER_MIX=1 interleaves narrow tiles with wide ones to spread
+  // the L2 -> SM row traffic; measured neutral to -0.7% since 3-tile warps)
   {
-    static const bool plain = [] {
-      const char* e = std::getenv("CSB_TILE_ORDER_PLAIN");
+    static const bool mix = [] {
+      const char* e = std::getenv("CSB_TILE_ORDER_MIX");
       return e && e[0] == '1';
     }();
     const size_t nt = tiles.size(), keep = nt / 6;
-    if (!plain && nt > keep + 2) {
+    if (mix && nt > keep + 2) {
       std::vector<MomTile> mixed;
       mixed.reserve(nt);
       size_t lo = 0, hi = nt - keep;  // [lo, hi) interleaved from both ends
