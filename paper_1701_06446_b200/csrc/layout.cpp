@@ -283,21 +283,24 @@ void MomentPlan::build_dmma(int S_, int n_, int b_, const Layout& top, const Lay
         if (shard->owner(jp) != shard_index) continue;  // another shard's blocks
       }
       for (int k = 0; k < LM1; ++k) t[k] = pi[k];
-      for (int a = std::max(last, 8 * h); a < hi; a += 2) {
-        const bool two = a + 1 < hi;
+      // pairs (a, a + 1) start at even a (16-byte aligned column pairs: the
+      // producer loads x[a0], x[a0 + 1] with one LDS.128); when the first
+      // canonical a is odd, the pair's first slot is masked (hi is even)
+      const int a_lo = std::max(last, 8 * h);
+      for (int a = a_lo & ~1; a < hi; a += 2) {
         DmmaPair pr{};
         for (int k = 0; k < 6; ++k) pr.pidx[k] = pi[k];
         pr.a0 = static_cast<uint16_t>(a);
-        pr.a1 = static_cast<uint16_t>(two ? a + 1 : a);
+        pr.a1 = static_cast<uint16_t>(a + 1);
         pairs.push_back(pr);
-        t[LM1] = a;
-        rows.push_back(make_row(t, top, low));
-        if (two) {
-          t[LM1] = a + 1;
+        if (a >= a_lo) {
+          t[LM1] = a;
           rows.push_back(make_row(t, top, low));
         } else {
           rows.push_back(PrefixRow{});  // masked slot
         }
+        t[LM1] = a + 1;
+        rows.push_back(make_row(t, top, low));
       }
     }
     while (pairs.size() % 32) {  // pad the window's last row set

@@ -245,8 +245,9 @@ __device__ __forceinline__ void produce(const MomParams& P, const MomTile& tile,
       const double* xr = xst + (4 * t + q) * n;
 #pragma unroll
       for (int u = 0; u < LM1; ++u) xv[buf][q][u] = xr[pidx[u]];
-      xv[buf][q][LM1] = xr[a0];
-      xv[buf][q][LM1 + 1] = xr[a1];
+      const double2 xa = *reinterpret_cast<const double2*>(xr + a0);  // a1 == a0 + 1, a0 even
+      xv[buf][q][LM1] = xa.x;
+      xv[buf][q][LM1 + 1] = xa.y;
     }
   };
   // The row sums lag the products by one k4 step: the adds of the previous
