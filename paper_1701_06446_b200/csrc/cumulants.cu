@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.cuh"
 #include "ptx.cuh"
@@ -720,7 +721,10 @@ __global__ void __launch_bounds__(LOW2_THREADS, 8) moment_lower_side_kernel(cons
 constexpr int LOWT_THREADS = 256;
 constexpr int LOWT_MAXST = 8;
 
-template <int ST>
+// W > 1: a thread owns the W consecutive order-ST elements (pi, t0 .. t0 +
+// W - 1) of one prefix, so the prefix loads and products are shared (the
+// per-element chain is unchanged: acc += round(P x[t]), row order).
+template <int ST, int W>
 __global__ void __launch_bounds__(LOWT_THREADS + 32) moment_lower_tma_kernel(const Lower2Params P, int stages, int kr) {
   extern __shared__ __align__(128) double xs[];  // stages x kr x n
   __shared__ __align__(8) uint64_t full[LOWT_MAXST], empty[LOWT_MAXST];
@@ -770,13 +774,18 @@ __global__ void __launch_bounds__(LOWT_THREADS + 32) moment_lower_tma_kernel(con
 #pragma unroll
   for (int k = 0; k < NR; ++k) pidx[k] = NP > 0 ? T.pidx[k] : 0;
   const int col = T.t0;
+  const int cnt = live ? T.cnt : 0;
+  int cw[W];  // element columns, clamped to the row (entries w >= cnt are dropped)
+#pragma unroll
+  for (int w = 0; w < W; ++w) cw[w] = min(col + w, n - 1);
   bool rep[NR];
 #pragma unroll
   for (int k = 0; k < NR; ++k) rep[k] = NP > 0 && T.rep[k] != 0xffffffffu;
-  double res[2][1 + NR];
-  double acc[1 + NR];
+  constexpr int NA = W + NR;  // acc[0 .. W): the order-ST elements; acc[W + k]: prefix depth k + 1
+  double res[2][NA];
+  double acc[NA];
 #pragma unroll
-  for (int w = 0; w < 1 + NR; ++w) acc[w] = 0.0;
+  for (int w = 0; w < NA; ++w) acc[w] = 0.0;
   for (uint32_t c = 0; c < chunks; ++c) {
     const uint32_t st = c % stages;
     ptx::mbar_wait(full + st, (c / stages) & 1u);
@@ -790,15 +799,16 @@ __global__ void __launch_bounds__(LOWT_THREADS + 32) moment_lower_tma_kernel(con
 #pragma unroll
       for (int k = 0; k < NP; ++k) {
         pv = k == 0 ? x[pidx[0]] : __dmul_rn(pv, x[pidx[k]]);
-        if (rep[k]) acc[1 + k] = __dadd_rn(acc[1 + k], pv);
+        if (rep[k]) acc[W + k] = __dadd_rn(acc[W + k], pv);
       }
-      acc[0] = __dadd_rn(acc[0], NP > 0 ? __dmul_rn(pv, x[col]) : x[col]);
+#pragma unroll
+      for (int w = 0; w < W; ++w) acc[w] = __dadd_rn(acc[w], NP > 0 ? __dmul_rn(pv, x[cw[w]]) : x[cw[w]]);
     }
     __syncwarp();
     if ((threadIdx.x & 31) == 0) ptx::mbar_arrive(empty + st);
     if (c + 1 == cpp || c + 1 == chunks) {  // end of a pass
 #pragma unroll
-      for (int w = 0; w < 1 + NR; ++w) {
+      for (int w = 0; w < NA; ++w) {
         res[pass][w] = __dmul_rn(acc[w], P.inv);
         acc[w] = 0.0;
       }
@@ -806,14 +816,16 @@ __global__ void __launch_bounds__(LOWT_THREADS + 32) moment_lower_tma_kernel(con
   }
   if (!live) return;
   const bool update = P.npass == 2;
-  {
-    const double v = update ? __dsub_rn(res[0][0], res[1][0]) : res[0][0];
-    write_copies<ST>(P.m[ST - 1], P.elems[ST - 1][T.e0], n, P.b, update, P.c, v);
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    if (w >= cnt) break;
+    const double v = update ? __dsub_rn(res[0][w], res[1][w]) : res[0][w];
+    write_copies<ST>(P.m[ST - 1], P.elems[ST - 1][T.e0 + w], n, P.b, update, P.c, v);
   }
 #pragma unroll
   for (int k = 0; k < NP; ++k) {
     if (!rep[k]) continue;
-    const double v = update ? __dsub_rn(res[0][1 + k], res[1][1 + k]) : res[0][1 + k];
+    const double v = update ? __dsub_rn(res[0][W + k], res[1][W + k]) : res[0][W + k];
     switch (k) {
       case 0: write_copies<1>(P.m[0], P.elems[0][T.rep[0]], n, P.b, update, P.c, v); break;
       case 1: write_copies<(ST > 2 ? 2 : 1)>(P.m[1], P.elems[1][T.rep[1]], n, P.b, update, P.c, v); break;
@@ -825,23 +837,34 @@ __global__ void __launch_bounds__(LOWT_THREADS + 32) moment_lower_tma_kernel(con
 
 bool lower_tma_supported(const Lower2Params& p) { return p.n % 2 == 0 && p.n <= 4096; }
 
-void launch_moment_lower_tma(int ST, const Lower2Params& p, cudaStream_t st) {
+void launch_moment_lower_tma(int ST, int W, const Lower2Params& p, cudaStream_t st) {
   if (!p.nthreads) return;
   const unsigned g = (p.nthreads + LOWT_THREADS - 1) / LOWT_THREADS;
   const int kr = 32;
   const size_t stage_bytes = static_cast<size_t>(kr) * p.n * sizeof(double);
-  int stages = static_cast<int>(std::min<size_t>(LOWT_MAXST, (200u << 10) / stage_bytes));
+  // deep ring (up to 200 KB) unless the grid needs more than one CTA per SM
+  // to fit in one wave: then the stages that many CTAs per SM leave room for
+  static int sms = 0;
+  if (!sms) CSB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  const size_t per_sm = std::max<size_t>(1, (g + sms - 1) / static_cast<unsigned>(sms));
+  static const int forced = [] {  // CSB_LOWT_SMEM=KB per CTA (A/B)
+    const char* e = std::getenv("CSB_LOWT_SMEM");
+    return e ? std::atoi(e) : 0;
+  }();
+  const size_t budget = forced > 0 ? static_cast<size_t>(forced) << 10
+                                   : std::min<size_t>(200u << 10, (220u << 10) / std::min<size_t>(per_sm, 4));
+  int stages = static_cast<int>(std::min<size_t>(LOWT_MAXST, budget / stage_bytes));
   if (stages < 2) fail(CSB_EINVAL, "moment_lower_tma: rows too wide");
   const size_t sm = stages * stage_bytes;
-  switch (ST) {
-#define CSB_LOWT(SS)                                                                                          \
-  case SS:                                                                                                    \
-    ensure_smem(moment_lower_tma_kernel<SS>, sm);                                                     \
-    moment_lower_tma_kernel<SS><<<g, LOWT_THREADS + 32, sm, st>>>(p, stages, kr);                             \
+  switch (ST * 8 + W) {
+#define CSB_LOWT(SS, WW)                                                                                      \
+  case SS * 8 + WW:                                                                                           \
+    ensure_smem(moment_lower_tma_kernel<SS, WW>, sm);                                                         \
+    moment_lower_tma_kernel<SS, WW><<<g, LOWT_THREADS + 32, sm, st>>>(p, stages, kr);                         \
     break;
-    CSB_LOWT(1) CSB_LOWT(2) CSB_LOWT(3) CSB_LOWT(4)
+    CSB_LOWT(1, 1) CSB_LOWT(2, 1) CSB_LOWT(3, 1) CSB_LOWT(4, 1) CSB_LOWT(2, 4) CSB_LOWT(3, 4) CSB_LOWT(4, 4)
 #undef CSB_LOWT
-    default: fail(CSB_EINVAL, "moment_lower_tma: order out of range");
+    default: fail(CSB_EINVAL, "moment_lower_tma: order or width out of range");
   }
   CSB_CUDA(cudaGetLastError());
   count_launch();

@@ -127,7 +127,7 @@ void launch_moment_lower(int S, const LowerParams& p, cudaStream_t st);
 void launch_moment_lower2(int ST, int W, const Lower2Params& p, cudaStream_t st);
 // orders <= ST of few elements: one thread per element, TMA-staged rows
 bool lower_tma_supported(const Lower2Params& p);
-void launch_moment_lower_tma(int ST, const Lower2Params& p, cudaStream_t st);
+void launch_moment_lower_tma(int ST, int W, const Lower2Params& p, cudaStream_t st);
 void launch_moment_lower_side(int ST, const Lower2Params& p, cudaStream_t st);
 void launch_copy_c1(const double* m1, double* c1, double* partial, const LayoutDev& lay,
                     uint64_t nblocks, uint64_t stored, cudaStream_t st);

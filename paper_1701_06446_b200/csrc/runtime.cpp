@@ -628,14 +628,18 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
     };
     if (side) {
       CSB_CUDA(cudaEventRecord(dev.fork, st));  // the low orders depend only on work queued so far
-      side_launch = [&dev, ST, make_params, &side_tail, side_tail_ran]() {
-        const Lower2Params lp = make_params(1);
+      side_launch = [&dev, ST, make_params, &side_tail, side_tail_ran, m]() {
+        // many elements: a thread owns 4 consecutive ones (shared prefix work)
+        // (the TMA kernel only; same test as lower_tma_supported)
+        const bool tma = g_low_tma && m->n % 2 == 0 && m->n <= 4096;
+        const int W = tma && ST >= 2 && multiset_count(m->n, ST) > 60000 ? 4 : 1;
+        const Lower2Params lp = make_params(W);
         {
           std::lock_guard<std::mutex> lk(dev.mu);
           CSB_CUDA(cudaStreamWaitEvent(dev.side, dev.fork, 0));
           ProfScope pl("moment_low", dev.side);
-          if (g_low_tma && lower_tma_supported(lp))
-            launch_moment_lower_tma(ST, lp, dev.side);
+          if (tma && lower_tma_supported(lp))
+            launch_moment_lower_tma(ST, W, lp, dev.side);
           else
             launch_moment_lower_side(ST, lp, dev.side);
         }
