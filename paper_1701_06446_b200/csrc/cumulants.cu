@@ -90,8 +90,13 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
 
 // B: compile-time block size (0: runtime) -- full blocks then decode
 // positions and address factors with constant divisions and powers
+// Orders <= 4: registers capped (64) for 4 CTAs per SM -- the in-block
+// pass needs <= 56 KB of shared memory, so registers set the occupancy.
+#ifndef CSB_M2C_MINB4
+#define CSB_M2C_MINB4 4
+#endif
 template <int S, bool STAGED, int B>
-__global__ void __launch_bounds__(256, 2) moms2cums_v2(const M2CParams P) {
+__global__ void __launch_bounds__(256, (S <= 4 ? CSB_M2C_MINB4 : 2)) moms2cums_v2(const M2CParams P) {
   constexpr int NM = (1 << S) - 1;  // masks 1..NM-1: proper non-empty subsets
   extern __shared__ __align__(16) double sfac[];  // staged sub-blocks (STAGED)
   __shared__ uint64_t sbase[NM];                  // global (or smem) base per subset
