@@ -56,7 +56,7 @@ constexpr int THREADS = (CWARPS + PWARPS) * 32;
 #endif
 constexpr int MAXNC = CSB_MAXNC;          // column tiles per DMMA warp
 // Chunk geometry: HS k4 steps (4 HS data rows) per chunk, stage and A slot;
-// HS is a kernel template parameter (8, 6 or 4, whichever leaves >= 5 stages).
+// HS is a kernel template parameter (8, 6 or 4, whichever leaves >= 5 stages; 10 at n = 48, b = 4).
 constexpr int ASTRIDE = 8;                // doubles per (r, q) A-ring entry (swizzled, see apos)
 constexpr int ASLOTS = 2;                 // A-ring slots per row set
 template <int HS>
@@ -921,14 +921,19 @@ int stages_for(int n, int hs) {
   return s;
 }
 
-// the longest chunk that still leaves >= 5 stages (>= 2 at worst)
-int chunk_steps(int n) {
-  static const int forced = [] {  // CSB_HS=4|6|8 (experiments)
+// the longest chunk that still leaves >= 5 stages (>= 2 at worst); the
+// 10-step chunk (instantiated for cfg2's n = 48, b = 4 only) at >= 4 stages:
+// fewer chunk hand-offs per row beat the shallower ring there (cfg2 top
+// kernel 16.01 -> 15.79 ms, tools/gpu_hs10.sh)
+int chunk_steps(int n, int b) {
+  static const int forced = [] {  // CSB_HS=4|6|8|10 (experiments)
     const char* e = std::getenv("CSB_HS");
     return e ? std::atoi(e) : 0;
   }();
-  if (forced == 4 || forced == 6 || forced == 8)
+  const bool hs10 = n == 48 && b == 4;
+  if (forced == 4 || forced == 6 || forced == 8 || (forced == 10 && hs10))
     if (stages_for(n, forced) >= 2) return forced;
+  if (hs10 && stages_for(n, 10) >= 4) return 10;
   for (int hs : {8, 6, 4})
     if (stages_for(n, hs) >= 5) return hs;
   return 4;
@@ -963,7 +968,7 @@ void launch_mirror(int S, double* m, const LayoutDev& lay, const uint32_t* block
 void launch_moment_top_dmma(const MomParams& p_in, int ntiles, cudaStream_t st) {
   if (ntiles <= 0) return;
   MomParams p = p_in;
-  const int hs = chunk_steps(p.n);
+  const int hs = chunk_steps(p.n, p.b);
   p.stages = stages_for(p.n, hs);
   static const int ones4 = [] {  // CSB_ONES4=0..3: row-sum tile in R = 4 windows of <= k column tiles
     const char* e = std::getenv("CSB_ONES4");
@@ -983,6 +988,7 @@ void launch_moment_top_dmma(const MomParams& p_in, int ntiles, cudaStream_t st) 
   if (p.n == 96 && hs == 6 && p.b == 8) kern = moment_top_dmma_kernel<96, 6, 8>;
   else if (p.n == 96 && hs == 8 && p.b == 8) kern = moment_top_dmma_kernel<96, 8, 8>;
   else if (p.n == 48 && hs == 8 && p.b == 4) kern = moment_top_dmma_kernel<48, 8, 4>;
+  else if (p.n == 48 && hs == 10 && p.b == 4) kern = moment_top_dmma_kernel<48, 10, 4>;
   else if (p.n == 24 && hs == 8 && p.b == 3) kern = moment_top_dmma_kernel<24, 8, 3>;
   else if (p.n == 256 && hs == 4 && p.b == 16) kern = moment_top_dmma_kernel<256, 4, 16>;
   else if (hs == 8) kern = moment_top_dmma_kernel<0, 8, 0>;
