@@ -200,6 +200,7 @@ __global__ void __launch_bounds__(256, (S <= 4 ? CSB_M2C_MINB4 : 2)) moms2cums_v
     }
   }
 
+  double part = 0.0;  // this thread's share of the block's sum of squares
   // phase 1: canonical entries.  Full blocks (all extents b) walk the
   // precomputed canonical positions of their run pattern -- no lane idles
   // on the non-canonical copies of diagonal blocks -- and address a factor
@@ -209,8 +210,10 @@ __global__ void __launch_bounds__(256, (S <= 4 ? CSB_M2C_MINB4 : 2)) moms2cums_v
     uint32_t pat = 0;
 #pragma unroll
     for (int k = 1; k < S; ++k) pat |= static_cast<uint32_t>(j[k] == j[k - 1]) << (k - 1);
-    const uint32_t* list = P.canon + P.canon_off[pat];
-    const uint32_t cnt = P.canon_off[pat + 1] - P.canon_off[pat];
+    const uint32_t cbase = P.canon_off[pat];
+    const uint32_t* list = P.canon + cbase;
+    const uint32_t cnt = P.canon_off[pat + 1] - cbase;
+    const bool direct = !inblk && P.cstart;  // copies + norm term written here (no second pass)
     uint32_t bp[S];  // b^0 .. b^(S-1)
     bp[0] = 1;
 #pragma unroll
@@ -244,10 +247,17 @@ __global__ void __launch_bounds__(256, (S <= 4 ? CSB_M2C_MINB4 : 2)) moms2cums_v
         f[m] = sfac[(S <= 5 ? sb[m < NB ? m : 0] : static_cast<uint32_t>(sbase[m])) + a];
       }
       const double corr = partition_correction<S>(f);
-      if (inblk)
+      if (inblk) {
         cblk[pos] = __dsub_rn(cblk[pos], corr);
-      else
-        P.c[boff + pos] = __dsub_rn(P.m[boff + pos], corr);
+      } else {
+        const double v = __dsub_rn(P.m[boff + pos], corr);
+        P.c[boff + pos] = v;
+        if (direct) {
+          const uint32_t c0 = __ldg(P.cstart + cbase + i), c1 = __ldg(P.cstart + cbase + i + 1);
+          for (uint32_t q = c0; q < c1; ++q) P.c[boff + __ldg(P.cdst + q)] = v;
+          part = __fma_rn(static_cast<double>(1u + c1 - c0), __dmul_rn(v, v), part);
+        }
+      }
     }
   } else {
     for (uint32_t pos = threadIdx.x; pos < vol; pos += blockDim.x) {
@@ -273,7 +283,6 @@ __global__ void __launch_bounds__(256, (S <= 4 ? CSB_M2C_MINB4 : 2)) moms2cums_v
   __syncthreads();  // canonical entries of this block are visible to the CTA
 
   // phase 2: copies + the block's sum of squares (fixed order)
-  double part = 0.0;
   if (inblk) {
     uint32_t pat = 0;
 #pragma unroll
@@ -290,8 +299,9 @@ __global__ void __launch_bounds__(256, (S <= 4 ? CSB_M2C_MINB4 : 2)) moms2cums_v
       part = __fma_rn(v, v, part);
     }
   }
-  const bool listed = !inblk && STAGED && full && P.canon && P.mlist;
-  if (listed) {
+  const bool direct = !inblk && STAGED && full && P.canon && P.cstart;  // done in phase 1
+  const bool listed = !inblk && STAGED && full && P.canon && (P.mlist || direct);
+  if (listed && !direct) {
     // copies from the canonical entries this CTA just wrote (visible to the
     // block after the barrier above), then the sum of squares in order
     uint32_t pat = 0;

@@ -61,6 +61,11 @@ struct M2CParams {
   // (bit k-1: j_k == j_{k-1}): canon[canon_off[pat] .. canon_off[pat + 1])
   const uint32_t* canon = nullptr;
   const uint32_t* canon_off = nullptr;
+  // per canonical position (indexed like canon): its symmetric copies in the
+  // block, cdst[cstart[i] .. cstart[i + 1]) -- the out-of-block pass writes
+  // them and weights the norm term by 1 + copies right after computing it
+  const uint32_t* cstart = nullptr;
+  const uint32_t* cdst = nullptr;
   double* partial = nullptr;        // per block: sum over stored entries of v*v
 };
 

@@ -68,6 +68,7 @@ struct Device {
   std::map<std::tuple<int, int, int>, std::shared_ptr<DevBuf<uint64_t>>> subs;
   std::map<std::pair<int, int>, std::pair<std::shared_ptr<DevBuf<uint32_t>>, std::shared_ptr<DevBuf<uint32_t>>>> canon;
   std::map<std::pair<int, int>, std::pair<std::shared_ptr<DevBuf<uint2>>, std::shared_ptr<DevBuf<uint32_t>>>> mirror;
+  std::map<std::pair<int, int>, std::pair<std::shared_ptr<DevBuf<uint32_t>>, std::shared_ptr<DevBuf<uint32_t>>>> copies;
   std::map<std::tuple<int, int, int, int>, std::shared_ptr<ShardPlan>> shards;
   void* comm = nullptr;  // NCCL communicator (csb_comm_init)
   int nranks = 1, rank = 0;
@@ -368,6 +369,59 @@ std::pair<const uint2*, const uint32_t*> get_mirror_lists(Device& dev, int S, in
   return {slot.first->ptr, slot.second->ptr};
 }
 
+// Per canonical position of a full order-S block (indexed like get_canon's
+// lists, patterns concatenated): its symmetric copies, as CSR (start, dst).
+// The out-of-block moms2cums pass writes each copy and its norm term as
+// soon as the canonical value exists.  Built where the mirror lists are.
+std::pair<const uint32_t*, const uint32_t*> get_copy_lists(Device& dev, int S, int b) {
+  uint64_t vol = 1;
+  for (int k = 0; k < S; ++k) vol *= static_cast<uint64_t>(b);
+  const uint32_t npat = 1u << (S - 1);
+  if (vol * npat > (1ull << 20)) return {nullptr, nullptr};
+  std::lock_guard<std::mutex> lk(dev.mu);
+  auto& slot = dev.copies[{S, b}];
+  if (!slot.first) {
+    std::vector<uint32_t> start, dst;
+    std::vector<std::vector<uint32_t>> by_src(vol);
+    int o[kMaxOrder];
+    for (uint32_t pat = 0; pat < npat; ++pat) {
+      for (auto& v : by_src) v.clear();
+      std::vector<uint32_t> canon;
+      for (uint64_t pos = 0; pos < vol; ++pos) {
+        uint64_t rem = pos;
+        for (int k = S - 1; k >= 0; --k) {
+          o[k] = static_cast<int>(rem % static_cast<uint64_t>(b));
+          rem /= static_cast<uint64_t>(b);
+        }
+        bool canonical = true;
+        for (int k = 1; k < S; ++k)
+          if ((pat >> (k - 1) & 1) && o[k] < o[k - 1]) canonical = false;
+        if (canonical) {
+          canon.push_back(static_cast<uint32_t>(pos));
+          continue;
+        }
+        for (int pass = 0; pass < S - 1; ++pass)
+          for (int k = 1; k < S; ++k)
+            if ((pat >> (k - 1) & 1) && o[k] < o[k - 1]) std::swap(o[k], o[k - 1]);
+        uint64_t src = 0;
+        for (int k = 0; k < S; ++k) src = src * static_cast<uint64_t>(b) + static_cast<uint64_t>(o[k]);
+        by_src[src].push_back(static_cast<uint32_t>(pos));
+      }
+      for (uint32_t c : canon) {  // same order as get_canon's list for this pattern
+        start.push_back(static_cast<uint32_t>(dst.size()));
+        dst.insert(dst.end(), by_src[c].begin(), by_src[c].end());
+      }
+    }
+    start.push_back(static_cast<uint32_t>(dst.size()));
+    auto st = std::make_shared<DevBuf<uint32_t>>(start.size());
+    auto ds = std::make_shared<DevBuf<uint32_t>>(std::max<size_t>(1, dst.size()));
+    h2d_sync(st->ptr, start.data(), st->bytes());
+    if (!dst.empty()) h2d_sync(ds->ptr, dst.data(), dst.size() * sizeof(uint32_t));
+    slot = {st, ds};
+  }
+  return {slot.first->ptr, slot.second->ptr};
+}
+
 // Thread table of the staged low-order kernel for orders 1..ST: the
 // order-ST tuples in lexicographic order, cut into runs of <= W sharing
 // their (ST-1)-prefix pi; a prefix's first run also represents the tuples
@@ -524,6 +578,12 @@ const bool g_low_side = [] {
 const bool g_low_tma = [] {
   const char* e = std::getenv("CSB_LOW_KERNEL");
   return !(e && std::strcmp(e, "side") == 0);
+}();
+// CSB_M2C_DIRECT=0: moms2cums' out-of-block pass writes the copies and the
+// norm terms in a second pass over the block (A/B)
+const bool g_m2c_direct = [] {
+  const char* e = std::getenv("CSB_M2C_DIRECT");
+  return !(e && e[0] == '0');
 }();
 const bool g_low_defer = [] {
   const char* e = std::getenv("CSB_LOW_DEFER");
@@ -802,6 +862,11 @@ void run_moms2cums(const csb_series* m, csb_series* c, NormScratch& ns, cudaStre
         auto ml = get_mirror_lists(*m->dev, s, m->b);
         p.mlist = ml.first;
         p.mlist_off = ml.second;
+        if (g_m2c_direct) {
+          auto cp = get_copy_lists(*m->dev, s, m->b);
+          p.cstart = cp.first;
+          p.cdst = cp.second;
+        }
       }
     }
     if (m->mirror_defer >> (s - 1) & 1u) {
