@@ -90,18 +90,17 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
 
 // B: compile-time block size (0: runtime) -- full blocks then decode
 // positions and address factors with constant divisions and powers
-// Orders <= 4: registers capped (64) for 4 CTAs per SM -- the in-block
-// pass needs <= 56 KB of shared memory, so registers set the occupancy.
-#ifndef CSB_M2C_MINB4
-#define CSB_M2C_MINB4 4
-#endif
+// Orders <= 4: registers capped at 64 -- four 256-thread CTAs per SM for
+// the in-block pass (<= 56 KB of shared memory, so registers set the
+// occupancy), or one 1024-thread CTA beside large staged sub-blocks
+// (b = 16: 144 KB), whose global-memory latency then has 32 warps to hide it.
 template <int S, bool STAGED, int B>
-__global__ void __launch_bounds__(256, (S <= 4 ? CSB_M2C_MINB4 : 2)) moms2cums_v2(const M2CParams P) {
+__global__ void __launch_bounds__(S <= 4 ? 1024 : 256, S <= 4 ? 1 : 2) moms2cums_v2(const M2CParams P) {
   constexpr int NM = (1 << S) - 1;  // masks 1..NM-1: proper non-empty subsets
   extern __shared__ __align__(16) double sfac[];  // staged sub-blocks (STAGED)
   __shared__ uint64_t sbase[NM];                  // global (or smem) base per subset
   __shared__ uint32_t sstride[NM][S];
-  __shared__ double red[8];
+  __shared__ double red[32];
   __shared__ __align__(8) uint64_t mbar;  // TMA staging of a full block (even b)
   const uint64_t blk = P.blk0 + blockIdx.x;
   const LayoutDev& LS = P.lay[S - 1];
@@ -617,10 +616,16 @@ void launch_moms2cums_v2(int S, const M2CParams& p, uint64_t nblocks, cudaStream
     if (q.mfix) fail(CSB_ERUNTIME, "moms2cums: deferred mirror without an in-block pass");
   }
   const int bb = p.b < p.n ? p.b : p.n;
+  // big blocks outside shared memory: one wide CTA per SM (orders <= 4)
+  static const bool wide_ok = [] {  // CSB_M2C_WIDE=0: always 256 threads (A/B)
+    const char* e = std::getenv("CSB_M2C_WIDE");
+    return !(e && e[0] == '0');
+  }();
+  const unsigned threads = wide_ok && S <= 4 && staged && !q.inblk && vol >= 16384 ? 1024u : 256u;
   switch (S) {
 #define CSB_M2C_B(SS, BB)                                                                                  \
   ensure_smem(moms2cums_v2<SS, true, BB>, sm);                                                             \
-  moms2cums_v2<SS, true, BB><<<g, 256, sm, st>>>(q);
+  moms2cums_v2<SS, true, BB><<<g, threads, sm, st>>>(q);
 #define CSB_M2C(SS)                                                                                         \
   case SS:                                                                                                  \
     if (staged) {                                                                                           \

@@ -21,6 +21,7 @@ CASES = [  # (n, d, b, T, p, steps, seed)
     (130, 3, 16, 200, 50, 2, 12),  # > 16 column tiles: split column ranges, edge blocks
     (40, 6, 4, 24, 8, 2, 13),      # cfg2 geometry (order 6, R = 2 and 4 windows)
     (72, 5, 8, 40, 10, 1, 14),     # order 5, full and edge blocks
+    (48, 4, 16, 40, 10, 1, 16),    # cfg3 block size: 64K-entry blocks, 1024-thread moms2cums pass
 ]
 
 
