@@ -795,9 +795,10 @@ __global__ void __launch_bounds__(LOWT_THREADS + 32) moment_lower_tma_kernel(con
   for (int k = 0; k < NR; ++k) pidx[k] = NP > 0 ? T.pidx[k] : 0;
   const int col = T.t0;
   const int cnt = live ? T.cnt : 0;
+  const int stride = T.pad ? static_cast<int>(T.pad) : 1;  // strided tables: elements t0 + k * stride
   int cw[W];  // element columns, clamped to the row (entries w >= cnt are dropped)
 #pragma unroll
-  for (int w = 0; w < W; ++w) cw[w] = min(col + w, n - 1);
+  for (int w = 0; w < W; ++w) cw[w] = min(col + w * stride, n - 1);
   bool rep[NR];
 #pragma unroll
   for (int k = 0; k < NR; ++k) rep[k] = NP > 0 && T.rep[k] != 0xffffffffu;
@@ -840,7 +841,7 @@ __global__ void __launch_bounds__(LOWT_THREADS + 32) moment_lower_tma_kernel(con
   for (int w = 0; w < W; ++w) {
     if (w >= cnt) break;
     const double v = update ? __dsub_rn(res[0][w], res[1][w]) : res[0][w];
-    write_copies<ST>(P.m[ST - 1], P.elems[ST - 1][T.e0 + w], n, P.b, update, P.c, v);
+    write_copies<ST>(P.m[ST - 1], P.elems[ST - 1][T.e0 + w * stride], n, P.b, update, P.c, v);
   }
 #pragma unroll
   for (int k = 0; k < NP; ++k) {

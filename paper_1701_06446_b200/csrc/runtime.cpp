@@ -456,7 +456,31 @@ std::shared_ptr<DevBuf<LowerThread>> get_lower2_threads(Device& dev, int ST, int
       // t = (pi, t_ST) with t_ST = pi_last (or 0): the first tuple of pi
       const int np = ST - 1;
       const int first = np > 0 ? t[np - 1] : 0;
-      for (int t0 = first; t0 < n; t0 += W) {
+      if (W < 0) {
+        // strided: thread q of the prefix's nthr threads owns the elements
+        // t = first + q + k * nthr (k < -W), so the lanes of one prefix read
+        // consecutive columns of a staged row (no shared-memory bank
+        // conflicts between them); pad = the stride
+        const int m = n - first, nthr = (m - W - 1) / -W;
+        for (int q = 0; q < nthr; ++q) {
+          LowerThread lt{};
+          lt.e0 = id + static_cast<uint32_t>(q);
+          for (int k = 0; k < np; ++k) lt.pidx[k] = static_cast<uint16_t>(t[k]);
+          lt.t0 = static_cast<uint16_t>(first + q);
+          lt.cnt = static_cast<uint16_t>((m - q + nthr - 1) / nthr);
+          lt.pad = static_cast<uint32_t>(nthr);
+          for (int k = 0; k < 3; ++k) lt.rep[k] = 0xffffffffu;
+          if (q == 0)
+            for (int s = 1; s <= np; ++s) {
+              bool ok = true;
+              for (int k = s; k < np; ++k) ok &= t[k] == t[s - 1];
+              if (ok) lt.rep[s - 1] = ids.at(key(t, s));
+            }
+          v.push_back(lt);
+        }
+        id += static_cast<uint32_t>(m);
+      }
+      for (int t0 = first; W > 0 && t0 < n; t0 += W) {
         LowerThread lt{};
         lt.e0 = id;
         for (int k = 0; k < np; ++k) lt.pidx[k] = static_cast<uint16_t>(t[k]);
@@ -693,7 +717,11 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
         // (the TMA kernel only; same test as lower_tma_supported)
         const bool tma = g_low_tma && m->n % 2 == 0 && m->n <= 4096;
         const int W = tma && ST >= 2 && multiset_count(m->n, ST) > 60000 ? 4 : 1;
-        const Lower2Params lp = make_params(W);
+        static const bool strided = [] {  // CSB_LOWT_STRIDED=0: consecutive elements per thread (A/B)
+          const char* e = std::getenv("CSB_LOWT_STRIDED");
+          return !(e && e[0] == '0');
+        }();
+        const Lower2Params lp = make_params(W > 1 && strided ? -W : W);
         {
           std::lock_guard<std::mutex> lk(dev.mu);
           CSB_CUDA(cudaStreamWaitEvent(dev.side, dev.fork, 0));
