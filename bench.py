@@ -3,11 +3,18 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
-Workload: BASELINE.json configs[1] (d=4, n=96, b=8, T=20000, p=1000), the
-config the metric is quoted on that fits one GPU.  One step = one window
-update of the reference's `step()` (stream.cpp:85-108): exchange p rows,
-moments_update of M1..M4, moms2cums to C1..C4, and the window report with
-nu_3, nu_4 (the config's stated output) read back to the host.
+Workload (default): BASELINE.json configs[2] (d=6, n=48, b=4, T=50000,
+p=2000) -- BASELINE's metric names no config, so the largest config it does
+not assign to sharding: the order-6 update.  --config 0..4 selects another
+(cfg1 and cfg3 are the order-4 ones; cfg4 needs ~55 GB of HBM).  One step =
+one window update of the reference's `step()` (stream.cpp:85-108):
+exchange p rows, moments_update of M1..Md, moms2cums to C1..Cd, and the
+window report (nu_3..nu_d, the config's stated gauge) read back to the host.
+
+--gpus N (N > 1) without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks; every rank owns a block-prefix shard of
+M_d / C_d and exchanges over NCCL (allgather M_{d-1}, allreduce of the norm
+partials); value = window updates/s of the one sharded stream.
 
 value  = window updates/s with the incoming rows already resident in HBM
          (device timed with CUDA events on the engine's stream; L2 flushed
@@ -15,13 +22,15 @@ value  = window updates/s with the incoming rows already resident in HBM
 e2e    = the same through the C ABI with HOST buffers (csb_stream_step on
          pinned rows): H2D of the rows and D2H of the report inside the
          timed region.
-roofline = the order-4/3 moment kernel (moment_top): algorithmic flops per
+roofline = the order-d/d-1 moment kernel (moment_top): algorithmic flops per
          launch / its event-timed average duration, against the measured
          FP64 peak (profiles/fp64_peak.json; MEASURED_PEAKS.json has no FP64
          entry).
 cpu_baseline = the reference itself (oracle/_ref, compiled from
-         /root/reference) on the host cores: prime + 2 steps of the same
-         workload.
+         /root/reference) on the host cores: one step's two library calls
+         (moments_update + moms2cums, stream.cpp:85-108) at the config's
+         full size on a zero-initialised state (their cost does not depend
+         on the values), all host threads.
 
 --impl reference: the reference CPU library on the same workload, all host
 threads, rank 0 only.
@@ -135,31 +144,50 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_baseline_sample(cfg, gen_window, batches, steps: int = 2) -> dict | None:
-    """The reference library (oracle/_ref) on a bounded sample of the same
-    workload: prime + `steps` window updates, all host threads."""
+def cpu_model() -> str:
     try:
-        from oracle.oracle import Oracle, RefStream, ref_library_path
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baseline_sample(cfg, batch_in, batch_out) -> dict | None:
+    """The reference library (oracle/_ref) on a bounded sample of the same
+    workload: the two calls one step() makes (moments_update of M1..Md with
+    p rows in / p rows out, then moms2cums; stream.cpp:85-108) at full size
+    on a zero-initialised series -- prime skipped, its cost is T/p steps'
+    worth of accumulation and outside every step."""
+    try:
+        from oracle.oracle import Oracle, ref_library_path
     except Exception:
         return None
     if ref_library_path() is None:
         return None
     cores = os.cpu_count() or 1
     ref = Oracle("ref", workers=cores)
+    m = ref.alloc_series(cfg.n, cfg.d, cfg.b)
     t0 = time.perf_counter()
-    st = RefStream(ref, cfg.n, cfg.d, cfg.T, cfg.p, cfg.b, gen_window, resync_every=0)
-    t_prime = time.perf_counter() - t0
-    times = []
-    for k in range(steps):
-        t0 = time.perf_counter()
-        st.step(batches[k])
-        times.append(time.perf_counter() - t0)
-    st.close()
-    med = statistics.median(times)
-    return {"value": 1.0 / med, "unit": UNIT, "cores": cores, "kind": "reference",
-            "sample": f"{cfg.name}: prime ({t_prime:.1f} s) + {steps} step() calls of the reference "
-                      f"library (oracle/_ref, {os.path.basename(ref.path)}), median step {med:.3f} s",
-            "s_per_step": med}
+    ref.moments_update(m, cfg.T, batch_in, batch_out, cfg.b)
+    t1 = time.perf_counter()
+    ref.moms2cums(m, cfg.n, cfg.b, cfg.T)
+    t2 = time.perf_counter()
+    dt = t2 - t0
+    return {"value": 1.0 / dt, "unit": UNIT, "cores": cores, "kind": "reference",
+            "cpu": cpu_model(),
+            "sample": f"{cfg.name}: one step of the reference library (oracle/_ref, "
+                      f"{os.path.basename(ref.path)}, workers={cores}): moments_update {t1 - t0:.2f} s + "
+                      f"moms2cums {t2 - t1:.2f} s on a zero-initialised state",
+            "s_per_step": dt}
+
+
+def bench_config(cfg) -> dict:
+    """The workload, identical in both arms' lines."""
+    return {"workload": cfg.name, "d": cfg.d, "n": cfg.n, "b": cfg.b, "T": cfg.T, "p": cfg.p,
+            "l2": "GPU arm: 256 MB written between steps, outside the step events"}
 
 
 def run_reference_arm(args, cfg) -> None:
@@ -195,15 +223,28 @@ def run_reference_arm(args, cfg) -> None:
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": cfg.name, "d": cfg.d, "n": cfg.n, "b": cfg.b,
-                                         "T": cfg.T, "p": cfg.p},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+        "data": "synthetic", "config": bench_config(cfg),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "cpu": cpu_model(),
                          "sample": f"prime ({t_prime:.1f} s) + {args.warmup} warm-up + {args.steps} timed "
                                    f"step() calls of the unmodified reference library "
                                    f"({os.path.basename(ref.path)}, workers={cores})"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "last_report_nu": [float(rep[6]), float(rep[7])],
+        "last_report_nu": [float(v) for v in rep[6:6 + cfg.d - 2]],
     }))
+
+
+def relaunch_under_torchrun(args) -> None:
+    """--gpus N outside torchrun: one rank per GPU on this node."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd, env=env))
 
 
 def main() -> None:
@@ -212,11 +253,15 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     cfg = CONFIGS[args.config]
+
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args)
+        return
 
     if args.impl == "reference":
         run_reference_arm(args, cfg)
@@ -345,7 +390,7 @@ def main() -> None:
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_sample(cfg, window, batches[:2])
+        cpu = cpu_baseline_sample(cfg, batches[0], window[:cfg.p])
 
     if rank == 0:
         ms_per_step = 1e3 * dev_s / args.steps
@@ -353,11 +398,11 @@ def main() -> None:
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg.name, "d": cfg.d, "n": cfg.n, "b": cfg.b, "T": cfg.T, "p": cfg.p,
-                       "l2": "flushed between steps (256 MB write, outside the step events)",
-                       "parallelism": (f"block-prefix shards x{world} (NCCL allgather M_d-1, allreduce "
+            "config": bench_config(cfg),
+            "method": {"parallelism": (f"block-prefix shards x{world} (NCCL allgather M_d-1, allreduce "
                                        "norm partials)") if world > 1 else "single",
-                       "step": "exchange + moments_update(M1..M4) + moms2cums(C1..C4) + report(nu3, nu4)"},
+                       "step": f"exchange + moments_update(M1..M{cfg.d}) + moms2cums(C1..C{cfg.d}) + "
+                               f"report(nu3..nu{cfg.d})"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "kernel": f"moment_top_dmma_kernel (orders {cfg.d} and {cfg.d - 1}, FP64 DMMA)",
@@ -376,7 +421,7 @@ def main() -> None:
             "gpu_launches": launches,
             "clocks": clocks.summary(),
             "wall_s_timed_region": wall,
-            "last_report": {"window": rep["window"], "nu3": rep["nu"][3], "nu4": rep["nu"][4]},
+            "last_report": {"window": rep["window"], "nu": {str(k): v for k, v in rep["nu"].items()}},
             "cpu_baseline": cpu,
         }
         print(json.dumps(line))

@@ -80,6 +80,10 @@ int csb_series_device_ptr(const csb_series* s, int order, double** dev);
  * equal the stored size. */
 int csb_series_upload(csb_series* s, int order, const double* host, uint64_t count);
 int csb_series_download(const csb_series* s, int order, double* host, uint64_t count);
+/* host[i] = order's stored element at offsets[i] (block-storage offsets,
+ * SymTensor addressing): sampled reads of tensors too large to download. */
+int csb_series_gather(const csb_series* s, int order, const uint64_t* offsets, uint64_t count,
+                      double* host);
 
 /* ---- hot path, host buffers ------------------------------------------------ */
 /* moment_series (moments.hpp:52): M_1..M_d of x (rows x cols, row-major).
@@ -157,7 +161,12 @@ int csb_stream_destroy(csb_stream* st);
  * when report is non-NULL the window report of the new window is filled. */
 int csb_stream_step(csb_stream* st, const double* x, uint64_t rows, uint64_t cols,
                     csb_step_timing* timing, csb_report* report);
-/* Same as csb_stream_step with x already in device memory. */
+/* Same as csb_stream_step with x already in device memory.  The engine
+ * reads x_dev on its own stream (csb_stream_cuda_stream): the caller must
+ * order the writes that produced x_dev before that stream (e.g. record an
+ * event on the producing stream and cudaStreamWaitEvent the engine's), and
+ * must not overwrite x_dev until the engine's stream has passed this step
+ * (the call returns early when report and timing are NULL). */
 int csb_stream_step_dev(csb_stream* st, const double* x_dev, uint64_t rows, uint64_t cols,
                         csb_step_timing* timing, csb_report* report);
 /* Report of the current window (after prime: window 1). */
@@ -168,8 +177,9 @@ int csb_stream_cumulants(csb_stream* st, const csb_series** c);
 int csb_stream_window(const csb_stream* st, uint64_t* window);
 /* WindowBuffer::materialize (stream.hpp:47): window rows in arrival order. */
 int csb_stream_materialize(const csb_stream* st, double* host, uint64_t count);
-/* Per-block partial squared norms of the owned shard, for the multi-GPU
- * fixed-order norm reduction (collective C3). */
+/* Per-block partial squared norms (count = the order's block count).  For a
+ * sharded stream's order d these are already reduced over the ranks
+ * (collective C3), so every entry is valid and first_block is 0. */
 int csb_stream_norm_partials(csb_stream* st, int order, double* host, uint64_t count,
                              uint64_t* first_block);
 /* Device stream (cudaStream_t) the engine launches on, for interop. */
@@ -184,6 +194,25 @@ int csb_stream_cuda_stream(csb_stream* st, void** cuda_stream);
  * M_{d-1} and reduces the order-d norm partials / diagonal with NCCL. */
 int csb_comm_unique_id(unsigned char* out /* 128 bytes */);
 int csb_comm_init(int nranks, int rank, const unsigned char* id /* 128 bytes */);
+/* Caller-supplied collectives in place of NCCL (any transport).  Callbacks
+ * return 0 on success.  allgather_ranges: rank r owns buf[off[r], off[r] +
+ * cnt[r]) on entry; on return every rank holds every range.  allreduce_sum:
+ * elementwise sum over ranks, in place.  host_staged != 0: buf is host
+ * memory, offsets are relative to buf and cuda_stream is NULL (the engine
+ * drains its stream and copies around the call); host_staged == 0: buf is
+ * device memory and the callback must order its work on cuda_stream
+ * (a cudaStream_t).  The ops struct is copied; ctx must outlive the
+ * streams primed under it. */
+typedef struct {
+  void* ctx;
+  int host_staged;
+  int (*allgather_ranges)(void* ctx, double* buf, const uint64_t* off, const uint64_t* cnt, int nranks,
+                          void* cuda_stream);
+  int (*allreduce_sum)(void* ctx, double* buf, uint64_t count, void* cuda_stream);
+} csb_comm_ops;
+int csb_comm_init_ops(int nranks, int rank, const csb_comm_ops* ops);
+/* Releases this process's communicator; streams primed under it keep their
+ * reference until they are destroyed. */
 int csb_comm_destroy(void);
 /* Block and element range of one shard: which = 0 for order d, 1 for d-1. */
 int csb_shard_range(int max_order, int dim, int block, int shard_index, int shard_count, int which,
@@ -198,6 +227,9 @@ int csb_moms2cums_shard(const csb_series* m, csb_series* c, int shard_index, int
 /* ---- instrumentation (bench.py) ------------------------------------------ */
 /* Kernels launched by this library so far in this process. */
 uint64_t csb_launch_count(void);
+/* Name of the kernel (template instantiation) that computes orders d and
+ * d-1 of a window update for this shape, given 16-byte aligned rows. */
+int csb_top_kernel(int dim, int max_order, int block, char* out, uint64_t cap);
 /* When enabled, CUDA events bracket every kernel launch on its own stream,
  * grouped by tag: "moment_top" (the order-d/d-1 pair kernel), "moment_low"
  * (lower pairs), "moms2cums", "norms". */

@@ -1,7 +1,7 @@
 /*
  * TEST INFRASTRUCTURE ONLY — the CPU oracle.  Never linked into the product.
  *
- * A plain-C, single-threaded restatement of the reference algorithm for the
+ * A plain-C restatement of the reference algorithm for the
  * hot path (sliding-window moment update -> moments-to-cumulants -> norms),
  * written from the reference's behaviour, not copied from it.  Each function
  * cites the reference file:line it restates (paths under
@@ -13,6 +13,10 @@
  * compiler's own contraction choices.  tests/test_oracle.py pins this port
  * against the reference itself (oracle/_ref) and the committed golden
  * vectors under tests/golden/.
+ *
+ * Threads (OpenMP) only split work by output element -- the pyramid by
+ * leading index like the reference's workers, moms2cums by block -- so
+ * every element's arithmetic is the single-threaded sequence.
  *
  * Parity pinned: yes (bitwise against oracle/_ref and tests/golden).
  */
@@ -185,17 +189,26 @@ static void descend(const double* row, int n, int d, int level, int lo, int hi, 
   }
 }
 
-/* accumulate<WriteAll>, moments.cpp:122-151 (single worker: the split never
- * changes a bit, README.md:69-71) */
+/* accumulate<WriteAll>, moments.cpp:122-151.  Workers split the pyramid by
+ * leading index (split_leading, moments.cpp:76-101): each owns every
+ * element whose first index is i0 and walks all rows in order, so every
+ * element sees exactly the single-worker arithmetic (the split never
+ * changes a bit, README.md:69-71). */
 static void accumulate(double** acc, int n, int d, const double* x, size_t rows, int write_all) {
-  size_t pos[OC_MAX_ORDER];
-  for (size_t r = 0; r < rows; ++r) {
-    const double* row = x + r * (size_t)n;
-    memset(pos, 0, sizeof(pos));
-    if (d == 1) {
-      for (int i = 0; i < n; ++i) acc[0][i] += row[i];
-    } else {
-      descend(row, n, d, 0, 0, n, 1.0, acc, pos, write_all);
+  if (d == 1) {
+    for (size_t r = 0; r < rows; ++r)
+      for (int i = 0; i < n; ++i) acc[0][i] += x[r * (size_t)n + i];
+  } else {
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int i0 = 0; i0 < n; ++i0) {
+      size_t start[OC_MAX_ORDER], pos[OC_MAX_ORDER];
+      /* tuples of order k+1 with first index < i0 precede i0's */
+      for (int k = 0; k < d; ++k)
+        start[k] = (size_t)(multiset_count(n, k + 1) - multiset_count(n - i0, k + 1));
+      for (size_t r = 0; r < rows; ++r) {
+        memcpy(pos, start, sizeof(size_t) * (size_t)d);
+        descend(x + r * (size_t)n, n, d, 0, i0, i0 + 1, 1.0, acc, pos, write_all);
+      }
     }
   }
   const double inv = 1.0 / (double)rows;
@@ -422,8 +435,9 @@ int oc_moms2cums(const double* const* m, double* const* c, int n, int d, int b) 
     double* data = c[s - 1];
     memcpy(data, m[s - 1], L->stored * sizeof(double));
     oc_packed pk = pack_corrections(s);
-    int o[OC_MAX_ORDER], idx[OC_MAX_ORDER], so[OC_MAX_ORDER];
+#pragma omp parallel for schedule(dynamic, 16)
     for (size_t r = 0; r < L->nblocks; ++r) {
+      int o[OC_MAX_ORDER], idx[OC_MAX_ORDER], so[OC_MAX_ORDER];
       const int* jx = L->index + r * s;
       const int* e = L->ext + r * s;
       double* blk = data + L->offset[r];
@@ -587,4 +601,110 @@ double oc_sample_moment(const double* x, size_t rows, size_t cols, const int* id
     acc += p;
   }
   return (double)(acc / (long double)rows);
+}
+
+/* ---------------------------------------------------------------------- */
+/* Exact sampled-element oracle (for configs too large to run
+ * the full CPU pipeline).  Unlike oc_sample_moment these reproduce the
+ * reference's per-element arithmetic bit for bit, so the GPU's stored values
+ * can be checked exactly at full size on a sample of elements. */
+
+/* Means of a tile of canonical elements over rows [r0, r0 + rows): for each
+ * element the descent of moments.cpp:40-57 -- prefix product from 1.0 left
+ * to right, then at the top order of the pyramid the contracted multiply-add
+ * out = fma(q, x[i_s], out) (moments.cpp:47), at every lower order the plain
+ * add of the full product (moments.cpp:44,55-57) -- in row order, then the
+ * reciprocal scaling of moments.cpp:148-150.  Rows are the outer loop so a
+ * tile of elements shares each row's reads. */
+#define OC_TILE 256
+static void sample_means_exact(const double* x, size_t r0, size_t rows, int n, const int* idx, int s, int top,
+                               size_t ne, double* out) {
+  double acc[OC_TILE];
+  for (size_t e = 0; e < ne; ++e) acc[e] = 0.0;
+  for (size_t r = r0; r < r0 + rows; ++r) {
+    const double* row = x + r * (size_t)n;
+    for (size_t e = 0; e < ne; ++e) {
+      const int* ix = idx + e * (size_t)s;
+      double q = 1.0;
+      if (top && s >= 2) {
+        for (int k = 0; k < s - 1; ++k) q = q * row[ix[k]];
+        acc[e] = fma(q, row[ix[s - 1]], acc[e]);
+      } else {
+        for (int k = 0; k < s; ++k) q = q * row[ix[k]];
+        acc[e] += q;
+      }
+    }
+  }
+  const double inv = 1.0 / (double)rows;
+  for (size_t e = 0; e < ne; ++e) out[e] = acc[e] * inv;
+}
+
+/* Value of canonical elements idx[count][s] of M_s after prime over rows
+ * [0, T) of x (rows in arrival order) and `steps` window updates of p rows
+ * (step k: incoming rows [T + k p, T + (k+1) p), outgoing [k p, (k+1) p);
+ * stream.cpp:85-108 with resync disabled): moment_series, then
+ * M = fma(p/T, a - b, M) per update (moments.cpp:287,297).  top != 0 when
+ * s is the series' max_order d. */
+int oc_sample_stream_moments(const double* x, int n, size_t T, size_t p, int steps, int s, int top,
+                             const int* idx, size_t count, double* out) {
+  if (s < 1 || s > OC_MAX_ORDER || p < 1 || p > T) return 1;
+  const double c = (double)p / (double)T;
+  const long ntiles = (long)((count + OC_TILE - 1) / OC_TILE);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (long t = 0; t < ntiles; ++t) {
+    const size_t e0 = (size_t)t * OC_TILE;
+    const size_t ne = count - e0 < OC_TILE ? count - e0 : OC_TILE;
+    const int* ix = idx + e0 * (size_t)s;
+    double m[OC_TILE], a[OC_TILE], b[OC_TILE];
+    sample_means_exact(x, 0, T, n, ix, s, top, ne, m);
+    for (int k = 0; k < steps; ++k) {
+      sample_means_exact(x, T + (size_t)k * p, p, n, ix, s, top, ne, a);
+      sample_means_exact(x, (size_t)k * p, p, n, ix, s, top, ne, b);
+      for (size_t e = 0; e < ne; ++e) m[e] = fma(c, a[e] - b[e], m[e]);
+    }
+    for (size_t e = 0; e < ne; ++e) out[e0 + e] = m[e];
+  }
+  return 0;
+}
+
+/* Stored offsets of sorted element indices idx[count][order] in the block
+ * layout (at_sorted_unchecked addressing, symten.cpp:171-181). */
+int oc_element_offsets(int order, int n, int b, const int* idx, size_t count, uint64_t* out) {
+  oc_layout L;
+  if (layout_init(&L, order, n, b)) return 1;
+  for (size_t e = 0; e < count; ++e) {
+    const int* ix = idx + e * (size_t)order;
+    int j[OC_MAX_ORDER];
+    for (int k = 0; k < order; ++k) j[k] = ix[k] / b;
+    const size_t r = (size_t)ranker_rank(&L.ranker, j);
+    const int* ex = L.ext + r * order;
+    size_t off = 0;
+    for (int k = 0; k < order; ++k) off = off * (size_t)ex[k] + (size_t)(ix[k] - j[k] * b);
+    out[e] = (uint64_t)(L.offset[r] + off);
+  }
+  layout_free(&L);
+  return 0;
+}
+
+/* C_s at sorted element indices from M_s's values there and the complete
+ * lower cumulants C_1..C_{s-1} (block storage): C = M - correction_sorted
+ * (cumulants.cpp:64-82,171). */
+int oc_sample_cumulants(const double* const* c_lower, int n, int b, int s, const int* idx, const double* m_val,
+                        size_t count, double* out) {
+  if (s < 2 || s > 16) return 1;
+  oc_layout* lay[OC_MAX_ORDER];
+  for (int k = 1; k < s; ++k) {
+    lay[k - 1] = (oc_layout*)malloc(sizeof(oc_layout));
+    if (layout_init(lay[k - 1], k, n, b)) return 1;
+  }
+  oc_packed pk = pack_corrections(s);
+#pragma omp parallel for schedule(static)
+  for (size_t e = 0; e < count; ++e)
+    out[e] = m_val[e] - correction_sorted(idx + e * (size_t)s, &pk, lay, c_lower);
+  free(pk.stream);
+  for (int k = 1; k < s; ++k) {
+    layout_free(lay[k - 1]);
+    free(lay[k - 1]);
+  }
+  return 0;
 }

@@ -199,6 +199,42 @@ class Oracle:
             out.append(parts)
         return out
 
+    # -- exact sampled-element oracle (port only) ---------------------------
+    def sample_stream_moments(self, x: np.ndarray, T: int, p: int, steps: int, s: int, top: bool,
+                              idx: np.ndarray) -> np.ndarray:
+        """Exact M_s at sorted canonical indices idx (count x s) after prime
+        over x[:T] and `steps` updates of p rows (rows in arrival order)."""
+        assert self.backend == "port"
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        idx = np.ascontiguousarray(idx, dtype=np.int32)
+        out = np.empty(idx.shape[0])
+        f = self._fn("sample_stream_moments", [_dp, C.c_int, _sz, _sz, C.c_int, C.c_int, C.c_int, _ip, _sz, _dp])
+        self._check(f(_dptr(x), x.shape[1], T, p, steps, s, 1 if top else 0,
+                      idx.ctypes.data_as(_ip), idx.shape[0], _dptr(out)), "sample_stream_moments")
+        return out
+
+    def element_offsets(self, order: int, n: int, b: int, idx: np.ndarray) -> np.ndarray:
+        """Stored offsets of sorted indices idx (count x order) in block storage."""
+        assert self.backend == "port"
+        idx = np.ascontiguousarray(idx, dtype=np.int32)
+        out = np.empty(idx.shape[0], dtype=np.uint64)
+        f = self._fn("element_offsets", [C.c_int, C.c_int, C.c_int, _ip, _sz, C.POINTER(_u64)])
+        self._check(f(order, n, b, idx.ctypes.data_as(_ip), idx.shape[0], out.ctypes.data_as(C.POINTER(_u64))),
+                    "element_offsets")
+        return out
+
+    def sample_cumulants(self, c_lower: Sequence[np.ndarray], n: int, b: int, s: int, idx: np.ndarray,
+                         m_val: np.ndarray) -> np.ndarray:
+        """Exact C_s at sorted indices from M_s's values there and C_1..C_{s-1}."""
+        assert self.backend == "port"
+        idx = np.ascontiguousarray(idx, dtype=np.int32)
+        m_val = np.ascontiguousarray(m_val, dtype=np.float64)
+        out = np.empty(idx.shape[0])
+        f = self._fn("sample_cumulants", [C.POINTER(_dp), C.c_int, C.c_int, C.c_int, _ip, _dp, _sz, _dp])
+        self._check(f(_ptrs(list(c_lower)), n, b, s, idx.ctypes.data_as(_ip), _dptr(m_val), idx.shape[0],
+                      _dptr(out)), "sample_cumulants")
+        return out
+
 
 class RefStream:
     """cumstream::prime/step (stream.hpp:69,73) on the reference backend."""

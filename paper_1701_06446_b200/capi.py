@@ -67,6 +67,15 @@ class StreamConfig(C.Structure):
                 ("workers", C.c_int), ("shard_index", C.c_int), ("shard_count", C.c_int)]
 
 
+_AllgatherFn = C.CFUNCTYPE(C.c_int, C.c_void_p, _dp, C.POINTER(_u64), C.POINTER(_u64), C.c_int, C.c_void_p)
+_AllreduceFn = C.CFUNCTYPE(C.c_int, C.c_void_p, _dp, _u64, C.c_void_p)
+
+
+class CommOps(C.Structure):
+    _fields_ = [("ctx", C.c_void_p), ("host_staged", C.c_int), ("allgather_ranges", _AllgatherFn),
+                ("allreduce_sum", _AllreduceFn)]
+
+
 class StepTiming(C.Structure):
     _fields_ = [("update_s", C.c_double), ("moms2cums_s", C.c_double)]
 
@@ -105,6 +114,7 @@ def lib() -> C.CDLL:
             "csb_series_device_ptr": ([C.c_void_p, C.c_int, C.POINTER(C.c_void_p)], C.c_int),
             "csb_series_upload": ([C.c_void_p, C.c_int, _dp, _u64], C.c_int),
             "csb_series_download": ([C.c_void_p, C.c_int, _dp, _u64], C.c_int),
+            "csb_series_gather": ([C.c_void_p, C.c_int, C.POINTER(_u64), _u64, _dp], C.c_int),
             "csb_moment_series": ([C.c_void_p, _dp, _u64, _u64], C.c_int),
             "csb_moment_tensor": ([C.c_void_p, C.c_int, _dp, _u64, _u64], C.c_int),
             "csb_moments_update": ([C.c_void_p, _dp, _dp, _u64, _u64], C.c_int),
@@ -129,12 +139,14 @@ def lib() -> C.CDLL:
             "csb_stream_cuda_stream": ([C.c_void_p, C.POINTER(C.c_void_p)], C.c_int),
             "csb_comm_unique_id": ([C.c_char_p], C.c_int),
             "csb_comm_init": ([C.c_int, C.c_int, C.c_char_p], C.c_int),
+            "csb_comm_init_ops": ([C.c_int, C.c_int, C.POINTER(CommOps)], C.c_int),
             "csb_comm_destroy": ([], C.c_int),
             "csb_shard_range": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(_u64),
                                  C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64)], C.c_int),
             "csb_moments_update_shard": ([C.c_void_p, _dp, _dp, _u64, _u64, C.c_int, C.c_int], C.c_int),
             "csb_moms2cums_shard": ([C.c_void_p, C.c_void_p, C.c_int, C.c_int], C.c_int),
             "csb_launch_count": ([], _u64),
+            "csb_top_kernel": ([C.c_int, C.c_int, C.c_int, C.c_char_p, _u64], C.c_int),
             "csb_profile_enable": ([C.c_int], C.c_int),
             "csb_profile_read": ([C.c_char_p, C.POINTER(C.c_double), C.POINTER(_u64)], C.c_int),
         }
@@ -171,6 +183,13 @@ def launch_count() -> int:
     return int(lib().csb_launch_count())
 
 
+def top_kernel(dim: int, max_order: int, block: int) -> str:
+    """The kernel instantiation that updates orders d and d-1 for this shape."""
+    buf = C.create_string_buffer(128)
+    check(lib().csb_top_kernel(dim, max_order, block, buf, 128))
+    return buf.value.decode()
+
+
 def profile_enable(on: bool = True) -> None:
     check(lib().csb_profile_enable(1 if on else 0))
 
@@ -197,6 +216,76 @@ def comm_unique_id() -> bytes:
 
 def comm_init(nranks: int, rank: int, uid: bytes) -> None:
     check(lib().csb_comm_init(nranks, rank, uid))
+
+
+def comm_destroy() -> None:
+    check(lib().csb_comm_destroy())
+
+
+_comm_keepalive: list = []
+
+
+def comm_init_host(nranks: int, rank: int, allgather_ranges, allreduce_sum) -> None:
+    """Caller-supplied collectives over HOST buffers (csb_comm_init_ops with
+    host_staged = 1).  allgather_ranges(buf, off, cnt): rank r owns
+    buf[off[r]:off[r]+cnt[r]] on entry, every rank holds all ranges on
+    return; allreduce_sum(buf): elementwise sum over ranks, in place.  buf
+    is a float64 numpy view of the engine's pinned staging buffer."""
+
+    def ag(_ctx, buf, off, cnt, n, _stream):
+        try:
+            o = [int(off[i]) for i in range(n)]
+            k = [int(cnt[i]) for i in range(n)]
+            size = max((a + b for a, b in zip(o, k)), default=0)
+            allgather_ranges(np.ctypeslib.as_array(buf, shape=(size,)), o, k)
+            return 0
+        except Exception:  # noqa: BLE001 -- reported through the status code
+            import traceback
+            traceback.print_exc()
+            return 1
+
+    def ar(_ctx, buf, count, _stream):
+        try:
+            allreduce_sum(np.ctypeslib.as_array(buf, shape=(int(count),)))
+            return 0
+        except Exception:  # noqa: BLE001
+            import traceback
+            traceback.print_exc()
+            return 1
+
+    ops = CommOps(None, 1, _AllgatherFn(ag), _AllreduceFn(ar))
+    _comm_keepalive.append(ops)  # the library keeps the function pointers
+    check(lib().csb_comm_init_ops(nranks, rank, C.byref(ops)))
+
+
+def comm_init_torch(group=None) -> None:
+    """Host-staged collectives over a torch.distributed process group (gloo
+    on CPU): ranges by one broadcast per owner, sums by all_reduce."""
+    import torch
+    import torch.distributed as dist
+
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+
+    def allgather_ranges(buf, off, cnt):
+        t = torch.from_numpy(buf)
+        for r in range(world):
+            if cnt[r]:
+                seg = t[off[r]: off[r] + cnt[r]].clone()
+                dist.broadcast(seg, src=r, group=group)
+                t[off[r]: off[r] + cnt[r]] = seg
+
+    def allreduce_sum(buf):
+        t = torch.from_numpy(buf)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+
+    comm_init_host(world, rank, allgather_ranges, allreduce_sum)
+
+
+def _gather(h, order: int, offsets: np.ndarray) -> np.ndarray:
+    off = np.ascontiguousarray(offsets, dtype=np.uint64)
+    out = np.empty(off.size)
+    check(lib().csb_series_gather(h, order, off.ctypes.data_as(C.POINTER(_u64)), off.size, _dptr(out)))
+    return out
 
 
 class Series:
@@ -247,6 +336,9 @@ class Series:
         out = np.empty(self.stored(order))
         check(lib().csb_series_download(self.h, order, _dptr(out), out.size))
         return out
+
+    def gather(self, order: int, offsets: np.ndarray) -> np.ndarray:
+        return _gather(self.h, order, offsets)
 
     def tensors(self) -> list[np.ndarray]:
         return [self.download(s) for s in range(1, self.max_order + 1)]
@@ -379,6 +471,24 @@ class Stream:
 
     def moments(self) -> list[np.ndarray]:
         return self._series(lib().csb_stream_moments)
+
+    def _handle(self, which: str):
+        p = C.c_void_p()
+        check((lib().csb_stream_moments if which == "M" else lib().csb_stream_cumulants)(self.h, C.byref(p)))
+        return p
+
+    def gather(self, which: str, order: int, offsets: np.ndarray) -> np.ndarray:
+        """Sampled stored elements of M_order (which="M") or C_order ("C")."""
+        return _gather(self._handle(which), order, offsets)
+
+    def download(self, which: str, order: int) -> np.ndarray:
+        """One whole stored tensor, M_order (which="M") or C_order ("C")."""
+        p = self._handle(which)
+        st = _u64()
+        check(lib().csb_series_stored(p, order, C.byref(st)))
+        a = np.empty(st.value)
+        check(lib().csb_series_download(p, order, _dptr(a), a.size))
+        return a
 
     def cumulants(self) -> list[np.ndarray]:
         return self._series(lib().csb_stream_cumulants)

@@ -32,17 +32,6 @@ namespace {
 
 __device__ __forceinline__ int ext_of(int j, int n, int b) { return b < n - j * b ? b : n - j * b; }
 
-__device__ __forceinline__ uint64_t rank_dev(const LayoutDev& L, const int* j, int order) {
-  uint64_t acc = 0;
-  int lo = 0;
-  for (int i = 0; i < order; ++i) {
-    const int rem = order - 1 - i;
-    acc += L.prefix[static_cast<size_t>(rem) * (L.grid + 1) + j[i]] -
-           L.prefix[static_cast<size_t>(rem) * (L.grid + 1) + lo];
-    lo = j[i];
-  }
-  return acc;
-}
 
 constexpr int popcount_c(int m) { return m == 0 ? 0 : (m & 1) + popcount_c(m >> 1); }
 
@@ -617,11 +606,7 @@ void launch_moms2cums_v2(int S, const M2CParams& p, uint64_t nblocks, cudaStream
   }
   const int bb = p.b < p.n ? p.b : p.n;
   // big blocks outside shared memory: one wide CTA per SM (orders <= 4)
-  static const bool wide_ok = [] {  // CSB_M2C_WIDE=0: always 256 threads (A/B)
-    const char* e = std::getenv("CSB_M2C_WIDE");
-    return !(e && e[0] == '0');
-  }();
-  const unsigned threads = wide_ok && S <= 4 && staged && !q.inblk && vol >= 16384 ? 1024u : 256u;
+  const unsigned threads = S <= 4 && staged && !q.inblk && vol >= 16384 ? 1024u : 256u;
   switch (S) {
 #define CSB_M2C_B(SS, BB)                                                                                  \
   ensure_smem(moms2cums_v2<SS, true, BB>, sm);                                                             \
@@ -856,7 +841,9 @@ __global__ void __launch_bounds__(LOWT_THREADS + 32) moment_lower_tma_kernel(con
   }
 }
 
-bool lower_tma_supported(const Lower2Params& p) { return p.n % 2 == 0 && p.n <= 4096; }
+bool lower_tma_supported(const Lower2Params& p) {
+  return p.n % 2 == 0 && p.n <= 4096 && rows_aligned16(p.src, p.npass);
+}
 
 void launch_moment_lower_tma(int ST, int W, const Lower2Params& p, cudaStream_t st) {
   if (!p.nthreads) return;
@@ -868,12 +855,7 @@ void launch_moment_lower_tma(int ST, int W, const Lower2Params& p, cudaStream_t 
   static int sms = 0;
   if (!sms) CSB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   const size_t per_sm = std::max<size_t>(1, (g + sms - 1) / static_cast<unsigned>(sms));
-  static const int forced = [] {  // CSB_LOWT_SMEM=KB per CTA (A/B)
-    const char* e = std::getenv("CSB_LOWT_SMEM");
-    return e ? std::atoi(e) : 0;
-  }();
-  const size_t budget = forced > 0 ? static_cast<size_t>(forced) << 10
-                                   : std::min<size_t>(200u << 10, (220u << 10) / std::min<size_t>(per_sm, 4));
+  const size_t budget = std::min<size_t>(200u << 10, (220u << 10) / std::min<size_t>(per_sm, 4));
   int stages = static_cast<int>(std::min<size_t>(LOWT_MAXST, budget / stage_bytes));
   if (stages < 2) fail(CSB_EINVAL, "moment_lower_tma: rows too wide");
   const size_t sm = stages * stage_bytes;

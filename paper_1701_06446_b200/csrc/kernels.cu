@@ -294,98 +294,6 @@ __global__ void __launch_bounds__(T, 1) moment_pair_kernel(const MomParams P) {
   }
 }
 
-// ---------------------------------------------------------------------------
-// moms2cums for order S (cumulants.cpp:128-196): one CTA per stored block.
-__device__ __forceinline__ uint64_t rank_dev(const LayoutDev& L, const int* j, int order) {
-  uint64_t acc = 0;
-  int lo = 0;
-  for (int i = 0; i < order; ++i) {
-    const int rem = order - 1 - i;
-    acc += L.prefix[static_cast<size_t>(rem) * (L.grid + 1) + j[i]] -
-           L.prefix[static_cast<size_t>(rem) * (L.grid + 1) + lo];
-    lo = j[i];
-  }
-  return acc;
-}
-
-constexpr int popcount_c(int m) { return m == 0 ? 0 : (m & 1) + popcount_c(m >> 1); }
-
-template <int S>
-__global__ void __launch_bounds__(256) moms2cums_kernel(const M2CParams P) {
-  constexpr int NM = (1 << S) - 1;  // masks 1..NM-1 are the proper subsets
-  __shared__ uint64_t sbase[NM];
-  __shared__ uint32_t sstride[NM][S];
-  __shared__ double red[8];
-  const uint64_t blk = P.blk0 + blockIdx.x;
-  const LayoutDev& LS = P.lay[S - 1];
-  const int n = P.n, b = P.b;
-  int j[S], e[S];
-#pragma unroll
-  for (int k = 0; k < S; ++k) {
-    j[k] = LS.index[blk * S + k];
-    e[k] = ext_of(j[k], n, b);
-  }
-  const uint64_t boff = LS.offset[blk];
-  const uint64_t vol = LS.offset[blk + 1] - boff;
-  for (int m = 1 + threadIdx.x; m < NM; m += blockDim.x) {
-    int sub[S], cnt = 0;
-    for (int k = 0; k < S; ++k)
-      if (m >> k & 1) sub[cnt++] = j[k];
-    const LayoutDev& Lq = P.lay[cnt - 1];
-    sbase[m] = Lq.offset[rank_dev(Lq, sub, cnt)];
-    // Horner strides of the sub-block (C order over the positions in m)
-    uint32_t stride = 1;
-    for (int k = S - 1; k >= 0; --k) {
-      if (m >> k & 1) {
-        sstride[m][k] = stride;
-        stride *= static_cast<uint32_t>(e[k]);
-      } else {
-        sstride[m][k] = 0;
-      }
-    }
-  }
-  __syncthreads();
-
-  double part = 0.0;
-  for (uint64_t pos = threadIdx.x; pos < vol; pos += blockDim.x) {
-    int o[S];
-    uint64_t rem = pos;
-#pragma unroll
-    for (int k = S - 1; k >= 0; --k) {
-      o[k] = static_cast<int>(rem % e[k]);
-      rem /= e[k];
-    }
-    bool canonical = true;
-#pragma unroll
-    for (int k = 1; k < S; ++k)
-      if (j[k] == j[k - 1] && o[k] < o[k - 1]) canonical = false;
-    if (!canonical) continue;
-    double f[NM];
-#pragma unroll
-    for (int m = 1; m < NM; ++m) {
-      uint64_t a = sbase[m];
-#pragma unroll
-      for (int k = 0; k < S; ++k)
-        if (m >> k & 1) a += static_cast<uint64_t>(o[k]) * sstride[m][k];
-      f[m] = P.lower[popcount_c(m) - 1][a];
-    }
-    const double corr = partition_correction<S>(f);
-    const double v = __dsub_rn(P.m[boff + pos], corr);
-    double* out = P.c;
-    const int copies = for_each_copy(S, j, o, e, boff, [&](uint64_t off) { out[off] = v; });
-    part = __fma_rn(static_cast<double>(copies), __dmul_rn(v, v), part);
-  }
-  // deterministic block reduction
-  for (int s = 16; s > 0; s >>= 1) part = __dadd_rn(part, __shfl_down_sync(0xffffffffu, part, s));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) s = __dadd_rn(s, red[w]);
-    P.partial[blockIdx.x] = s;
-  }
-}
-
 __global__ void copy_c1_kernel(const double* m1, double* c1, double* partial, LayoutDev lay,
                                uint64_t nblocks) {
   // C_1 = M_1 (cumulants.cpp:139), one CTA per block; the block's sum of
@@ -498,17 +406,19 @@ void launch_moment_pair(const MomParams& p, int ntiles, bool top_fma, cudaStream
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
-void launch_moms2cums(int S, const M2CParams& p, uint64_t nblocks, cudaStream_t st) {
-  if (nblocks == 0) return;
-  const unsigned g = static_cast<unsigned>(nblocks);
-  switch (S) {
-    case 2: moms2cums_kernel<2><<<g, 256, 0, st>>>(p); break;
-    case 3: moms2cums_kernel<3><<<g, 256, 0, st>>>(p); break;
-    case 4: moms2cums_kernel<4><<<g, 256, 0, st>>>(p); break;
-    case 5: moms2cums_kernel<5><<<g, 256, 0, st>>>(p); break;
-    case 6: moms2cums_kernel<6><<<g, 256, 0, st>>>(p); break;
-    default: fail(CSB_EINVAL, "moms2cums: device path supports orders <= 6");
-  }
+// out[i] = t[off[i]]: sampled elements of a stored tensor (parity checks
+// at full size, dumps of selected entries)
+__global__ void gather_kernel(const double* __restrict__ t, const uint64_t* __restrict__ off, uint64_t count,
+                              double* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[i] = t[off[i]];
+}
+
+void launch_gather(const double* t, const uint64_t* off, uint64_t count, double* out, cudaStream_t st) {
+  if (!count) return;
+  const unsigned g = static_cast<unsigned>(std::min<uint64_t>((count + 255) / 256, 4096));
+  gather_kernel<<<g, 256, 0, st>>>(t, off, count, out);
   CSB_CUDA(cudaGetLastError());
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }

@@ -28,8 +28,6 @@ struct MomParams {
   double* scratch = nullptr;  // pass-0 stash (DMMA: per tile)
   const double* zeros = nullptr;  // DMMA: >= 16 x n zero doubles (tail rows of a pass)
   int stages = 0;                 // DMMA: row-chunk stages in shared memory
-  int ones4 = 0;                  // DMMA: row sums on the DMMA pipe in R = 4 windows with <= ones4 column tiles
-  bool ones_r12 = false;          // DMMA: ... and in spare sub-partition slots of R = 1 / 2 tiles
   double c = 0.0;             // p / T        (moments.cpp:287)
   double inv = 1.0;           // 1.0 / rows   (moments.cpp:148)
 };
@@ -123,7 +121,6 @@ struct NormParams {
 };
 
 void launch_moment_pair(const MomParams& p, int ntiles, bool top_fma, cudaStream_t st);
-void launch_moms2cums(int S, const M2CParams& p, uint64_t nblocks, cudaStream_t st);
 // whether moms2cums of order S assembles every block in shared memory
 // (then it can also fill M_S's symmetric copies: MomentPlan's deferred mirror)
 bool m2c_fuse_ok(int S, int n, int b);
@@ -134,6 +131,7 @@ void launch_moment_lower2(int ST, int W, const Lower2Params& p, cudaStream_t st)
 bool lower_tma_supported(const Lower2Params& p);
 void launch_moment_lower_tma(int ST, int W, const Lower2Params& p, cudaStream_t st);
 void launch_moment_lower_side(int ST, const Lower2Params& p, cudaStream_t st);
+void launch_gather(const double* t, const uint64_t* off, uint64_t count, double* out, cudaStream_t st);
 void launch_copy_c1(const double* m1, double* c1, double* partial, const LayoutDev& lay,
                     uint64_t nblocks, uint64_t stored, cudaStream_t st);
 void launch_norm_finalize(const NormParams& p, cudaStream_t st);
@@ -153,6 +151,18 @@ void count_launch();
 
 // FP64 tensor-core (DMMA) kernel for the top pair of orders (moment_dmma.cu)
 bool dmma_supported(const MomParams& p);
+uint32_t dmma_chunk_rows(int n, int b);
+const char* dmma_kernel_name(int n, int b);
+// every non-empty segment of the pass sources starts on a 16-byte boundary
+// (the bulk copies' requirement; rows themselves are 16-byte multiples
+// when n is even)
+inline bool rows_aligned16(const RowSource* src, int npass) {
+  for (int q = 0; q < npass; ++q) {
+    if (src[q].len0 && (reinterpret_cast<uintptr_t>(src[q].seg0) & 15u)) return false;
+    if (src[q].len1 && (reinterpret_cast<uintptr_t>(src[q].seg1) & 15u)) return false;
+  }
+  return true;
+}
 size_t dmma_scratch_per_tile();
 void launch_moment_top_dmma(const MomParams& p, int ntiles, cudaStream_t st);
 // copies of canonical entries in blocks with runs (after the DMMA kernel)

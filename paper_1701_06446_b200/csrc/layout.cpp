@@ -316,15 +316,7 @@ void MomentPlan::build_dmma(int S_, int n_, int b_, const Layout& top, const Lay
     // each row set's tiles spread over 4/R sub-partitions; the choice keeps
     // the busiest sub-partition's share per row set smallest
     constexpr int kMaxNc = 3;
-    static const int r4max = [] {  // CSB_R4_MAX / CSB_R2_MAX: thresholds (experiments)
-      const char* e = std::getenv("CSB_R4_MAX");
-      return e ? std::atoi(e) : 6;
-    }();
-    static const int r2max = [] {
-      const char* e = std::getenv("CSB_R2_MAX");
-      return e ? std::atoi(e) : 12;
-    }();
-    const int R = ncg <= std::min(r4max, 6) ? 4 : ncg <= std::min(r2max, 12) ? 2 : 1;
+    const int R = ncg <= 6 ? 4 : ncg <= 12 ? 2 : 1;
     const int per_cta = kMaxNc * 8 / R;
     const int nranges = (ncg + per_cta - 1) / per_cta;
     for (int q = 0; q < nranges; ++q) {
@@ -347,24 +339,6 @@ void MomentPlan::build_dmma(int S_, int n_, int b_, const Layout& top, const Lay
   auto width = [](const MomTile& t) { return (t.ncols + (4 / t.pad0) - 1) / (4 / t.pad0); };
   std::stable_sort(tiles.begin(), tiles.end(),
                    [&](const MomTile& a, const MomTile& c) { return width(a) > width(c); });
-  // (CSB_TILE_ORDER_MIX=1 interleaves narrow tiles with wide ones to spread
-  // the L2 -> SM row traffic; measured neutral to -0.7% since 3-tile warps)
-  {
-    static const bool mix = [] {
-      const char* e = std::getenv("CSB_TILE_ORDER_MIX");
-      return e && e[0] == '1';
-    }();
-    const size_t nt = tiles.size(), keep = nt / 6;
-    if (mix && nt > keep + 2) {
-      std::vector<MomTile> mixed;
-      mixed.reserve(nt);
-      size_t lo = 0, hi = nt - keep;  // [lo, hi) interleaved from both ends
-      bool front = true;
-      while (lo < hi) mixed.push_back(front ? tiles[lo++] : tiles[--hi]), front = !front;
-      for (size_t i = nt - keep; i < nt; ++i) mixed.push_back(tiles[i]);
-      tiles.swap(mixed);
-    }
-  }
   for (size_t i = 0; i < tiles.size(); ++i) tiles[i].pad1 = static_cast<uint32_t>(i);
   scratch_per_tile = scratch;
 }

@@ -40,10 +40,6 @@
 
 #include "kernels.cuh"
 
-#ifndef CSB_EXP
-#define CSB_EXP 0  // timing experiments (tools/gpu_exp.sh); 0 in the product
-#endif
-
 namespace csb {
 
 namespace {
@@ -51,10 +47,7 @@ namespace {
 constexpr int CWARPS = 8;                 // DMMA consumer warps (two per SM sub-partition)
 constexpr int PWARPS = 4;                 // producer warps (one per row set)
 constexpr int THREADS = (CWARPS + PWARPS) * 32;
-#ifndef CSB_MAXNC
-#define CSB_MAXNC 3
-#endif
-constexpr int MAXNC = CSB_MAXNC;          // column tiles per DMMA warp
+constexpr int MAXNC = 3;                  // column tiles per DMMA warp
 // Chunk geometry: HS k4 steps (4 HS data rows) per chunk, stage and A slot;
 // HS is a kernel template parameter (8, 6 or 4, whichever leaves >= 5 stages; 10 at n = 48, b = 4).
 constexpr int ASTRIDE = 8;                // doubles per (r, q) A-ring entry (swizzled, see apos)
@@ -123,20 +116,6 @@ __device__ __forceinline__ const double* row_ptr(const RowSource& s, uint32_t k,
 }
 
 __device__ __forceinline__ int ext_of(int j, int n, int b) { return b < n - j * b ? b : n - j * b; }
-
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-      "selp.u32 %0, 1, 0, p;\n"
-      "}\n"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -225,7 +204,7 @@ __device__ __forceinline__ void produce(const MomParams& P, const MomTile& tile,
   int pidx[LM1];
 #pragma unroll
   for (int t = 0; t < LM1; ++t) pidx[t] = pr.pidx[t];
-  const int a0 = pr.a0, a1 = pr.a1;
+  const int a0 = pr.a0;  // pr.a1 == a0 + 1
   const bool update = P.npass == 2;
   const size_t stage_elems = static_cast<size_t>(KC) * n;
   double* aring = g.arings + static_cast<size_t>(rs) * g.aslots * ASLOT;
@@ -258,9 +237,6 @@ __device__ __forceinline__ void produce(const MomParams& P, const MomTile& tile,
   auto form = [&](double* as, int t, int buf) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-#if (CSB_EXP & 3) == 3  // timing experiment: no producer work
-      (void)as;
-#else
       double pv = xv[buf][q][0];
 #pragma unroll
       for (int u = 1; u < LM1; ++u) pv = __dmul_rn(pv, xv[buf][q][u]);
@@ -273,87 +249,39 @@ __device__ __forceinline__ void produce(const MomParams& P, const MomTile& tile,
         h1[q] = v1;
       }
       *reinterpret_cast<double2*>(as + t * 32 * ASTRIDE + apos(pr_r * 4 + q, pr_gp)) = make_double2(v0, v1);
-#endif
     }
   };
   auto flush = [&]() {  // add the held products (end of a pass)
-    if (!SUMS) return;
+    if (SUMS) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      s0 = __dadd_rn(s0, h0[q]);
-      s1 = __dadd_rn(s1, h1[q]);
-      h0[q] = h1[q] = 0.0;
+      for (int q = 0; q < 4; ++q) {
+        s0 = __dadd_rn(s0, h0[q]);
+        s1 = __dadd_rn(s1, h1[q]);
+        h0[q] = h1[q] = 0.0;
+      }
     }
   };
   Cursor cur;
   mbar_wait(g.xfull, 0);
-#if CSB_EXP & 64
-  long long pwait_e = 0, pwait_x = 0;
-  const long long pl0 = clock64();
-#endif
   const double* xst = g.xs;
   load(xst, 0, 0);
-#if CSB_EXP & 128
-  uint64_t pt[16][4];
-#endif
   for (uint32_t c = 0; c < g.chunks; ++c) {
-#if CSB_EXP & 128
-    uint64_t q0, q1, q2, q3;
-    asm volatile("mov.u64 %0, %%clock64;" : "=l"(q0));
-#endif
     Cursor nx = cur;
     nx.next(g.stages);
     const double* nxst = g.xs + nx.st * stage_elems;
     const uint32_t slot = c & (g.aslots - 1);
-#if CSB_EXP & 128
-    asm volatile("mov.u64 %0, %%clock64;" : "=l"(q1));
-#endif
-#if CSB_EXP & 64
-    {
-      const long long w0 = clock64();
-      if (c >= g.aslots) mbar_wait(aempty + slot, ((c >> g.alog) - 1) & 1u);
-      pwait_e += clock64() - w0;
-    }
-#else
     if (c >= g.aslots) mbar_wait(aempty + slot, ((c >> g.alog) - 1) & 1u);
-#endif
-#if CSB_EXP & 128
-    asm volatile("mov.u64 %0, %%clock64;" : "=l"(q2));
-    q3 = 0;
-#endif
     double* as = aring + slot * ASLOT;
 #pragma unroll
     for (int t = 0; t < HSTEPS; ++t) {
       if (t + 1 < HSTEPS) {
         load(xst, t + 1, (t + 1) & 1);
       } else if (c + 1 < g.chunks) {
-#if CSB_EXP & 128
-        uint64_t w0;
-        asm volatile("mov.u64 %0, %%clock64;" : "=l"(w0));
         mbar_wait(g.xfull + nx.st, nx.ph);
-        asm volatile("mov.u64 %0, %%clock64;" : "=l"(q3));
-        q3 -= w0;
-#elif CSB_EXP & 64
-        {
-          const long long w0 = clock64();
-          mbar_wait(g.xfull + nx.st, nx.ph);
-          pwait_x += clock64() - w0;
-        }
-#else
-        mbar_wait(g.xfull + nx.st, nx.ph);
-#endif
         load(nxst, 0, (t + 1) & 1);
       }
       form(as, t, t & 1);
     }
-#if CSB_EXP & 128
-    if (c >= 20 && c < 36) {
-      pt[c - 20][0] = q0;
-      pt[c - 20][1] = q1 - q0;
-      pt[c - 20][2] = q2 - q1;
-      pt[c - 20][3] = q3;
-    }
-#endif
     // one arrival per warp: __syncwarp orders the lanes' A-ring stores
     // before lane 0's (release) arrive
     __syncwarp();
@@ -369,16 +297,6 @@ __device__ __forceinline__ void produce(const MomParams& P, const MomTile& tile,
     xst = nxst;
   }
   flush();
-#if CSB_EXP & 64
-  if (lane == 0 && P.npass == 2)
-    printf("P %u %d %lld %lld %lld\n", blockIdx.x, rs, pwait_e, pwait_x, clock64() - pl0);
-#endif
-#if CSB_EXP & 128
-  if (lane == 0 && (blockIdx.x % 53) == 0 && P.npass == 2)
-    for (int i = 1; i < 16; ++i)
-      printf("P %u %d %d %lld %lld %lld %lld\n", blockIdx.x, rs, i, (long long)(pt[i][0] - pt[i - 1][0]),
-             (long long)pt[i][1], (long long)pt[i][2], (long long)pt[i][3]);
-#endif
   // ---- order L = d-1: the row sums of this lane's two slots ----
   if (!SUMS) return;
   const double cc = P.c;
@@ -396,15 +314,6 @@ __device__ __forceinline__ void produce(const MomParams& P, const MomTile& tile,
   }
 }
 
-#if CSB_EXP & 64
-__shared__ uint64_t exp_t[2][CWARPS];  // per DMMA warp: first A slot ready, main loop done
-__shared__ uint64_t exp_w[CWARPS + PWARPS][2];  // per warp: clock64 cycles waiting (A slot / stage), loop cycles
-__device__ __forceinline__ uint64_t gtimer() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-#endif
 
 // DMMA warp: row set rs, column tiles [ct0, ct0 + NC) of the CTA's range.
 // Lane (r, q): A fragment g = row slot (r, g) at k = q; B fragment c =
@@ -412,12 +321,7 @@ __device__ __forceinline__ uint64_t gtimer() {
 // col + 8c + 2q + e.  The operand loads run one k4 step ahead across chunk
 // boundaries: the next chunk's barriers are checked and its first operands
 // loaded in the middle of the current chunk's last DMMA step.
-// ONES: the warp's last tile is the row-sum tile: B = 1.0 in every column,
-// so its accumulators are the order-(d-1) row sums -- each DMMA output is
-// the sequential fma(A, 1.0, acc) = acc + A chain, i.e. exactly the
-// reference's row-ordered plain adds (moments.cpp:44) -- and the producer
-// skips its own adds.  Used where a sub-partition has a spare tile slot.
-template <int NC, int N, int HS, int B, bool ONES>
+template <int NC, int N, int HS, int B>
 __device__ __forceinline__ void consume(const MomParams& P, const MomTile& tile, const Ring& g, int rs, int ct0,
                                         int warp) {
   constexpr int HSTEPS = HS, KC = Geo<HS>::KC, ASLOT = Geo<HS>::ASLOT;
@@ -430,11 +334,7 @@ __device__ __forceinline__ void consume(const MomParams& P, const MomTile& tile,
   const bool update = P.npass == 2;
   const size_t stage_elems = static_cast<size_t>(KC) * n;
   const double* aring = g.arings + static_cast<size_t>(rs) * g.aslots * ASLOT;
-#if CSB_EXP & 8  // timing experiment: conflict-free (wrong) B addresses
-  const double* xlane = g.xs + static_cast<size_t>(q) * (n + 4) + colbase + r;
-#else
   const double* xlane = g.xs + static_cast<size_t>(q) * n + colbase + r;
-#endif
   uint64_t* afull = g.afull + rs * g.aslots;
   uint64_t* aempty = g.aempty + rs * g.aslots;
   // pass-0 means of this thread (64 doubles), in the CTA's scratch
@@ -456,40 +356,21 @@ __device__ __forceinline__ void consume(const MomParams& P, const MomTile& tile,
     }
 #pragma unroll
     for (int cc = 0; cc < NC; ++cc)
-      bb[buf][cc] = (ONES && cc == NC - 1) ? 1.0 : xb[static_cast<size_t>(4 * t) * n + 8 * cc];
+      bb[buf][cc] = xb[static_cast<size_t>(4 * t) * n + 8 * cc];
   };
   auto mma_rows = [&](int buf, int g0, int g1) {
 #pragma unroll
     for (int cc = 0; cc < NC; ++cc)
 #pragma unroll
       for (int gg = g0; gg < g1; ++gg) {
-#if CSB_EXP & 4  // timing experiment: no DMMAs (operands still loaded)
-        asm volatile("" ::"d"(a[buf][gg]), "d"(bb[buf][cc]));
-#else
         dmma(acc[gg][cc][0], acc[gg][cc][1], a[buf][gg], bb[buf][cc]);
-#endif
       }
   };
-#if CSB_EXP & 128
-  uint64_t tl[16][3], rl[16];
-#endif
   // The x stage of a chunk is complete once its A slot is: the producer
   // arrives on afull only after its own wait on the stage's TMA barrier.
-#ifdef CSB_STAGGER  // timing experiment: the second DMMA warp of each SM sub-partition starts late
-  if (warp & 4) {
-    const long long t0 = clock64();
-    while (clock64() - t0 < CSB_STAGGER) {
-    }
-  }
-#endif
   Cursor cur;  // stage of chunk c
   uint32_t slot = 0, aph = 0;
   mbar_wait(afull, 0);
-#if CSB_EXP & 64
-  exp_t[0][warp] = gtimer();
-  long long cwait = 0;
-  const long long cl0 = clock64();
-#endif
   const double* as = aring;
   const double* xb = xlane;
   load(as, xb, 0, 0);
@@ -508,40 +389,13 @@ __device__ __forceinline__ void consume(const MomParams& P, const MomTile& tile,
     constexpr int LB = (HSTEPS - 1) & 1;
     mma_rows(LB, 0, 4);
     if (c + 1 < g.chunks) {
-#if CSB_EXP & 128  // timing experiment: per-chunk wait timeline of one warp
-      uint64_t t0, t1, t2;
-      asm volatile("mov.u64 %0, %%clock64;" : "=l"(t0));
-      asm volatile("mov.u64 %0, %%clock64;" : "=l"(t1));
       mbar_wait(afull + nslot, naph);
-      asm volatile("mov.u64 %0, %%clock64;" : "=l"(t2));
-      if (c >= 20 && c < 36) {
-        tl[c - 20][0] = t0;
-        tl[c - 20][1] = t1;
-        tl[c - 20][2] = t2;
-      }
-#elif CSB_EXP & 64
-      {
-        const long long w0 = clock64();
-        mbar_wait(afull + nslot, naph);
-        cwait += clock64() - w0;
-      }
-#else
-      mbar_wait(afull + nslot, naph);
-#endif
       load(nas, nxb, 0, LB ^ 1);
     }
     mma_rows(LB, 4, 8);
-#if CSB_EXP & 128
-    uint64_t r0, r1;
-    asm volatile("mov.u64 %0, %%clock64;" : "=l"(r0));
-#endif
     __syncwarp();  // every lane has consumed the slot
     if (lane == 0) mbar_arrive(aempty + slot);
     release_chunk(P, g, c, cur.st);
-#if CSB_EXP & 128
-    asm volatile("mov.u64 %0, %%clock64;" : "=l"(r1));
-    if (c >= 20 && c < 36) rl[c - 20] = r1 - r0;
-#endif
     if (update && c + 1 == g.cpp) {
       // end of the incoming pass: stash its means, restart the accumulators
 #pragma unroll
@@ -562,18 +416,6 @@ __device__ __forceinline__ void consume(const MomParams& P, const MomTile& tile,
     xb = nxb;
   }
 
-#if CSB_EXP & 128
-  if (lane == 0 && (blockIdx.x % 53) == 0 && P.npass == 2)
-    for (int i = 1; i < 16; ++i)
-      printf("C %u %d %d %d %lld %lld %lld %lld\n", blockIdx.x, warp, NC, i, (long long)(tl[i][0] - tl[i - 1][2]),
-             (long long)(tl[i][1] - tl[i][0]), (long long)(tl[i][2] - tl[i][1]), (long long)rl[i]);
-#endif
-#if CSB_EXP & 64
-  exp_t[1][warp] = gtimer();
-  exp_w[warp][0] = cwait;
-  exp_w[warp][1] = clock64() - cl0;
-  const long long e0 = clock64();
-#endif
   // ---- epilogue: canonical entries only ----
   // Entries of blocks with equal neighbouring coordinates have symmetric
   // copies; for those the update's delta is also written to the delta
@@ -609,7 +451,7 @@ __device__ __forceinline__ void consume(const MomParams& P, const MomTile& tile,
 #pragma unroll
     for (int gg = 0; gg < 8; ++gg)
 #pragma unroll
-      for (int c = 0; c < NC - (ONES ? 1 : 0); ++c) {
+      for (int c = 0; c < NC; ++c) {
         bool ok;
         const size_t o = offset(gg, c, 0, ok);
         if (ok) asm volatile("prefetch.global.L2 [%0];" ::"l"(P.top + o));
@@ -633,30 +475,12 @@ __device__ __forceinline__ void consume(const MomParams& P, const MomTile& tile,
 #pragma unroll
         for (int e = 0; e < 2; ++e) acc[gg][c][e] = __dmul_rn(acc[gg][c][e], P.inv);
   }
-#if CSB_EXP & 64
-  const long long e1 = clock64();
-#endif
   double* __restrict__ top = P.top;
   const double cc = P.c;
   // batches of GB slots: offsets are recomputed at the stores rather than
   // kept live next to the loaded old values
   constexpr int GB = NC >= 2 ? 2 : 4;
-  constexpr int NCD = ONES ? NC - 1 : NC;  // data-column tiles
-  if (ONES && q == 0) {
-    // row sums: lane (r, 0) holds slots (r, 0..7) in column 0 of the tile
-    double* __restrict__ low = P.low;
-#pragma unroll
-    for (int gg = 0; gg < 8; ++gg) {
-      if (vp[gg] == 0) continue;
-      const uint64_t lo = rows[gg].low_off;
-      const double v = acc[gg][NC - 1][0];
-      if (update) {
-        low[lo] = __fma_rn(cc, v, low[lo]);
-      } else {
-        low[lo] = v;
-      }
-    }
-  }
+  constexpr int NCD = NC;
 #pragma unroll
   for (int g0 = 0; g0 < 8; g0 += GB) {
     double old[GB][NCD > 0 ? NCD : 1][2];
@@ -689,10 +513,6 @@ __device__ __forceinline__ void consume(const MomParams& P, const MomTile& tile,
           }
         }
   }
-#if CSB_EXP & 64
-  if (lane == 0 && P.npass == 2 && (blockIdx.x % 7) == 0)
-    printf("E %u %d %d %lld %lld\n", blockIdx.x, warp, NC, e1 - e0, clock64() - e1);
-#endif
 }
 
 // Column tiles [ct0, ct1) of DMMA warp w in a CTA with R row-set slots and
@@ -717,24 +537,12 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t bars[MAX_STAGES + 2 * PWARPS * ASLOTS];
   __shared__ uint32_t rel[MAX_STAGES];
-#if CSB_EXP & 64
-  uint64_t t_start;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-#endif
   const MomTile tile = P.tiles[blockIdx.x];
   const int R = static_cast<int>(tile.pad0);    // row-set slots of this CTA: 1, 2, 4
   const int nrs = static_cast<int>(tile.nrows); // live row sets (<= R)
   const int nct0 = static_cast<int>(tile.ncols);
-  // Optionally (P.ones_r12 / P.ones4, off by default: measured slower on
-  // B200 -- the extra DMMAs slow the producer sharing the FP64 pipe more
-  // than its adds cost) the order-(d-1) row sums run on the DMMA pipe as
-  // an extra all-ones column tile where a sub-partition has a spare tile
-  // slot (R = 1: nct not a multiple of 4, R = 2: nct odd) or in the
-  // thinnest windows (R = 4, nct <= P.ones4).  Bit-identical either way.
   const bool sums = P.low != nullptr && tile.low;
-  const bool ones = sums && ((P.ones_r12 && ((R == 1 && (nct0 & 3) != 0) || (R == 2 && (nct0 & 1) != 0))) ||
-                             (R == 4 && nct0 <= P.ones4));
-  const int nct = nct0 + (ones ? 1 : 0);
+  const int nct = nct0;
   Ring g;
   g.stages = static_cast<uint32_t>(P.stages);
   g.xs = smem;
@@ -752,11 +560,7 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
   g.chunks = g.cpp * P.npass;  // incoming pass, then outgoing pass
   const int warp = threadIdx.x >> 5;
   // active warps: DMMA warps whose row set is live, one producer per live row set
-#if CSB_EXP & 16  // timing experiment: producers exit at once
-  int active = 0;
-#else
   int active = nrs;
-#endif
   int cparts = 0;  // DMMA warps with tiles per row set (the same for every row set)
   for (int w = 0; w < CWARPS; ++w) {
     int c0, c1;
@@ -780,10 +584,9 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
   __syncthreads();
   if (warp >= CWARPS) {
     const int rs = warp - CWARPS;
-    if (rs >= nrs || (CSB_EXP & 16)) return;
-    const bool psums = sums && !ones;
+    if (rs >= nrs) return;
 #define CSB_PRODUCE(LM1)                                       \
-  if (psums) produce<LM1, N, HS, true>(P, tile, g, rs);        \
+  if (sums) produce<LM1, N, HS, true>(P, tile, g, rs);        \
   else produce<LM1, N, HS, false>(P, tile, g, rs);
     switch (P.L) {
       case 2: CSB_PRODUCE(1) break;
@@ -799,33 +602,12 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
   if (rs >= nrs) return;
   int ct0, ct1;
   warp_tiles(warp, R, nct, ct0, ct1);
-  static_assert(MAXNC == 2 || MAXNC == 3, "column tiles per DMMA warp");
-  const bool wones = ones && ct1 == nct;  // this warp's last tile is the row-sum tile
-  switch ((ct1 - ct0) * 2 + (wones ? 1 : 0)) {
-    case 2: consume<1, N, HS, B, false>(P, tile, g, rs, ct0, warp); break;
-    case 3: consume<1, N, HS, B, true>(P, tile, g, rs, ct0, warp); break;
-    case 4: consume<2, N, HS, B, false>(P, tile, g, rs, ct0, warp); break;
-    case 5: consume<2, N, HS, B, true>(P, tile, g, rs, ct0, warp); break;
-#if CSB_MAXNC >= 3
-    case 6: consume<3, N, HS, B, false>(P, tile, g, rs, ct0, warp); break;
-    case 7: consume<3, N, HS, B, true>(P, tile, g, rs, ct0, warp); break;
-#endif
+  switch (ct1 - ct0) {
+    case 1: consume<1, N, HS, B>(P, tile, g, rs, ct0, warp); break;
+    case 2: consume<2, N, HS, B>(P, tile, g, rs, ct0, warp); break;
+    case 3: consume<3, N, HS, B>(P, tile, g, rs, ct0, warp); break;
     default: break;
   }
-#if CSB_EXP & 64  // timing experiment: per-CTA timeline of consumer warps
-  {
-    uint64_t t_end;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
-    uint32_t smid;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    if ((threadIdx.x & 31) == 0 && P.npass == 2)
-      printf("T %u %u %d %d %d %d %llu %llu %llu %llu\n", blockIdx.x, smid, warp, R, nrs, ct1 - ct0,
-             (unsigned long long)t_start, (unsigned long long)t_end, (unsigned long long)exp_t[0][warp],
-             (unsigned long long)exp_t[1][warp]);
-    if ((threadIdx.x & 31) == 0 && P.npass == 2 && ct1 > ct0)
-      printf("W %u %d %d %lld %lld\n", blockIdx.x, warp, ct1 - ct0, (long long)exp_w[warp][0], (long long)exp_w[warp][1]);
-  }
-#endif
 }
 
 // Symmetric copies of the canonical entries written above, one CTA per
@@ -926,30 +708,54 @@ int stages_for(int n, int hs) {
 // fewer chunk hand-offs per row beat the shallower ring there (cfg2 top
 // kernel 16.01 -> 15.79 ms, tools/gpu_hs10.sh)
 int chunk_steps(int n, int b) {
-  static const int forced = [] {  // CSB_HS=4|6|8|10 (experiments)
-    const char* e = std::getenv("CSB_HS");
-    return e ? std::atoi(e) : 0;
-  }();
   const bool hs10 = n == 48 && b == 4;
-  if (forced == 4 || forced == 6 || forced == 8 || (forced == 10 && hs10))
-    if (stages_for(n, forced) >= 2) return forced;
   if (hs10 && stages_for(n, 10) >= 4) return 10;
   for (int hs : {8, 6, 4})
     if (stages_for(n, hs) >= 5) return hs;
   return 4;
 }
 
+struct DmmaKernel {
+  void (*fn)(MomParams);
+  const char* name;
+};
+
+// specialised (row length, chunk, block size) of the BASELINE configs; generic otherwise
+DmmaKernel pick_dmma_kernel(int n, int b) {
+  const int hs = chunk_steps(n, b);
+#define CSB_K(NN, HH, BB) {moment_top_dmma_kernel<NN, HH, BB>, "moment_top_dmma_kernel<" #NN "," #HH "," #BB ">"}
+  if (n == 96 && hs == 6 && b == 8) return CSB_K(96, 6, 8);
+  if (n == 96 && hs == 8 && b == 8) return CSB_K(96, 8, 8);
+  if (n == 48 && hs == 8 && b == 4) return CSB_K(48, 8, 4);
+  if (n == 48 && hs == 10 && b == 4) return CSB_K(48, 10, 4);
+  if (n == 24 && hs == 8 && b == 3) return CSB_K(24, 8, 3);
+  if (n == 256 && hs == 4 && b == 16) return CSB_K(256, 4, 16);
+  if (hs == 8) return CSB_K(0, 8, 0);
+  if (hs == 6) return CSB_K(0, 6, 0);
+  return CSB_K(0, 4, 0);
+#undef CSB_K
+}
+
 }  // namespace
+
+const char* dmma_kernel_name(int n, int b) { return pick_dmma_kernel(n, b).name; }
 
 // per tile: the incoming pass's means (64 values per consumer thread)
 size_t dmma_scratch_per_tile() { return static_cast<size_t>(CWARPS) * 32 * 16 * MAXNC; }
 
 bool dmma_supported(const MomParams& p) {
   // instantiated for orders 3..6 (L = 2..5); rows must be 16-byte aligned
-  // for the bulk copies, and at least two stages must fit
+  // for the bulk copies (even n and 16-byte aligned segment starts: a
+  // caller's pointer may be offset by one double), and at least two stages
+  // must fit
   if (p.n % 2 != 0 || p.L < 2 || p.L > 5) return false;
+  if (!rows_aligned16(p.src, p.npass)) return false;
   return stages_for(p.n, 4) >= 2;
 }
+
+// data rows per chunk of the launched kernel: the zero-row source of a
+// pass's last chunk must hold this many rows
+uint32_t dmma_chunk_rows(int n, int b) { return 4u * static_cast<uint32_t>(chunk_steps(n, b)); }
 
 void launch_mirror(int S, double* m, const LayoutDev& lay, const uint32_t* blocks, uint32_t nblocks, int n, int b,
                    const uint2* lists, const uint32_t* list_off, cudaStream_t st) {
@@ -970,31 +776,11 @@ void launch_moment_top_dmma(const MomParams& p_in, int ntiles, cudaStream_t st) 
   MomParams p = p_in;
   const int hs = chunk_steps(p.n, p.b);
   p.stages = stages_for(p.n, hs);
-  static const int ones4 = [] {  // CSB_ONES4=0..3: row-sum tile in R = 4 windows of <= k column tiles
-    const char* e = std::getenv("CSB_ONES4");
-    return e ? std::max(0, std::min(3, std::atoi(e))) : 0;
-  }();
-  static const bool ones_r12 = [] {  // CSB_ONES=1: row-sum tile in spare R = 1 / 2 slots
-    const char* e = std::getenv("CSB_ONES");
-    return e && e[0] == '1';
-  }();
-  p.ones4 = ones4;
-  p.ones_r12 = ones_r12;
   if (p.stages < 2) fail(CSB_EINVAL, "moment_top_dmma: rows too wide for the staging ring");
   const size_t smem = smem_bytes(p.n, p.stages, hs);
-  using K = void (*)(MomParams);
-  K kern = nullptr;
-  // specialised (row length, chunk, block size) of the BASELINE configs; generic otherwise
-  if (p.n == 96 && hs == 6 && p.b == 8) kern = moment_top_dmma_kernel<96, 6, 8>;
-  else if (p.n == 96 && hs == 8 && p.b == 8) kern = moment_top_dmma_kernel<96, 8, 8>;
-  else if (p.n == 48 && hs == 8 && p.b == 4) kern = moment_top_dmma_kernel<48, 8, 4>;
-  else if (p.n == 48 && hs == 10 && p.b == 4) kern = moment_top_dmma_kernel<48, 10, 4>;
-  else if (p.n == 24 && hs == 8 && p.b == 3) kern = moment_top_dmma_kernel<24, 8, 3>;
-  else if (p.n == 256 && hs == 4 && p.b == 16) kern = moment_top_dmma_kernel<256, 4, 16>;
-  else if (hs == 8) kern = moment_top_dmma_kernel<0, 8, 0>;
-  else if (hs == 6) kern = moment_top_dmma_kernel<0, 6, 0>;
-  else kern = moment_top_dmma_kernel<0, 4, 0>;
-  ensure_smem(kern, smem);
+  const DmmaKernel k = pick_dmma_kernel(p.n, p.b);
+  ensure_smem(k.fn, smem);
+  auto kern = k.fn;
   kern<<<ntiles, THREADS, smem, st>>>(p);
   CSB_CUDA(cudaGetLastError());
   count_launch();

@@ -2,9 +2,11 @@
 
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "common.hpp"
 
@@ -109,4 +111,97 @@ void allreduce_sum(void* comm, double* buf, uint64_t count, cudaStream_t st) {
 }
 
 }  // namespace nccl
+
+namespace {
+
+class NcclComm final : public Comm {
+ public:
+  NcclComm(int nranks, int rank, const unsigned char* id) : Comm(nranks, rank), c_(nccl::comm_init(nranks, rank, id)) {}
+  ~NcclComm() override { nccl::comm_destroy(c_); }
+  void allgather_ranges(double* buf, const uint64_t* off, const uint64_t* cnt, cudaStream_t st) override {
+    nccl::allgather_ranges(c_, buf, off, cnt, nranks, st);
+  }
+  void allreduce_sum(double* buf, uint64_t count, cudaStream_t st) override {
+    nccl::allreduce_sum(c_, buf, count, st);
+  }
+
+ private:
+  void* c_;
+};
+
+// Caller-supplied collectives.  host_staged: the engine drains its stream,
+// copies the span to a pinned host buffer, calls back on host memory and
+// copies the result back (a CPU transport such as gloo); otherwise the
+// callback gets the device pointer and the cudaStream_t to order on.
+class OpsComm final : public Comm {
+ public:
+  OpsComm(int nranks, int rank, const csb_comm_ops& ops) : Comm(nranks, rank), ops_(ops) {}
+  ~OpsComm() override {
+    if (host_) cudaFreeHost(host_);
+  }
+  void allgather_ranges(double* buf, const uint64_t* off, const uint64_t* cnt, cudaStream_t st) override {
+    if (!ops_.allgather_ranges) fail(CSB_ERUNTIME, "comm: allgather_ranges callback missing");
+    if (!ops_.host_staged) {
+      if (ops_.allgather_ranges(ops_.ctx, buf, off, cnt, nranks, st) != 0)
+        fail(CSB_ERUNTIME, "comm: allgather_ranges callback failed");
+      return;
+    }
+    uint64_t lo = UINT64_MAX, hi = 0;
+    for (int r = 0; r < nranks; ++r)
+      if (cnt[r]) {
+        lo = std::min(lo, off[r]);
+        hi = std::max(hi, off[r] + cnt[r]);
+      }
+    if (hi <= lo) return;
+    double* h = stage(buf + lo, hi - lo, st);
+    std::vector<uint64_t> rel(off, off + nranks);
+    for (auto& o : rel) o = o >= lo ? o - lo : 0;
+    if (ops_.allgather_ranges(ops_.ctx, h, rel.data(), cnt, nranks, nullptr) != 0)
+      fail(CSB_ERUNTIME, "comm: allgather_ranges callback failed");
+    unstage(buf + lo, hi - lo, st);
+  }
+  void allreduce_sum(double* buf, uint64_t count, cudaStream_t st) override {
+    if (!ops_.allreduce_sum) fail(CSB_ERUNTIME, "comm: allreduce_sum callback missing");
+    if (!count) return;
+    if (!ops_.host_staged) {
+      if (ops_.allreduce_sum(ops_.ctx, buf, count, st) != 0) fail(CSB_ERUNTIME, "comm: allreduce_sum callback failed");
+      return;
+    }
+    double* h = stage(buf, count, st);
+    if (ops_.allreduce_sum(ops_.ctx, h, count, nullptr) != 0) fail(CSB_ERUNTIME, "comm: allreduce_sum callback failed");
+    unstage(buf, count, st);
+  }
+
+ private:
+  double* stage(const double* dev, uint64_t count, cudaStream_t st) {
+    if (cap_ < count) {
+      if (host_) cudaFreeHost(host_);
+      host_ = nullptr;
+      cap_ = 0;
+      CSB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&host_), count * sizeof(double)));
+      cap_ = count;
+    }
+    CSB_CUDA(cudaMemcpyAsync(host_, dev, count * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CSB_CUDA(cudaStreamSynchronize(st));
+    return host_;
+  }
+  void unstage(double* dev, uint64_t count, cudaStream_t st) {
+    CSB_CUDA(cudaMemcpyAsync(dev, host_, count * sizeof(double), cudaMemcpyHostToDevice, st));
+    CSB_CUDA(cudaStreamSynchronize(st));  // the host buffer is reused by the next call
+  }
+  csb_comm_ops ops_;
+  double* host_ = nullptr;
+  uint64_t cap_ = 0;
+};
+
+}  // namespace
+
+std::shared_ptr<Comm> make_nccl_comm(int nranks, int rank, const unsigned char* id) {
+  return std::make_shared<NcclComm>(nranks, rank, id);
+}
+
+std::shared_ptr<Comm> make_ops_comm(int nranks, int rank, const csb_comm_ops& ops) {
+  return std::make_shared<OpsComm>(nranks, rank, ops);
+}
+
 }  // namespace csb

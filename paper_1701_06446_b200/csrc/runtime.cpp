@@ -70,8 +70,7 @@ struct Device {
   std::map<std::pair<int, int>, std::pair<std::shared_ptr<DevBuf<uint2>>, std::shared_ptr<DevBuf<uint32_t>>>> mirror;
   std::map<std::pair<int, int>, std::pair<std::shared_ptr<DevBuf<uint32_t>>, std::shared_ptr<DevBuf<uint32_t>>>> copies;
   std::map<std::tuple<int, int, int, int>, std::shared_ptr<ShardPlan>> shards;
-  void* comm = nullptr;  // NCCL communicator (csb_comm_init)
-  int nranks = 1, rank = 0;
+  std::shared_ptr<Comm> comm;  // csb_comm_init / csb_comm_init_ops
 };
 
 std::mutex g_dev_mu;
@@ -591,37 +590,6 @@ struct Scratch {
   }
 };
 thread_local std::map<int, Scratch> g_scratch;
-// CSB_NO_DMMA=1 forces the DFMA kernel for the top pair (A/B testing)
-// CSB_LOW_INLINE=1 runs the low-order kernel in line (A/B testing)
-const bool g_low_side = [] {
-  const char* e = std::getenv("CSB_LOW_INLINE");
-  return !(e && e[0] == '1');
-}();
-// CSB_LOW_KERNEL=side: the register-only low-order kernel instead of the
-// TMA-staged one; CSB_LOW_DEFER=0: launch it before the top kernel (A/B)
-const bool g_low_tma = [] {
-  const char* e = std::getenv("CSB_LOW_KERNEL");
-  return !(e && std::strcmp(e, "side") == 0);
-}();
-// CSB_M2C_DIRECT=0: moms2cums' out-of-block pass writes the copies and the
-// norm terms in a second pass over the block (A/B)
-const bool g_m2c_direct = [] {
-  const char* e = std::getenv("CSB_M2C_DIRECT");
-  return !(e && e[0] == '0');
-}();
-const bool g_low_defer = [] {
-  const char* e = std::getenv("CSB_LOW_DEFER");
-  return !(e && e[0] == '0');
-}();
-const bool g_low_top = [] {
-  const char* e = std::getenv("CSB_LOW_TOP");
-  return e && e[0] == '1';
-}();
-const bool g_use_dmma = [] {
-  const char* e = std::getenv("CSB_NO_DMMA");
-  return !(e && e[0] == '1');
-}();
-
 // Orders are processed as pairs (S, S-1): (d, d-1), (d-2, d-3), ... with a
 // lone order 1 when d is odd.  Only the pair topped by d uses the fused
 // multiply-add of the reference's deepest loop (moments.cpp:47).
@@ -635,7 +603,7 @@ const bool g_use_dmma = [] {
 struct ShardCtx {
   const ShardPlan* plan = nullptr;
   int index = 0;
-  void* comm = nullptr;
+  Comm* comm = nullptr;
   bool active() const { return plan && plan->count > 1; }
   uint64_t lo(int which) const { return (which ? plan->low_blk : plan->top_blk)[index]; }
   uint64_t hi(int which) const { return (which ? plan->low_blk : plan->top_blk)[index + 1]; }
@@ -666,19 +634,15 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
   p.inv = 1.0 / static_cast<double>(K);
   // the top pair runs on the FP64 tensor cores when the rows allow TMA
   // bulk copies; otherwise on the DFMA kernel
-  const bool use_dmma = g_use_dmma && dmma_supported(p);
+  const bool use_dmma = dmma_supported(p);
   // sharding applies to the DMMA plan (the DFMA fallback computes all blocks)
   const bool sharded = use_dmma && sh.active() && !only_order;
   // orders <= d-2 beside the DMMA top pair: a lean kernel on the side
   // stream (joined at the end of this call) when they are few (it is
   // latency bound and hides under the top pair); else staged, in line
   // (the TMA-staged kernel handles any count when rows are 16-byte multiples)
-  const bool side = lower && d - 2 <= 4 && use_dmma && g_low_side &&
-                    (multiset_count(m->n, d - 2) <= 60000 || (g_low_tma && m->n % 2 == 0));
-  // CSB_LOW_TOP=1: order d-1 too in the side-stream kernel, so the top
-  // kernel's producers carry no row sums (A/B: see DESIGN.md)
-  const bool low_top = side && g_low_tma && g_low_top && !sharded && d - 1 <= 4 && m->n % 2 == 0;
-  if (low_top) p.low = nullptr;
+  const bool side = lower && d - 2 <= 4 && use_dmma &&
+                    (multiset_count(m->n, d - 2) <= 60000 || m->n % 2 == 0);
   bool joined = true;
   // The side-stream launch is deferred until the top kernel is queued: the
   // block scheduler hands SMs to the top kernel's CTAs first and the few
@@ -687,7 +651,7 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
   // ~180 us and cost cfg1's top kernel 31 us (measured; CSB_LOW_DEFER=0).
   std::function<void()> side_launch;
   if (lower && d - 2 <= 4) {
-    const int ST = low_top ? d - 1 : d - 2;
+    const int ST = d - 2;
     // the tables are looked up inside the launch: on the side path that
     // runs after the top kernel is queued, keeping the host work before
     // the step's first (and longest) kernel short
@@ -712,21 +676,20 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
     };
     if (side) {
       CSB_CUDA(cudaEventRecord(dev.fork, st));  // the low orders depend only on work queued so far
-      side_launch = [&dev, ST, make_params, &side_tail, side_tail_ran, m]() {
+      side_launch = [&dev, ST, make_params, &side_tail, side_tail_ran, m, src, npass]() {
         // many elements: a thread owns 4 consecutive ones (shared prefix work)
         // (the TMA kernel only; same test as lower_tma_supported)
-        const bool tma = g_low_tma && m->n % 2 == 0 && m->n <= 4096;
+        const bool tma = m->n % 2 == 0 && m->n <= 4096 && rows_aligned16(src, npass);
         const int W = tma && ST >= 2 && multiset_count(m->n, ST) > 60000 ? 4 : 1;
-        static const bool strided = [] {  // CSB_LOWT_STRIDED=0: consecutive elements per thread (A/B)
-          const char* e = std::getenv("CSB_LOWT_STRIDED");
-          return !(e && e[0] == '0');
-        }();
-        const Lower2Params lp = make_params(W > 1 && strided ? -W : W);
+        // W > 1: a thread's elements are strided over its prefix (negative W
+        // selects that thread table), so a prefix's lanes read consecutive
+        // staged columns
+        const Lower2Params lp = make_params(W > 1 ? -W : W);
         {
           std::lock_guard<std::mutex> lk(dev.mu);
           CSB_CUDA(cudaStreamWaitEvent(dev.side, dev.fork, 0));
           ProfScope pl("moment_low", dev.side);
-          if (tma && lower_tma_supported(lp))
+          if (tma)
             launch_moment_lower_tma(ST, W, lp, dev.side);
           else
             launch_moment_lower_side(ST, lp, dev.side);
@@ -738,10 +701,6 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
         std::lock_guard<std::mutex> lk(dev.mu);
         CSB_CUDA(cudaEventRecord(dev.join, dev.side));
       };
-      if (!g_low_defer) {
-        side_launch();
-        side_launch = nullptr;
-      }
       joined = false;
     } else {
       ProfScope ps("moment_low", st);
@@ -775,7 +734,7 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
     const uint64_t ntiles = plan->tiles.size();
     if (npass == 2 || use_dmma) p.scratch = sc.get(ntiles * plan->scratch_per_tile);
     if (use_dmma) {
-      p.zeros = sc.get_zeros(32ull * m->n);
+      p.zeros = sc.get_zeros(static_cast<uint64_t>(dmma_chunk_rows(m->n, m->b)) * m->n);
       {
         ProfScope ps("moment_top", st);  // the DMMA kernel alone (bench roofline)
         launch_moment_top_dmma(p, static_cast<int>(ntiles), st);
@@ -810,7 +769,7 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
             cnt[r] = LL->host.offset[sh.plan->low_blk[r + 1]] - off[r];
           }
           ProfScope pc("allgather", st);
-          nccl::allgather_ranges(sh.comm, p.low, off.data(), cnt.data(), sh.plan->count, st);
+          sh.comm->allgather_ranges(p.low, off.data(), cnt.data(), st);
         }
       }
     } else {
@@ -890,11 +849,9 @@ void run_moms2cums(const csb_series* m, csb_series* c, NormScratch& ns, cudaStre
         auto ml = get_mirror_lists(*m->dev, s, m->b);
         p.mlist = ml.first;
         p.mlist_off = ml.second;
-        if (g_m2c_direct) {
-          auto cp = get_copy_lists(*m->dev, s, m->b);
-          p.cstart = cp.first;
-          p.cdst = cp.second;
-        }
+        auto cp = get_copy_lists(*m->dev, s, m->b);
+        p.cstart = cp.first;
+        p.cdst = cp.second;
       }
     }
     if (m->mirror_defer >> (s - 1) & 1u) {
@@ -911,7 +868,7 @@ void run_moms2cums(const csb_series* m, csb_series* c, NormScratch& ns, cudaStre
       launch_moms2cums_v2(s, p, hi - lo, st);
       if (sh.comm) {
         ProfScope pc("allreduce", st);
-        nccl::allreduce_sum(sh.comm, ns.partial[s - 1].ptr, m->lay[s - 1]->host.nblocks, st);  // collective C3
+        sh.comm->allreduce_sum(ns.partial[s - 1].ptr, m->lay[s - 1]->host.nblocks, st);  // collective C3
       }
     } else {
       p.blk0 = 0;
@@ -975,7 +932,7 @@ void finalize_norms(const csb_series* c, NormScratch& ns, cudaStream_t st, const
     if (ns.diag.count < static_cast<uint64_t>(c->n)) ns.diag.alloc(c->n);
     launch_diag_pick(c->data[d - 1].ptr, dt.off[d - 2].ptr, L->host.offset[sh.lo(0)], L->host.offset[sh.hi(0)],
                      c->n, ns.diag.ptr, st);
-    if (sh.comm) nccl::allreduce_sum(sh.comm, ns.diag.ptr, c->n, st);
+    if (sh.comm) sh.comm->allreduce_sum(ns.diag.ptr, c->n, st);
     p.diag_src[d - 2] = ns.diag.ptr;
     p.diag_off[d - 2] = dt.iota.ptr;
   }
@@ -1071,6 +1028,7 @@ struct csb_stream {
   int early_m2c = 0;  // moms2cums orders already enqueued on the side stream this step
   bool norms_valid = false;
   std::shared_ptr<ShardPlan> splan;  // shard_count > 1
+  std::shared_ptr<Comm> comm;        // kept alive for the stream's lifetime
   ShardCtx sh;
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
   ~csb_stream() {
@@ -1307,6 +1265,24 @@ int csb_series_download(const csb_series* s, int order, double* host, uint64_t c
   });
 }
 
+int csb_series_gather(const csb_series* s, int order, const uint64_t* offsets, uint64_t count, double* host) {
+  return guard([&] {
+    check_order(s, order);
+    require(count == 0 || (offsets && host), "series_gather: null argument");
+    if (!count) return;
+    const uint64_t stored = s->lay[order - 1]->host.stored;
+    for (uint64_t i = 0; i < count; ++i)
+      if (offsets[i] >= stored) fail(CSB_ERANGE, "series_gather: offset out of range");
+    cudaStream_t st = s->dev->stream;
+    DevBuf<uint64_t> off(count);
+    DevBuf<double> out(count);
+    CSB_CUDA(cudaMemcpyAsync(off.ptr, offsets, count * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+    launch_gather(s->data[order - 1].ptr, off.ptr, count, out.ptr, st);
+    CSB_CUDA(cudaMemcpyAsync(host, out.ptr, count * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CSB_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
 static void moment_series_impl(csb_series* out, const double* xd, uint64_t rows, uint64_t,
                                const ShardCtx& sh = ShardCtx{}) {
   RowSource src[2];
@@ -1476,12 +1452,14 @@ int csb_stream_prime(const csb_stream_config* cfg, const double* first, uint64_t
     if (cfg->shard_count > 1) {
       if (cfg->shard_index < 0 || cfg->shard_index >= cfg->shard_count)
         fail(CSB_EINVAL, "StreamConfig: shard_index must be in [0, shard_count)");
-      if (!s->dev->comm || s->dev->nranks != cfg->shard_count || s->dev->rank != cfg->shard_index)
+      const auto& cm = s->dev->comm;
+      if (!cm || cm->nranks != cfg->shard_count || cm->rank != cfg->shard_index)
         fail(CSB_EINVAL, "prime: shard_count > 1 needs csb_comm_init(shard_count, shard_index, id) first");
+      s->comm = cm;
       s->splan = get_shard_plan(*s->dev, cfg->max_order, cfg->dim, cfg->block_size, cfg->shard_count);
       s->sh.plan = s->splan.get();
       s->sh.index = cfg->shard_index;
-      s->sh.comm = s->dev->comm;
+      s->sh.comm = s->comm.get();
     }
     s->M = make_series(cfg->dim, cfg->max_order, cfg->block_size);
     s->C = make_series(cfg->dim, cfg->max_order, cfg->block_size);
@@ -1568,7 +1546,8 @@ int csb_stream_norm_partials(csb_stream* s, int order, double* host, uint64_t co
     require(count == buf.count, "norm_partials: size mismatch");
     CSB_CUDA(cudaStreamSynchronize(s->st));
     CSB_CUDA(cudaMemcpy(host, buf.ptr, buf.bytes(), cudaMemcpyDeviceToHost));
-    if (first_block) *first_block = (s->sh.active() && order == s->cfg.max_order) ? s->sh.lo(0) : 0;
+    // a sharded stream's order-d partials are allreduced: the whole array is valid
+    if (first_block) *first_block = 0;
   });
 }
 
@@ -1583,20 +1562,23 @@ int csb_comm_init(int nranks, int rank, const unsigned char* id) {
   return guard([&] {
     require(id != nullptr && nranks >= 1 && rank >= 0 && rank < nranks, "comm_init: bad arguments");
     Device& dev = device();
-    if (dev.comm) nccl::comm_destroy(dev.comm);
-    dev.comm = nranks > 1 ? nccl::comm_init(nranks, rank, id) : nullptr;
-    dev.nranks = nranks;
-    dev.rank = rank;
+    dev.comm.reset();  // live streams keep theirs
+    if (nranks > 1) dev.comm = make_nccl_comm(nranks, rank, id);
+  });
+}
+
+int csb_comm_init_ops(int nranks, int rank, const csb_comm_ops* ops) {
+  return guard([&] {
+    require(ops != nullptr && nranks >= 1 && rank >= 0 && rank < nranks, "comm_init_ops: bad arguments");
+    Device& dev = device();
+    dev.comm.reset();
+    if (nranks > 1) dev.comm = make_ops_comm(nranks, rank, *ops);
   });
 }
 
 int csb_comm_destroy(void) {
   return guard([&] {
-    Device& dev = device();
-    if (dev.comm) nccl::comm_destroy(dev.comm);
-    dev.comm = nullptr;
-    dev.nranks = 1;
-    dev.rank = 0;
+    device().comm.reset();
   });
 }
 
@@ -1655,6 +1637,21 @@ int csb_moms2cums_shard(const csb_series* m, csb_series* c, int shard_index, int
 }
 
 uint64_t csb_launch_count(void) { return csb::launch_count(); }
+
+int csb_top_kernel(int dim, int max_order, int block, char* out, uint64_t cap) {
+  return guard([&] {
+    require(out && cap > 0, "top_kernel: null output");
+    require(dim >= 1 && block >= 1 && block <= dim && max_order >= 1 && max_order <= kMaxOrder,
+            "top_kernel: bad shape");
+    MomParams p;
+    p.n = dim;
+    p.b = block;
+    p.L = max_order - 1;
+    p.npass = 1;  // aligned rows assumed
+    std::string name = dmma_supported(p) ? dmma_kernel_name(dim, block) : "moment_pair_kernel (DFMA)";
+    std::snprintf(out, cap, "%s", name.c_str());
+  });
+}
 
 int csb_profile_enable(int on) {
   return guard([&] {

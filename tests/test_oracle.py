@@ -184,3 +184,25 @@ def test_sampled_element_oracle(port):
     idx = (C.c_int * 3)(0, 2, 4)
     v = lib.oc_sample_moment(x.ctypes.data_as(C.POINTER(C.c_double)), 64, 5, idx, 3)
     assert math.isclose(v, float(np.mean(x[:, 0] * x[:, 2] * x[:, 4])), rel_tol=1e-13)
+
+
+def test_exact_sampled_oracle_matches_full_port(port):
+    """The exact sampled-element oracle (used by the full-size GPU parity
+    tests at cfg2-cfg4) reproduces the full port bit for bit: moments after
+    prime + updates, element offsets, cumulants from the lower orders."""
+    from itertools import combinations_with_replacement as cwr
+    for (n, d, b, T, p, steps) in ((10, 4, 3, 40, 7, 3), (7, 6, 2, 20, 5, 2)):
+        rng = np.random.default_rng(n * d)
+        x = rng.standard_normal((T + steps * p, n))
+        m = port.moment_series(x[:T], d, b)
+        for k in range(steps):
+            port.moments_update(m, T, x[T + k * p: T + (k + 1) * p], x[k * p: (k + 1) * p], b)
+        c = port.moms2cums(m, n, b)
+        for s in range(1, d + 1):
+            idx = np.array(list(cwr(range(n), s)), dtype=np.int32)
+            off = port.element_offsets(s, n, b, idx).astype(np.int64)
+            v = port.sample_stream_moments(x, T, p, steps, s, s == d, idx)
+            assert np.array_equal(v, m[s - 1][off]), (n, d, s)
+            if s >= 2:
+                cv = port.sample_cumulants(c[:s - 1], n, b, s, idx, m[s - 1][off])
+                assert np.array_equal(cv, c[s - 1][off]), (n, d, s)
