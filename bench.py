@@ -22,10 +22,12 @@ value  = window updates/s with the incoming rows already resident in HBM
 e2e    = the same through the C ABI with HOST buffers (csb_stream_step on
          pinned rows): H2D of the rows and D2H of the report inside the
          timed region.
-roofline = the order-d/d-1 moment kernel (moment_top): algorithmic flops per
-         launch / its event-timed average duration, against the measured
-         FP64 peak (profiles/fp64_peak.json; MEASURED_PEAKS.json has no FP64
-         entry).
+roofline = the order-d/d-1 moment computation: the DMMA kernel (moment_top,
+         the wide column windows) plus, where the plan uses it, the CUDA-core
+         kernel of the narrowest windows (moment_tail) -- algorithmic flops
+         of orders d and d-1 per step / the two kernels' event-timed average
+         durations per step, against the measured FP64 peak
+         (profiles/fp64_peak.json; MEASURED_PEAKS.json has no FP64 entry).
 cpu_baseline = the reference itself (oracle/_ref, compiled from
          /root/reference) on the host cores: one step's two library calls
          (moments_update + moms2cums, stream.cpp:85-108) at the config's
@@ -314,6 +316,7 @@ def main() -> None:
         if profiled:
             capi.profile_enable(True)
             capi.profile_read("moment_top")
+            capi.profile_read("moment_tail")
         l0 = capi.launch_count()
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(args.steps)]
@@ -332,6 +335,9 @@ def main() -> None:
         w = time.perf_counter() - w0
         nl = capi.launch_count() - l0
         tm, tn = (capi.profile_read("moment_top") if profiled else (0.0, 0))
+        if profiled:
+            tt, _ = capi.profile_read("moment_tail")
+            tm += tt  # both kernels of the order-d/d-1 pair
         if profiled:
             capi.profile_enable(False)
         ms = [a.elapsed_time(b) for a, b in evs]
@@ -405,7 +411,8 @@ def main() -> None:
                                f"report(nu3..nu{cfg.d})"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "kernel": f"moment_top_dmma_kernel (orders {cfg.d} and {cfg.d - 1}, FP64 DMMA)",
+                         "kernel": (f"orders {cfg.d} and {cfg.d - 1}: moment_top_dmma_kernel (FP64 DMMA) + "
+                                    "moment_tail_kernel (FP64 FMA, narrowest column windows)"),
                          "flops_per_launch": flops["F_top_launch"], "avg_launch_ms": top_avg_s * 1e3,
                          "launches": top_n, "peak_source": peak_src,
                          "timed_in": "a profiled pass of the same K steps run just before the (unprofiled) value pass",

@@ -28,6 +28,9 @@ struct MomParams {
   double* scratch = nullptr;  // pass-0 stash (DMMA: per tile)
   const double* zeros = nullptr;  // DMMA: >= 16 x n zero doubles (tail rows of a pass)
   int stages = 0;                 // DMMA: row-chunk stages in shared memory
+  const TailTask* tail = nullptr;  // moment_tail_kernel: tasks (32 per warp), rows = their PrefixRows
+  uint32_t tail_warps = 0;
+  uint32_t stash_slots = 0, stash_stride = 0;  // moment_tail_kernel: per-SM stash in scratch
   double c = 0.0;             // p / T        (moments.cpp:287)
   double inv = 1.0;           // 1.0 / rows   (moments.cpp:148)
 };
@@ -152,6 +155,10 @@ void count_launch();
 // FP64 tensor-core (DMMA) kernel for the top pair of orders (moment_dmma.cu)
 bool dmma_supported(const MomParams& p);
 uint32_t dmma_chunk_rows(int n, int b);
+bool tail_supported(int n, int b);  // moment_tail_kernel fits for this row length
+int tail_windows(int S, int n, int b);  // column windows of order S the tail kernel takes
+size_t tail_scratch_doubles();          // scratch the tail kernel needs (per-SM stash)
+void launch_moment_tail(const MomParams& p, cudaStream_t st);
 const char* dmma_kernel_name(int n, int b);
 // every non-empty segment of the pass sources starts on a 16-byte boundary
 // (the bulk copies' requirement; rows themselves are 16-byte multiples

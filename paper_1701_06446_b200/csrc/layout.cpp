@@ -1,6 +1,8 @@
 #include "layout.hpp"
 
 #include <algorithm>
+#include <map>
+#include <tuple>
 #include <cstdlib>
 #include <array>
 #include <numeric>
@@ -243,7 +245,7 @@ int ShardPlan::owner(const int* jp) const {
 }
 
 void MomentPlan::build_dmma(int S_, int n_, int b_, const Layout& top, const Layout* low, uint64_t scratch,
-                            const ShardPlan* shard, int shard_index) {
+                            int tail_windows, const ShardPlan* shard, int shard_index) {
   S = S_;
   L = S_ - 1;
   n = n_;
@@ -270,18 +272,75 @@ void MomentPlan::build_dmma(int S_, int n_, int b_, const Layout& top, const Lay
     }
   }
   const int nh = (n + 7) / 8;
-  for (int h = 0; h < nh; ++h) {
+  auto owned = [&](const std::array<uint16_t, 6>& pi) {
+    if (!shard || shard->count <= 1) return true;
+    int jp[3] = {0, 0, 0};
+    for (int k = 0; k < shard->plen; ++k) jp[k] = pi[k] / b;
+    return shard->owner(jp) == shard_index;  // else another shard's blocks
+  };
+  // the last window (columns [8h, n), at most one 8-wide tile): CUDA-core
+  // tasks, grouped by the first last index s so a warp's lanes share the
+  // loop structure
+  tail.clear();
+  tail_rows.clear();
+  // whole 8-column chunks right of a window are needed by the rectangle
+  // tasks: a second tail window only when n is a multiple of 8
+  tail_windows = std::max(0, std::min({tail_windows, nh, n % 8 == 0 ? 2 : 1}));
+  const int nh_dmma = nh - tail_windows;
+  {
+    // tasks grouped by (kind, run length, s) so a warp's lanes share them
+    std::map<std::tuple<int, int, int>, std::vector<TailTask>> groups;
+    int t[8];
+    for (int h = nh_dmma; h < nh; ++h) {
+      const int lo = 8 * h, hi = std::min(8 * h + 8, n);
+      for (const auto& pi : pis) {
+        const int last = pi[LM1 - 1];
+        if (last >= hi || !owned(pi)) continue;
+        const int s = std::max(last, lo);
+        const uint32_t row0 = static_cast<uint32_t>(tail_rows.size());
+        for (int k = 0; k < LM1; ++k) t[k] = pi[k];
+        for (int a = s; a < hi; ++a) {
+          t[LM1] = a;
+          tail_rows.push_back(make_row(t, top, low));
+        }
+        TailTask tk{};
+        for (int k = 0; k < 6; ++k) tk.pidx[k] = pi[k];
+        tk.s = static_cast<uint16_t>(s);
+        tk.e = static_cast<uint16_t>(hi);
+        tk.c0 = static_cast<uint16_t>(s);
+        tk.kind = TAIL_TRI;
+        tk.row0 = row0;
+        groups[{TAIL_TRI, hi - s, s}].push_back(tk);
+        // the full 8-column chunks right of the window, by sub-runs of <= 4
+        for (int c0 = hi; c0 < n; c0 += 8)
+          for (int a = s; a < hi;) {
+            const int e = std::min(hi, std::max(a + 1, ((a + 4) / 4) * 4));  // 4-aligned sub-runs
+            TailTask r = tk;
+            r.s = static_cast<uint16_t>(a);
+            r.e = static_cast<uint16_t>(e);
+            r.c0 = static_cast<uint16_t>(c0);
+            r.kind = TAIL_RECT;
+            r.row0 = row0 + static_cast<uint32_t>(a - s);
+            groups[{TAIL_RECT, e - a, a}].push_back(r);
+            a = e;
+          }
+      }
+    }
+    for (auto& [key, v] : groups) {
+      for (const auto& tk : v) tail.push_back(tk);
+      TailTask pad = v.front();
+      pad.row0 = kNoRow;
+      for (size_t k = v.size(); k % 32; ++k) tail.push_back(pad);
+    }
+  }
+  for (int h = 0; h < nh_dmma; ++h) {
     const int hi = std::min(8 * h + 8, n);
     const uint32_t rs0 = static_cast<uint32_t>(pairs.size() / 32);
     int t[8];
     for (const auto& pi : pis) {
       const int last = pi[LM1 - 1];
       if (last >= hi) continue;  // every row of this window has i_L < i_{L-1}
-      if (shard && shard->count > 1) {
-        int jp[3] = {0, 0, 0};
-        for (int k = 0; k < shard->plen; ++k) jp[k] = pi[k] / b;
-        if (shard->owner(jp) != shard_index) continue;  // another shard's blocks
-      }
+      if (!owned(pi)) continue;
       for (int k = 0; k < LM1; ++k) t[k] = pi[k];
       // pairs (a, a + 1) start at even a (16-byte aligned column pairs: the
       // producer loads x[a0], x[a0 + 1] with one LDS.128); when the first
@@ -389,6 +448,10 @@ void MomentPlan::upload() {
     h2d_sync(d_rows.ptr, rows.data(), d_rows.bytes());
   if (!tiles.empty())
     h2d_sync(d_tiles.ptr, tiles.data(), d_tiles.bytes());
+  d_tail.alloc(tail.size());
+  d_tail_rows.alloc(tail_rows.size());
+  if (!tail.empty()) h2d_sync(d_tail.ptr, tail.data(), d_tail.bytes());
+  if (!tail_rows.empty()) h2d_sync(d_tail_rows.ptr, tail_rows.data(), d_tail_rows.bytes());
 }
 
 }  // namespace csb

@@ -64,6 +64,22 @@ struct DmmaPair {
 };
 static_assert(sizeof(DmmaPair) == 16, "DmmaPair layout");
 
+// One task of the CUDA-core kernel for the narrowest column windows
+// (moment_tail_kernel): prefix pi = (i_1..i_{L-1}) and a run of last
+// indices i_L in [s, e).  TAIL_TRI: the run spans the rest of its window and
+// the task covers the columns [i_L, e) of each row plus the rows' order-L
+// sums; TAIL_RECT: e - s <= 4 and the 8 columns [c0, c0 + 8) right of the
+// window.  tail_rows[row0 + i] is the PrefixRow of (pi, s + i); padding
+// tasks (whole warps share kind and run length) have row0 == kNoRow.
+constexpr uint32_t kNoRow = 0xffffffffu;
+constexpr uint16_t TAIL_TRI = 0, TAIL_RECT = 1;
+struct TailTask {
+  uint16_t pidx[6];
+  uint16_t s, e, c0, kind;
+  uint32_t row0;
+};
+static_assert(sizeof(TailTask) == 24, "TailTask layout");
+
 // DFMA kernel: rows [row0, row0 + nrows) of the row table, columns
 // [col0, col0 + ncols).  DMMA kernel: row sets [row0, row0 + nrows) (64
 // prefix-row slots / 32 pairs each), column tiles of 8 starting at col0,
@@ -103,14 +119,21 @@ struct MomentPlan {
   bool dmma = false;  // tiles are for moment_top_dmma_kernel
   std::vector<DmmaPair> pairs;  // DMMA: 32 per row set
   DevBuf<DmmaPair> d_pairs;
+  // DMMA plans: the narrowest column windows run on the CUDA cores instead
+  std::vector<TailTask> tail;
+  std::vector<PrefixRow> tail_rows;
+  DevBuf<TailTask> d_tail;
+  DevBuf<PrefixRow> d_tail_rows;
   void build(int S, int n, int b, const Layout& top, const Layout* low, int threads);
   // Tiles for the DMMA kernel.  Per column window h, the canonical prefix
   // rows with 8h <= i_L < 8h + 8 are packed in pairs (lexicographic pi, then
   // i_L), 32 pairs = 64 row slots per row set; rows[64 s + 2 j + e] is the
   // PrefixRow of element e of pair j of row set s (vprime == 0: masked).
   // Columns [8h, n) are covered in tiles of 8.
+  // tail_windows: the last so many column windows become TailTasks
+  // (moment_tail_kernel) instead of DMMA tiles
   void build_dmma(int S, int n, int b, const Layout& top, const Layout* low, uint64_t scratch_per_tile,
-                  const ShardPlan* shard = nullptr, int shard_index = 0);
+                  int tail_windows, const ShardPlan* shard = nullptr, int shard_index = 0);
   void upload();
 
  private:

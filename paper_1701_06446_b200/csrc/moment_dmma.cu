@@ -37,6 +37,8 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstdio>
+#include <map>
+#include <mutex>
 
 #include "kernels.cuh"
 
@@ -610,6 +612,195 @@ __global__ void __launch_bounds__(THREADS, 1) moment_top_dmma_kernel(const MomPa
   }
 }
 
+// ---------------------------------------------------------------------------
+// The narrowest column windows on the CUDA cores.  The prefix rows (pi, i_L)
+// of window h (8h <= i_L < 8h + 8) need the columns [i_L, n); in the last
+// window that is a triangle inside one 8-wide tile, which the DMMA path
+// executes about twice over while its producers set the pace (13.7 TFLOP/s
+// executed at cfg2, half of it useful).  Here a thread owns one task:
+//  * triangle (TAIL_TRI): a prefix pi and the run of its last indices
+//    i_L in [s, e) = [max(i_{L-1}, 8h), min(8h + 8, n)), with every column
+//    i_d in [i_L, e), plus the order-(d-1) sums of the run's rows;
+//  * rectangle (TAIL_RECT): a sub-run [s, e) of at most 4 last indices
+//    times the 8 columns [c0, c0 + 8) right of the window.
+// Per data row it forms P = x[pi_1] ... x[pi_{L-1}] (moments.cpp:55, left
+// to right), q = P x[i_L] for each i_L of the run, adds q to the order-(d-1)
+// sum (moments.cpp:44) and chains acc = fma(q, x[i_d], acc) over its
+// columns (moments.cpp:47) -- the reference's own per-element sequence, so
+// M_d and M_{d-1} stay bit-exact.  Tasks are grouped on the host so the
+// lanes of a warp share the kind and run length (compile-time accumulator
+// shapes) and the first last index s.  Rows stream through a TMA bulk-copy
+// ring like the DMMA kernel's (zero rows past the end of a pass add exact
+// zeros); the incoming pass's means are stashed in shared memory.
+constexpr int TAIL_THREADS = 384;  // 3 warps per SM sub-partition (one CTA per SM)
+constexpr int TAIL_WARPS = TAIL_THREADS / 32;
+constexpr int TAIL_KC = 32;     // data rows per chunk
+constexpr int TAIL_STASH = 44;  // doubles per thread: 36 + 8 (triangle of 8), 32 (rectangle 4 x 8)
+// The stash lives in global memory, one slot per SM: the kernel's shared
+// memory request (> half an SM's) keeps it at one resident CTA per SM.
+constexpr size_t TAIL_MIN_SMEM = 120 * 1024;
+
+__device__ __forceinline__ uint32_t sm_id() {
+  uint32_t s;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
+  return s;
+}
+
+template <int N, int LM1, int RL, int W, bool TRI>
+__device__ __forceinline__ void tail_run(const MomParams& P, const TailTask& tk, const Ring& g, double* stash) {
+  // TRI: the run is the column range, W == RL; else RL run rows x W columns
+  constexpr int NA = TRI ? RL * (RL + 1) / 2 : RL * W;
+  constexpr int NS = TRI ? RL : 0;  // order-(d-1) sums
+  const int n = N ? N : P.n;  // compile-time row length: immediate shared-memory offsets
+  const int s = tk.s, c0 = TRI ? tk.s : tk.c0;
+  const int tid = threadIdx.x;
+  int pidx[LM1];
+#pragma unroll
+  for (int u = 0; u < LM1; ++u) pidx[u] = tk.pidx[u];
+  double acc[NA], sum[NS > 0 ? NS : 1];
+#pragma unroll
+  for (int a = 0; a < NA; ++a) acc[a] = 0.0;
+#pragma unroll
+  for (int i = 0; i < NS; ++i) sum[i] = 0.0;
+  const bool update = P.npass == 2;
+  const size_t stage_elems = static_cast<size_t>(TAIL_KC) * n;
+  Cursor cur;
+  for (uint32_t c = 0; c < g.chunks; ++c) {
+    mbar_wait(g.xfull + cur.st, cur.ph);
+    const double* xs = g.xs + cur.st * stage_elems;
+#pragma unroll 8  // (measured: 2 -> 8 rows per iteration 7.38 -> 7.02 ms at cfg2)
+    for (int r = 0; r < TAIL_KC; ++r) {
+      const double* xr = xs + r * n;
+      double pv = xr[pidx[0]];
+#pragma unroll
+      for (int u = 1; u < LM1; ++u) pv = __dmul_rn(pv, xr[pidx[u]]);
+      double xa[RL], xc[W];
+#pragma unroll
+      for (int k = 0; k < RL; ++k) xa[k] = xr[s + k];
+#pragma unroll
+      for (int k = 0; k < W; ++k) xc[k] = TRI ? xa[k < RL ? k : 0] : xr[c0 + k];
+      int a = 0;
+#pragma unroll
+      for (int i = 0; i < RL; ++i) {
+        const double q = __dmul_rn(pv, xa[i]);
+        if (TRI) sum[i < NS ? i : 0] = __dadd_rn(sum[i < NS ? i : 0], q);
+#pragma unroll
+        for (int j = TRI ? i : 0; j < W; ++j, ++a) acc[a] = __fma_rn(q, xc[j], acc[a]);
+      }
+    }
+    release_chunk(P, g, c, cur.st);
+    if (update && c + 1 == g.cpp) {  // end of the incoming pass: stash its means
+#pragma unroll
+      for (int a = 0; a < NA; ++a) {
+        stash[a * P.stash_stride + tid] = __dmul_rn(acc[a], P.inv);
+        acc[a] = 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < NS; ++i) {
+        stash[(NA + i) * P.stash_stride + tid] = __dmul_rn(sum[i], P.inv);
+        sum[i] = 0.0;
+      }
+    }
+    cur.next(g.stages);
+  }
+  if (tk.row0 == kNoRow) return;
+  // epilogue: the canonical entries (pi, i_L, i_d) of M_d and (pi, i_L) of M_{d-1}
+  const int b = P.b;
+  const double cc = P.c;
+  double* __restrict__ top = P.top;
+  double* __restrict__ low = P.low;
+  int a = 0;
+#pragma unroll
+  for (int i = 0; i < RL; ++i) {
+    const PrefixRow& row = P.rows[tk.row0 + i];
+    const uint64_t tb = row.top_base;
+    const uint64_t vp = row.vprime, po = row.poff;
+    const int J = (s + i) / b;
+#pragma unroll
+    for (int j = TRI ? i : 0; j < W; ++j, ++a) {
+      const int col = c0 + j;
+      const int jd = col / b;
+      const size_t o = tb + vp * b * (jd - J) + po * ext_of(jd, n, b) + (col - jd * b);
+      const double v = __dmul_rn(acc[a], P.inv);
+      top[o] = update ? __fma_rn(cc, __dsub_rn(stash[a * P.stash_stride + tid], v), top[o]) : v;  // a - b
+    }
+    if (NS > 0 && low) {
+      const double v = __dmul_rn(sum[i < NS ? i : 0], P.inv);
+      low[row.low_off] =
+          update ? __fma_rn(cc, __dsub_rn(stash[(NA + i) * P.stash_stride + tid], v), low[row.low_off]) : v;
+    }
+  }
+}
+
+template <int N, int LM1>
+__device__ __forceinline__ void tail_dispatch(const MomParams& P, const TailTask& tk, const Ring& g, double* stash) {
+  const int rl = tk.e - tk.s;
+  if (tk.kind == TAIL_TRI) {
+    switch (rl) {
+      case 1: tail_run<N, LM1, 1, 1, true>(P, tk, g, stash); break;
+      case 2: tail_run<N, LM1, 2, 2, true>(P, tk, g, stash); break;
+      case 3: tail_run<N, LM1, 3, 3, true>(P, tk, g, stash); break;
+      case 4: tail_run<N, LM1, 4, 4, true>(P, tk, g, stash); break;
+      case 5: tail_run<N, LM1, 5, 5, true>(P, tk, g, stash); break;
+      case 6: tail_run<N, LM1, 6, 6, true>(P, tk, g, stash); break;
+      case 7: tail_run<N, LM1, 7, 7, true>(P, tk, g, stash); break;
+      case 8: tail_run<N, LM1, 8, 8, true>(P, tk, g, stash); break;
+      default: break;
+    }
+  } else {
+    switch (rl) {
+      case 1: tail_run<N, LM1, 1, 8, false>(P, tk, g, stash); break;
+      case 2: tail_run<N, LM1, 2, 8, false>(P, tk, g, stash); break;
+      case 3: tail_run<N, LM1, 3, 8, false>(P, tk, g, stash); break;
+      case 4: tail_run<N, LM1, 4, 8, false>(P, tk, g, stash); break;
+      default: break;
+    }
+  }
+}
+
+template <int N, int LM1>
+__global__ void __launch_bounds__(TAIL_THREADS, 1) moment_tail_kernel(const MomParams P) {
+  extern __shared__ __align__(128) double smem[];
+  __shared__ __align__(8) uint64_t bars[MAX_STAGES];
+  __shared__ uint32_t rel[MAX_STAGES];
+  const int warp = threadIdx.x >> 5;
+  const uint32_t live = min(static_cast<uint32_t>(TAIL_WARPS), P.tail_warps - blockIdx.x * TAIL_WARPS);
+  Ring g;
+  g.stages = static_cast<uint32_t>(P.stages);
+  g.xs = smem;
+  g.xfull = bars;
+  g.rel = rel;
+  g.kc = TAIL_KC;
+  g.cpp = (P.K + TAIL_KC - 1) / TAIL_KC;
+  g.chunks = g.cpp * P.npass;
+  g.active = live;
+  const uint32_t smid = sm_id();
+  if (smid >= P.stash_slots) __trap();  // the scratch is sized by %nsmid
+  double* stash = P.scratch + static_cast<size_t>(smid) * TAIL_THREADS;
+  if (threadIdx.x == 0) {
+    for (uint32_t s = 0; s < g.stages; ++s) {
+      mbar_init(g.xfull + s, 1);
+      rel[s] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (uint32_t i = 0; i < g.chunks && i < g.stages; ++i) issue_chunk(P, g, i, i);
+  }
+  __syncthreads();
+  if (static_cast<uint32_t>(warp) >= live) return;
+  const TailTask tk = P.tail[(static_cast<size_t>(blockIdx.x) * TAIL_WARPS + warp) * 32 + (threadIdx.x & 31)];
+  tail_dispatch<N, LM1>(P, tk, g, stash);
+}
+
+size_t tail_smem_bytes(int n, int stages) {
+  return std::max(TAIL_MIN_SMEM, sizeof(double) * static_cast<size_t>(stages) * TAIL_KC * n);
+}
+
+__global__ void nsmid_kernel(uint32_t* out) {
+  uint32_t v;
+  asm volatile("mov.u32 %0, %%nsmid;" : "=r"(v));
+  *out = v;
+}
+
 // Symmetric copies of the canonical entries written above, one CTA per
 // stored block with equal neighbouring coordinates (symten.cpp:195-220):
 // entry o of block j holds the value of the entry with o sorted within each
@@ -740,6 +931,76 @@ DmmaKernel pick_dmma_kernel(int n, int b) {
 
 const char* dmma_kernel_name(int n, int b) { return pick_dmma_kernel(n, b).name; }
 
+namespace {
+
+int tail_stages(int n) {
+  int st = MAX_STAGES;
+  while (st > 0 && tail_smem_bytes(n, st) > kSmemLimit) --st;
+  return st;
+}
+
+uint32_t sm_id_slots() {  // %nsmid of the current device (SM ids can exceed the SM count)
+  static std::mutex mu;
+  static std::map<int, uint32_t> cache;
+  int dev = 0;
+  CSB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  uint32_t* d = nullptr;
+  uint32_t v = 0;
+  CSB_CUDA(cudaMalloc(&d, sizeof(uint32_t)));
+  nsmid_kernel<<<1, 1>>>(d);
+  CSB_CUDA(cudaMemcpy(&v, d, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  CSB_CUDA(cudaFree(d));
+  cache[dev] = v;
+  return v;
+}
+
+}  // namespace
+
+bool tail_supported(int n, int /*b*/) { return tail_stages(n) >= 2; }
+
+size_t tail_scratch_doubles() { return static_cast<size_t>(sm_id_slots()) * TAIL_THREADS * TAIL_STASH; }
+
+int tail_windows(int S, int n, int b) {
+  if (S < 3 || S > 6 || !tail_supported(n, b)) return 0;
+  // one triangle task per (S-2)-prefix pi of the last window: below ~4 warps
+  // per SM the CUDA-core kernel is latency-bound and the DMMA tile wins
+  double tasks = 1.0;
+  for (int k = 1; k <= S - 2; ++k) tasks = tasks * (n + k - 1) / k;  // C(n + S - 3, S - 2)
+  if (tasks < 4.0 * 148 * 32) return 0;
+  return 2;  // the last two windows (one when n is not a multiple of 8)
+}
+
+void launch_moment_tail(const MomParams& p_in, cudaStream_t st) {
+  if (p_in.tail_warps == 0) return;
+  MomParams p = p_in;
+  p.stages = tail_stages(p.n);
+  if (p.stages < 2) fail(CSB_EINVAL, "moment_tail: rows too wide for the staging ring");
+  p.stash_slots = sm_id_slots();
+  p.stash_stride = p.stash_slots * TAIL_THREADS;  // doubles between a thread's stashed values
+  const size_t smem = tail_smem_bytes(p.n, p.stages);
+  using K = void (*)(MomParams);
+  K kern = nullptr;
+  // specialised row lengths of the BASELINE configs (orders 4 and 6); generic otherwise
+  const int lm1 = p.L - 1;
+  if (p.n == 48 && lm1 == 4) kern = moment_tail_kernel<48, 4>;
+  else if (p.n == 96 && lm1 == 4) kern = moment_tail_kernel<96, 4>;
+  else if (p.n == 96 && lm1 == 2) kern = moment_tail_kernel<96, 2>;
+  else if (p.n == 256 && lm1 == 2) kern = moment_tail_kernel<256, 2>;
+  else if (lm1 == 1) kern = moment_tail_kernel<0, 1>;
+  else if (lm1 == 2) kern = moment_tail_kernel<0, 2>;
+  else if (lm1 == 3) kern = moment_tail_kernel<0, 3>;
+  else if (lm1 == 4) kern = moment_tail_kernel<0, 4>;
+  else fail(CSB_EINVAL, "moment_tail: order out of range");
+  ensure_smem(kern, smem);
+  const unsigned grid = (p.tail_warps + TAIL_WARPS - 1) / TAIL_WARPS;
+  kern<<<grid, TAIL_THREADS, smem, st>>>(p);
+  CSB_CUDA(cudaGetLastError());
+  count_launch();
+}
+
 // per tile: the incoming pass's means (64 values per consumer thread)
 size_t dmma_scratch_per_tile() { return static_cast<size_t>(CWARPS) * 32 * 16 * MAXNC; }
 
@@ -755,7 +1016,9 @@ bool dmma_supported(const MomParams& p) {
 
 // data rows per chunk of the launched kernel: the zero-row source of a
 // pass's last chunk must hold this many rows
-uint32_t dmma_chunk_rows(int n, int b) { return 4u * static_cast<uint32_t>(chunk_steps(n, b)); }
+uint32_t dmma_chunk_rows(int n, int b) {
+  return std::max<uint32_t>(4u * static_cast<uint32_t>(chunk_steps(n, b)), TAIL_KC);  // either kernel's chunk
+}
 
 void launch_mirror(int S, double* m, const LayoutDev& lay, const uint32_t* blocks, uint32_t nblocks, int n, int b,
                    const uint2* lists, const uint32_t* list_off, cudaStream_t st) {

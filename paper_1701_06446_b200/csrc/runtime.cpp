@@ -158,7 +158,8 @@ std::shared_ptr<MomentPlan> get_plan(Device& dev, int S, int n, int b, bool dmma
   if (!slot) {
     auto p = std::make_shared<MomentPlan>();
     if (dmma)
-      p->build_dmma(S, n, b, top->host, low ? &low->host : nullptr, dmma_scratch_per_tile(), sp, shard_index);
+      p->build_dmma(S, n, b, top->host, low ? &low->host : nullptr, dmma_scratch_per_tile(), tail_windows(S, n, b), sp,
+                    shard_index);
     else
       p->build(S, n, b, top->host, low ? &low->host : nullptr, kMomThreads);
     p->upload();
@@ -573,6 +574,11 @@ struct Scratch {
     if (buf.count < count) buf.alloc(count);
     return buf.ptr;
   }
+  DevBuf<double> tail;  // the tail kernel's per-SM stash (beside the DMMA kernel's scratch)
+  double* get_tail(uint64_t count) {
+    if (tail.count < count) tail.alloc(count);
+    return tail.ptr;
+  }
   DevBuf<double> zeros;
   const double* get_zeros(uint64_t count) {
     if (zeros.count < count) {
@@ -738,6 +744,15 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
       {
         ProfScope ps("moment_top", st);  // the DMMA kernel alone (bench roofline)
         launch_moment_top_dmma(p, static_cast<int>(ntiles), st);
+      }
+      if (!plan->tail.empty()) {
+        ProfScope ps("moment_tail", st);  // the last column window on the CUDA cores
+        MomParams pt = p;
+        pt.rows = plan->d_tail_rows.ptr;
+        pt.tail = plan->d_tail.ptr;
+        pt.tail_warps = static_cast<uint32_t>(plan->tail.size() / 32);
+        pt.scratch = sc.get_tail(tail_scratch_doubles());
+        launch_moment_tail(pt, st);
       }
       if (side_launch) side_launch();
       ProfScope pm("mirror", st);
