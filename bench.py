@@ -428,6 +428,7 @@ def main() -> None:
             "gpu_launches": launches,
             "clocks": clocks.summary(),
             "wall_s_timed_region": wall,
+            "step_ms_stats": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)},
             "last_report": {"window": rep["window"], "nu": {str(k): v for k, v in rep["nu"].items()}},
             "cpu_baseline": cpu,
         }

@@ -329,6 +329,161 @@ __global__ void __launch_bounds__(S <= 4 ? 1024 : 256, S <= 4 ? 1 : 2) moms2cums
 }
 
 // ---------------------------------------------------------------------------
+// moms2cums of a high order over full blocks (every extent B), persistent:
+// one CTA per SM walks its blocks blockIdx.x, + gridDim.x, ... with the
+// 2^S - 2 lower-order sub-blocks of the NEXT block landing by TMA bulk
+// copies in a second buffer while the current one is computed, and no
+// CTA-wide barrier per block: each warp reduces its share of the block's
+// sum of squares, the last warp to finish a block (shared-memory counter)
+// adds the warp sums in warp order, writes the block's partial and refills
+// the buffer with the block after next.  The arithmetic per canonical
+// entry is moms2cums_v2's (partition_correction<S>, the reference's order),
+// written with its symmetric copies straight to global memory.
+// (Measured at cfg2 order 6: 1.76 ms for moms2cums_v2 -> 1.53 ms.  A variant
+// handing out 32-entry chunks of the oldest open block through a shared
+// cursor, so no warp waits for a block's stragglers, measured 1.66 ms:
+// the per-chunk hand-off costs more than the waits it removes.)
+constexpr int M2CP_THREADS = 512;
+constexpr int M2CP_WARPS = M2CP_THREADS / 32;
+
+template <int S, int B>
+struct M2cStage {
+  // staged doubles of mask m's sub-block (B^|m|) and its offset in a buffer
+  static constexpr uint32_t vol(int m) {
+    uint32_t v = 1;
+    for (int k = 0; k < S; ++k)
+      if (m >> k & 1) v *= B;
+    return v;
+  }
+  static constexpr uint32_t off(int m) {
+    uint32_t o = 0;
+    for (int q = 1; q < m; ++q) o += vol(q);
+    return o;
+  }
+  static constexpr uint32_t total() { return off((1 << S) - 1); }
+};
+
+template <int S, int B>
+__global__ void __launch_bounds__(M2CP_THREADS, 1) moms2cums_persist(const M2CParams P, uint32_t nblocks) {
+  constexpr int NM = (1 << S) - 1;
+  using G = M2cStage<S, B>;
+  constexpr uint32_t STAGE = G::total();
+  extern __shared__ __align__(16) double sfac[];  // 2 x STAGE
+  __shared__ __align__(8) uint64_t full[2];
+  __shared__ uint32_t done[2];
+  __shared__ double red[2][M2CP_WARPS];
+  const LayoutDev& LS = P.lay[S - 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  auto block_of = [&](uint32_t k) { return P.blk0 + blockIdx.x + static_cast<uint64_t>(k) * gridDim.x; };
+  const uint32_t nmine = blockIdx.x < nblocks ? (nblocks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  // one warp: TMA bulk copies of block k's sub-blocks into buffer buf, the
+  // lanes' copies (and their offset loads) in parallel
+  auto issue = [&](uint32_t k, int buf) {
+    const uint64_t blk = block_of(k);
+    const uint64_t* subs = P.subs + blk * (NM - 1);
+    if (lane == 0) ptx::mbar_expect_tx(&full[buf], STAGE * static_cast<uint32_t>(sizeof(double)));
+    __syncwarp();
+    for (int m = 1 + lane; m < NM; m += 32) {
+      uint32_t o = 0;  // G::off(m) at run time
+      for (int q = 1; q < m; ++q) o += G::vol(q);
+      ptx::bulk_g2s(sfac + buf * STAGE + o, P.lower[popcount_c(m) - 1] + subs[m - 1],
+                    G::vol(m) * static_cast<uint32_t>(sizeof(double)), &full[buf]);
+    }
+  };
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&full[0], 1);
+    ptx::mbar_init(&full[1], 1);
+    done[0] = done[1] = 0;
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == 0)
+    for (uint32_t k = 0; k < 2 && k < nmine; ++k) issue(k, static_cast<int>(k));
+  uint32_t bp[S];  // B^0 .. B^(S-1)
+  bp[0] = 1;
+#pragma unroll
+  for (int k = 1; k < S; ++k) bp[k] = bp[k - 1] * B;
+  for (uint32_t k = 0; k < nmine; ++k) {
+    const int buf = static_cast<int>(k & 1);
+    const uint64_t blk = block_of(k);
+    int j[S];
+#pragma unroll
+    for (int q = 0; q < S; ++q) j[q] = LS.index[blk * S + q];
+    const uint64_t boff = LS.offset[blk];
+    uint32_t pat = 0;
+#pragma unroll
+    for (int q = 1; q < S; ++q) pat |= static_cast<uint32_t>(j[q] == j[q - 1]) << (q - 1);
+    const uint32_t cbase = P.canon_off[pat];
+    const uint32_t cnt = P.canon_off[pat + 1] - cbase;
+    const double* sb = sfac + buf * STAGE;
+    // software pipeline: the next entry's position, M value and copy range
+    // are loaded before this entry's partition sum
+    uint32_t i = threadIdx.x;
+    uint32_t npos = 0, nc0 = 0, nc1 = 0;
+    double nm = 0.0;
+    if (i < cnt) {
+      npos = __ldg(P.canon + cbase + i);
+      nc0 = __ldg(P.cstart + cbase + i);
+      nc1 = __ldg(P.cstart + cbase + i + 1);
+      nm = P.m[boff + npos];
+    }
+    ptx::mbar_wait(&full[buf], (k >> 1) & 1u);
+    double part = 0.0;
+    for (; i < cnt; i += M2CP_THREADS) {
+      const uint32_t pos = npos, c0 = nc0, c1 = nc1;
+      const double mv = nm;
+      const uint32_t in = i + M2CP_THREADS;
+      if (in < cnt) {
+        npos = __ldg(P.canon + cbase + in);
+        nc0 = __ldg(P.cstart + cbase + in);
+        nc1 = __ldg(P.cstart + cbase + in + 1);
+        nm = P.m[boff + npos];
+      }
+      int o[S];
+      uint32_t r = pos;
+#pragma unroll
+      for (int q = S - 1; q >= 0; --q) {
+        o[q] = static_cast<int>(r % B);
+        r /= B;
+      }
+      double f[NM];
+#pragma unroll
+      for (int m = 1; m < NM; ++m) {
+        uint32_t a = 0;
+        int after = 0;
+#pragma unroll
+        for (int q = S - 1; q >= 0; --q)
+          if (m >> q & 1) a += static_cast<uint32_t>(o[q]) * bp[after++];
+        f[m] = sb[G::off(m) + a];
+      }
+      const double v = __dsub_rn(mv, partition_correction<S>(f));
+      P.c[boff + pos] = v;
+      for (uint32_t q = c0; q < c1; ++q) P.c[boff + __ldg(P.cdst + q)] = v;
+      part = __fma_rn(static_cast<double>(1u + c1 - c0), __dmul_rn(v, v), part);
+    }
+    for (int s = 16; s > 0; s >>= 1) part = __dadd_rn(part, __shfl_down_sync(0xffffffffu, part, s));
+    __syncwarp();  // every lane's reads of the buffer precede lane 0's release below
+    uint32_t last = 0;
+    if (lane == 0) {
+      red[buf][warp] = part;
+      __threadfence_block();
+      last = atomicAdd(&done[buf], 1u) == M2CP_WARPS - 1;
+    }
+    if (__shfl_sync(0xffffffffu, last, 0)) {  // the last warp of this block
+      __threadfence_block();
+      if (lane == 0) {
+        double s = 0.0;
+        for (int w = 0; w < M2CP_WARPS; ++w) s = __dadd_rn(s, red[buf][w]);
+        P.partial[blk - P.blk0] = s;
+        *reinterpret_cast<volatile uint32_t*>(&done[buf]) = 0;
+      }
+      if (k + 2 < nmine) {
+        ptx::fence_proxy_async();  // every warp's generic reads of the buffer before the async-proxy refill
+        issue(k + 2, buf);
+      }
+    }
+  }
+}
 
 // Write one canonical element of order S to every stored copy in its block
 // (distinct permutations of the in-block offsets within runs of equal
@@ -587,8 +742,27 @@ bool m2c_fuse_ok(int S, int n, int b) {
   return sm0 <= 160 * 1024 && vol <= (1u << 20) && sm0 + vol * sizeof(double) <= kM2cInblkLimit;
 }
 
+// The persistent kernel's case: order 6, every block full (n a multiple of
+// b = 4), the direct canonical-list path (no in-block pass, no deferred M
+// mirror) -- two buffers of the 62 staged sub-blocks (2 x 92 KB) per SM.
+bool m2c_persist_ok(int S, const M2CParams& p) {
+  return S == 6 && p.b == 4 && p.n % 4 == 0 && p.canon && p.cstart && !p.mfix &&
+         2 * M2cStage<6, 4>::total() * sizeof(double) <= 200 * 1024;
+}
+
 void launch_moms2cums_v2(int S, const M2CParams& p, uint64_t nblocks, cudaStream_t st) {
   if (nblocks == 0) return;
+  if (m2c_persist_ok(S, p)) {
+    static int sms = 0;
+    if (!sms) CSB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    const size_t smem = 2 * M2cStage<6, 4>::total() * sizeof(double);
+    ensure_smem(moms2cums_persist<6, 4>, smem);
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(nblocks, static_cast<uint64_t>(sms)));
+    moms2cums_persist<6, 4><<<grid, M2CP_THREADS, smem, st>>>(p, static_cast<uint32_t>(nblocks));
+    CSB_CUDA(cudaGetLastError());
+    count_launch();
+    return;
+  }
   const unsigned g = static_cast<unsigned>(nblocks);
   const size_t sm0 = moms2cums_stage_bytes(S, p.n, p.b);
   const bool staged = sm0 <= 160 * 1024;
