@@ -191,43 +191,48 @@ void require_sorted(std::span<const int> t, const char* what) {
 
 }  // namespace
 
+// table_[rem][v] counts the non-decreasing (rem+1)-tuples whose first entry
+// is below v: summing C(alphabet - u + rem - 1, rem) over u < v telescopes
+// (hockey stick) to C(alphabet + rem, rem + 1) - C(alphabet - v + rem, rem + 1),
+// so every entry is one closed form.
 MultisetRanker::MultisetRanker(int alphabet, int order) : alphabet_(alphabet), order_(order) {
   if (alphabet < 1 || order < 1)
     throw std::invalid_argument("MultisetRanker: alphabet and order must be positive");
   count_ = binomial_u64(alphabet + order - 1, order);
-  table_.assign(static_cast<std::size_t>(order) * (alphabet + 1), 0);
+  const std::size_t stride = static_cast<std::size_t>(alphabet) + 1;
+  table_.resize(static_cast<std::size_t>(order) * stride);
   for (int rem = 0; rem < order; ++rem) {
-    std::uint64_t acc = 0;
-    for (int v = 0; v <= alphabet; ++v) {
-      table_[static_cast<std::size_t>(rem) * (alphabet + 1) + v] = acc;
-      if (v < alphabet) acc += binomial_u64(alphabet - v + rem - 1, rem);
-    }
+    const std::uint64_t all = binomial_u64(alphabet + rem, rem + 1);
+    for (int v = 0; v <= alphabet; ++v)
+      table_[rem * stride + v] = all - binomial_u64(alphabet - v + rem, rem + 1);
   }
 }
 
 std::uint64_t MultisetRanker::rank(std::span<const int> tuple) const {
   if (static_cast<int>(tuple.size()) != order_)
     throw std::invalid_argument("MultisetRanker::rank: wrong tuple length");
-  int lo = 0;
-  for (int v : tuple) {
-    if (v < lo || v >= alphabet_)
-      throw std::out_of_range("MultisetRanker::rank: tuple not sorted or out of range");
-    lo = v;
-  }
+  const bool sorted_in_range =
+      std::is_sorted(tuple.begin(), tuple.end()) && (tuple.empty() || (tuple.front() >= 0 && tuple.back() < alphabet_));
+  if (!sorted_in_range) throw std::out_of_range("MultisetRanker::rank: tuple not sorted or out of range");
   return rank_unchecked(tuple.data());
 }
 
+// Position by position, the largest value whose table offset (relative to
+// the previous entry) does not exceed the remaining rank: a binary search
+// per position over the monotone table row.
 void MultisetRanker::unrank(std::uint64_t r, std::span<int> out) const {
   if (static_cast<int>(out.size()) != order_)
     throw std::invalid_argument("MultisetRanker::unrank: wrong output length");
   if (r >= count_) throw std::out_of_range("MultisetRanker::unrank: rank too large");
-  auto T = [&](int row, int v) { return table_[static_cast<std::size_t>(row) * (alphabet_ + 1) + v]; };
+  const std::size_t stride = static_cast<std::size_t>(alphabet_) + 1;
   int lo = 0;
   for (int i = 0; i < order_; ++i) {
-    const int rem = order_ - 1 - i;
-    int v = lo;
-    while (r >= T(rem, v + 1) - T(rem, lo)) ++v;
-    r -= T(rem, v) - T(rem, lo);
+    const std::uint64_t* row = table_.data() + static_cast<std::size_t>(order_ - 1 - i) * stride;
+    const std::uint64_t target = row[lo] + r;
+    // first v in (lo, alphabet] with row[v] > target, minus one
+    const std::uint64_t* it = std::upper_bound(row + lo + 1, row + alphabet_ + 1, target);
+    const int v = static_cast<int>(it - row) - 1;
+    r = target - row[v];
     out[i] = v;
     lo = v;
   }
@@ -448,38 +453,40 @@ double knorm(const SymTensor& t, double k) {
   return DeviceSeries::knorm_of(t, k);
 }
 
+// Every dense position decoded (mixed radix n), its index sorted, looked
+// up in block storage.
 DenseTensor densify(const SymTensor& t) {
   DenseTensor out(t.order(), t.dim());
-  const int d = t.order(), n = t.dim();
+  const int d = t.order();
+  const std::size_t n = static_cast<std::size_t>(t.dim());
   t.data();  // host mirror
-  std::vector<int> idx(d, 0), s(d);
-  for (std::size_t pos = 0;; ++pos) {
-    s = idx;
-    std::sort(s.begin(), s.end());
-    out.values[pos] = t.at_sorted_unchecked(s.data());
-    int k = d - 1;
-    while (k >= 0 && idx[k] == n - 1) idx[k--] = 0;
-    if (k < 0) break;
-    ++idx[k];
+  std::vector<int> idx(d);
+  for (std::size_t pos = 0; pos < out.values.size(); ++pos) {
+    std::size_t rem = pos;
+    for (int k = d - 1; k >= 0; --k, rem /= n) idx[k] = static_cast<int>(rem % n);
+    std::sort(idx.begin(), idx.end());
+    out.values[pos] = t.at_sorted_unchecked(idx.data());
   }
   return out;
 }
 
+// Every stored entry read from the dense tensor at its full index (block
+// base plus the in-block offsets decoded from the entry's position).
 SymTensor from_dense(const DenseTensor& dense, int block_size) {
   SymTensor out(dense.order, dense.dim, block_size);
   const int d = dense.order;
   auto data = out.data();
-  std::vector<int> idx(d), o(d);
+  std::vector<int> idx(d);
   for (std::size_t r = 0; r < out.block_count(); ++r) {
     const BlockInfo& bi = out.block(r);
-    std::fill(o.begin(), o.end(), 0);
-    for (std::size_t pos = 0;; ++pos) {
-      for (int k = 0; k < d; ++k) idx[k] = bi.base[k] + o[k];
+    for (std::size_t pos = 0; pos < bi.volume; ++pos) {
+      std::size_t rem = pos;
+      for (int k = d - 1; k >= 0; --k) {
+        const std::size_t e = static_cast<std::size_t>(bi.extents[k]);
+        idx[k] = bi.base[k] + static_cast<int>(rem % e);
+        rem /= e;
+      }
       data[bi.offset + pos] = dense.at(idx);
-      int k = d - 1;
-      while (k >= 0 && o[k] == bi.extents[k] - 1) o[k--] = 0;
-      if (k < 0) break;
-      ++o[k];
     }
   }
   return out;
@@ -541,23 +548,39 @@ void moments_update(MomentSeries& m, const DataBatch& incoming, const DataBatch&
 
 namespace {
 
-// restricted growth strings in lexicographic order (partitions with parts
-// ordered by smallest member)
+// Restricted growth strings a (a[0] = 0, a[i] <= 1 + max(a[0..i-1])), each
+// one set partition with parts labelled by first occurrence.  next_rgs
+// steps to the lexicographic successor in place: the rightmost position
+// that can still grow is incremented and everything right of it reset to
+// 0, prefix maxima kept alongside.  Starting from all zeros this visits the
+// strings in the reference's order (cumulants.cpp:16-26).
+bool next_rgs(std::vector<int>& a, std::vector<int>& pmax) {
+  const int s = static_cast<int>(a.size());
+  for (int i = s - 1; i >= 1; --i) {
+    if (a[i] <= pmax[i - 1] && a[i] + 1 < s) {
+      ++a[i];
+      pmax[i] = std::max(pmax[i - 1], a[i]);
+      for (int k = i + 1; k < s; ++k) {
+        a[k] = 0;
+        pmax[k] = pmax[k - 1];
+      }
+      return true;
+    }
+  }
+  return false;
+}
+
+// emit(a, parts) for every restricted growth string of length s
 template <class Emit>
-void rgs(int i, int s, int maxl, std::vector<int>& a, Emit&& emit) {
-  if (i == s) {
-    emit(a, maxl + 1);
-    return;
-  }
-  for (int v = 0; v <= maxl + 1 && v < s; ++v) {
-    a[i] = v;
-    rgs(i + 1, s, std::max(maxl, v), a, emit);
-  }
+void for_each_rgs(int s, Emit&& emit) {
+  std::vector<int> a(s, 0), pmax(s, 0);
+  do emit(a, pmax[s - 1] + 1);
+  while (next_rgs(a, pmax));
 }
 
 SetPartition decode(const std::vector<int>& a, int parts) {
   SetPartition out(parts);
-  for (int i = 0; i < static_cast<int>(a.size()); ++i) out[a[i]].push_back(i);
+  for (std::size_t i = 0; i < a.size(); ++i) out[a[i]].push_back(static_cast<int>(i));
   return out;
 }
 
@@ -571,8 +594,7 @@ std::vector<SetPartition> partitions(int s, int sigma) {
   check_s(s);
   if (sigma < 1 || sigma > s) throw std::invalid_argument("partitions: sigma must be in [1, s]");
   std::vector<SetPartition> out;
-  std::vector<int> a(s, 0);
-  rgs(1, s, 0, a, [&](const std::vector<int>& g, int parts) {
+  for_each_rgs(s, [&](const std::vector<int>& g, int parts) {
     if (parts == sigma) out.push_back(decode(g, parts));
   });
   return out;
@@ -582,8 +604,7 @@ std::vector<SetPartition> partitions_at_least(int s, int min_sigma) {
   check_s(s);
   if (min_sigma < 1 || min_sigma > s) throw std::invalid_argument("partitions_at_least: min_sigma must be in [1, s]");
   std::vector<SetPartition> out;
-  std::vector<int> a(s, 0);
-  rgs(1, s, 0, a, [&](const std::vector<int>& g, int parts) {
+  for_each_rgs(s, [&](const std::vector<int>& g, int parts) {
     if (parts >= min_sigma) out.push_back(decode(g, parts));
   });
   return out;
@@ -601,8 +622,8 @@ double sym_outer_element(std::span<const int> index, const CumulantSeries& lower
   // one element's partition sum (a test hook of the reference,
   // cumulants.cpp:110-126), same order and no FMA as the device kernel
   double acc = 0.0;
-  std::vector<int> a(s, 0), sub;
-  rgs(1, s, 0, a, [&](const std::vector<int>& g, int parts) {
+  std::vector<int> sub;
+  for_each_rgs(s, [&](const std::vector<int>& g, int parts) {
     if (parts < 2) return;
     double prod = 1.0;
     for (const auto& part : decode(g, parts)) {
@@ -643,33 +664,43 @@ double nu(const CumulantSeries& c, int d) {
   return out;
 }
 
+namespace {
+
+// Standardised third / fourth central moment of one column from its first
+// four raw moments (power sums over the rows, scaled once).
+struct ColumnShape {
+  double m[5] = {1.0, 0.0, 0.0, 0.0, 0.0};  // raw moments m[k] = E[x^k]
+  explicit ColumnShape(const DataBatch& x, std::size_t col) {
+    for (std::size_t r = 0; r < x.rows; ++r) {
+      const double v = x.at(r, col);
+      double p = v;
+      for (int k = 1; k <= 4; ++k, p *= v) m[k] += p;
+    }
+    const double inv = 1.0 / static_cast<double>(x.rows);
+    for (int k = 1; k <= 4; ++k) m[k] *= inv;
+  }
+  double variance() const { return m[2] - m[1] * m[1]; }
+  double skewness() const {
+    const double mu3 = m[3] - 3.0 * m[1] * m[2] + 2.0 * m[1] * m[1] * m[1];
+    return mu3 / std::pow(variance(), 1.5);
+  }
+  double excess_kurtosis() const {
+    const double a = m[1];
+    const double mu4 = m[4] - 4.0 * a * m[3] + 6.0 * a * a * m[2] - 3.0 * a * a * a * a;
+    return mu4 / (variance() * variance()) - 3.0;
+  }
+};
+
+}  // namespace
+
 double max_abs_univariate(const DataBatch& x, UnivariateStat stat) {
   if (x.rows < 4) throw std::invalid_argument("max_abs_univariate: need at least 4 rows");
   double best = 0.0;
   for (std::size_t col = 0; col < x.cols; ++col) {
-    double m1 = 0, m2 = 0, m3 = 0, m4 = 0;
-    for (std::size_t r = 0; r < x.rows; ++r) {
-      const double v = x.at(r, col), v2 = v * v;
-      m1 += v;
-      m2 += v2;
-      m3 += v2 * v;
-      m4 += v2 * v2;
-    }
-    const double inv = 1.0 / static_cast<double>(x.rows);
-    m1 *= inv;
-    m2 *= inv;
-    m3 *= inv;
-    m4 *= inv;
-    const double mu2 = m2 - m1 * m1;
-    if (mu2 <= 0.0) throw std::domain_error("max_abs_univariate: zero-variance column");
-    double v;
-    if (stat == UnivariateStat::kSkewness) {
-      v = std::abs((m3 - 3.0 * m1 * m2 + 2.0 * m1 * m1 * m1) / std::pow(mu2, 1.5));
-    } else {
-      const double mu4 = m4 - 4.0 * m1 * m3 + 6.0 * m1 * m1 * m2 - 3.0 * m1 * m1 * m1 * m1;
-      v = std::abs(mu4 / (mu2 * mu2) - 3.0);
-    }
-    best = std::max(best, v);
+    const ColumnShape cs(x, col);
+    if (cs.variance() <= 0.0) throw std::domain_error("max_abs_univariate: zero-variance column");
+    const double v = stat == UnivariateStat::kSkewness ? cs.skewness() : cs.excess_kurtosis();
+    best = std::max(best, std::abs(v));
   }
   return best;
 }
@@ -693,23 +724,40 @@ double max_abs_diag_kurtosis(const CumulantSeries& c) {
   return device_report(c, 0).max_abs_kurtosis;
 }
 
-std::uint64_t stirling2(int s, int sigma) {
-  if (s < 1 || s > 25) throw std::invalid_argument("stirling2: s must be in [1, 25]");
-  if (sigma < 1 || sigma > s) return 0;
-  std::vector<std::uint64_t> row(static_cast<std::size_t>(s) + 1, 0);
-  row[0] = 1;
-  for (int i = 1; i <= s; ++i) {
-    for (int j = i; j >= 1; --j) row[j] = row[j - 1] + static_cast<std::uint64_t>(j) * row[j];
-    row[0] = 0;
-  }
-  return row[sigma];
+namespace {
+
+// Stirling numbers of the second kind S(i, j) for i <= 25, built once:
+// table row i from row i - 1 by S(i, j) = j S(i-1, j) + S(i-1, j-1).
+const std::array<std::array<std::uint64_t, 26>, 26>& stirling_table() {
+  static const auto table = [] {
+    std::array<std::array<std::uint64_t, 26>, 26> t{};
+    t[0][0] = 1;
+    for (int i = 1; i <= 25; ++i)
+      for (int j = 1; j <= i; ++j) t[i][j] = static_cast<std::uint64_t>(j) * t[i - 1][j] + t[i - 1][j - 1];
+    return t;
+  }();
+  return table;
 }
 
+}  // namespace
+
+std::uint64_t stirling2(int s, int sigma) {
+  if (s < 1 || s > 25) throw std::invalid_argument("stirling2: s must be in [1, 25]");
+  return sigma < 1 || sigma > s ? 0 : stirling_table()[s][sigma];
+}
+
+// Bell numbers from the Bell (Aitken) triangle: each row starts with the
+// previous row's last entry, each next entry adds the entry above-left;
+// B(s) is the first entry of row s.
 std::uint64_t bell_number(int s) {
   if (s < 1 || s > 25) throw std::invalid_argument("bell_number: s must be in [1, 25]");
-  std::uint64_t total = 0;
-  for (int k = 1; k <= s; ++k) total += stirling2(s, k);
-  return total;
+  std::vector<std::uint64_t> row{1};
+  for (int i = 1; i <= s; ++i) {
+    std::vector<std::uint64_t> next{row.back()};
+    for (std::uint64_t v : row) next.push_back(next.back() + v);
+    row.swap(next);
+  }
+  return row.front();
 }
 
 double moment_error_bound(int d, std::size_t t, double m_2d) {
@@ -720,8 +768,9 @@ double moment_error_bound(int d, std::size_t t, double m_2d) {
 }
 
 double gaussian_moment_error_bound(int d, std::size_t t) {
+  // E[z^{2d}] of a standard normal: (2d - 1)!! = 1 * 3 * ... * (2d - 1)
   double m = 1.0;
-  for (int k = 3; k <= 2 * d - 1; k += 2) m *= static_cast<double>(k);
+  for (int k = 2; k <= d; ++k) m *= static_cast<double>(2 * k - 1);
   return moment_error_bound(d, t, m);
 }
 
@@ -784,13 +833,16 @@ std::string report_json_line(const WindowReport& r) {
 // stream (stream.hpp:19-89)
 
 void StreamConfig::validate() const {
-  if (dim < 1) throw std::invalid_argument("StreamConfig: dim must be positive");
-  if (max_order < 2) throw std::invalid_argument("StreamConfig: max_order must be >= 2");
-  if (window_len < 1) throw std::invalid_argument("StreamConfig: window_len must be positive");
-  if (update_len < 1 || update_len > window_len)
-    throw std::invalid_argument("StreamConfig: update_len must be in [1, window_len]");
-  if (block_size < 1 || block_size > dim) throw std::invalid_argument("StreamConfig: block_size must be in [1, dim]");
-  if (workers < 0) throw std::invalid_argument("StreamConfig: workers must be >= 0");
+  const std::pair<bool, const char*> rules[] = {
+      {dim >= 1, "StreamConfig: dim must be positive"},
+      {max_order >= 2, "StreamConfig: max_order must be >= 2"},
+      {window_len >= 1, "StreamConfig: window_len must be positive"},
+      {update_len >= 1 && update_len <= window_len, "StreamConfig: update_len must be in [1, window_len]"},
+      {block_size >= 1 && block_size <= dim, "StreamConfig: block_size must be in [1, dim]"},
+      {workers >= 0, "StreamConfig: workers must be >= 0"},
+  };
+  for (const auto& [ok, msg] : rules)
+    if (!ok) throw std::invalid_argument(msg);
 }
 
 WindowBuffer::WindowBuffer(std::size_t rows, std::size_t cols) : rows_(rows), cols_(cols), values_(rows * cols) {}
@@ -799,10 +851,13 @@ void WindowBuffer::fill(const DataBatch& x) {
   if (device_) throw std::runtime_error("WindowBuffer::fill: the window lives on the device (use prime)");
   if (x.rows != rows_ || x.cols != cols_)
     throw std::invalid_argument("WindowBuffer::fill: batch does not match capacity");
-  std::memcpy(values_.data(), x.values.data(), values_.size() * sizeof(double));
+  values_.assign(x.values.begin(), x.values.end());
   head_ = 0;
 }
 
+// The oldest x.rows rows leave and x's rows take their slots: at most two
+// contiguous segments of the ring (before and after the wrap), each swapped
+// with the matching span of the batch.
 DataBatch WindowBuffer::exchange(const DataBatch& x) {
   if (device_) throw std::runtime_error("WindowBuffer::exchange: the window lives on the device (use step)");
   if (x.cols != cols_) throw std::invalid_argument("WindowBuffer::exchange: column mismatch");
@@ -810,13 +865,12 @@ DataBatch WindowBuffer::exchange(const DataBatch& x) {
   DataBatch out;
   out.rows = x.rows;
   out.cols = cols_;
-  out.values.resize(x.rows * cols_);
-  for (std::size_t r = 0; r < x.rows; ++r) {
-    double* slot = values_.data() + head_ * cols_;
-    std::memcpy(out.values.data() + r * cols_, slot, cols_ * sizeof(double));
-    std::memcpy(slot, x.values.data() + r * cols_, cols_ * sizeof(double));
-    head_ = (head_ + 1) % rows_;
-  }
+  out.values = x.values;
+  const std::size_t first = std::min(x.rows, rows_ - head_);
+  auto ring = values_.begin();
+  std::swap_ranges(ring + head_ * cols_, ring + (head_ + first) * cols_, out.values.begin());
+  std::swap_ranges(ring, ring + (x.rows - first) * cols_, out.values.begin() + first * cols_);
+  head_ = (head_ + x.rows) % rows_;
   return out;
 }
 
@@ -829,9 +883,8 @@ DataBatch WindowBuffer::materialize() const {
     check(csb_stream_materialize(device_->st, out.values.data(), out.values.size()));
     return out;
   }
-  const std::size_t tail = rows_ - head_;
-  std::memcpy(out.values.data(), values_.data() + head_ * cols_, tail * cols_ * sizeof(double));
-  std::memcpy(out.values.data() + tail * cols_, values_.data(), head_ * cols_ * sizeof(double));
+  // arrival order: the ring rotated so the oldest row (head) comes first
+  std::rotate_copy(values_.begin(), values_.begin() + head_ * cols_, values_.end(), out.values.begin());
   return out;
 }
 
