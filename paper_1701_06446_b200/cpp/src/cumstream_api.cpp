@@ -20,6 +20,13 @@
 #include "cumstream/symten.hpp"
 #include "cumstream_b200.h"
 
+#if __has_include(<json.hpp>)
+#include <json.hpp>  // nlohmann/json 3.11.3, the reference's JSON dependency
+#define CSB_HAVE_NLOHMANN 1
+#else
+#define CSB_HAVE_NLOHMANN 0
+#endif
+
 namespace cumstream {
 
 namespace detail {
@@ -798,6 +805,7 @@ WindowReport to_report(const csb_report& r) {
 }
 
 // JSON number: shortest round-trip form, integral values keep ".0"
+#if !CSB_HAVE_NLOHMANN
 std::string num(double v) {
   if (!std::isfinite(v)) return "null";
   char buf[64];
@@ -806,6 +814,7 @@ std::string num(double v) {
   if (s.find_first_of(".eE") == std::string::npos) s += ".0";
   return s;
 }
+#endif
 }  // namespace
 
 WindowReport make_window_report(std::uint64_t window, const CumulantSeries& c) {
@@ -814,6 +823,22 @@ WindowReport make_window_report(std::uint64_t window, const CumulantSeries& c) {
 }
 
 std::string report_json_line(const WindowReport& r) {
+#if CSB_HAVE_NLOHMANN
+  // the reference's JSON library (nlohmann/json 3.11.3, ordered_json) and
+  // key order (gauge.cpp:156-168, docs/window_report.schema.json): with
+  // bit-identical report values the lines are byte-identical
+  nlohmann::ordered_json j;
+  j["window"] = r.window;
+  j["rows"] = r.rows;
+  j["norm_c1"] = r.norm_c1;
+  j["norm_c2"] = r.norm_c2;
+  auto nus = nlohmann::ordered_json::object();
+  for (const auto& [o, v] : r.nu) nus[std::to_string(o)] = v;
+  j["nu"] = std::move(nus);
+  if (r.max_abs_skewness) j["max_abs_skewness"] = *r.max_abs_skewness;
+  if (r.max_abs_kurtosis) j["max_abs_kurtosis"] = *r.max_abs_kurtosis;
+  return j.dump();
+#else
   // key order of docs/window_report.schema.json
   std::string s = "{\"window\":" + std::to_string(r.window) + ",\"rows\":" + std::to_string(r.rows) +
                   ",\"norm_c1\":" + num(r.norm_c1) + ",\"norm_c2\":" + num(r.norm_c2) + ",\"nu\":{";
@@ -827,6 +852,7 @@ std::string report_json_line(const WindowReport& r) {
   if (r.max_abs_skewness) s += ",\"max_abs_skewness\":" + num(*r.max_abs_skewness);
   if (r.max_abs_kurtosis) s += ",\"max_abs_kurtosis\":" + num(*r.max_abs_kurtosis);
   return s + "}";
+#endif
 }
 
 // ===========================================================================

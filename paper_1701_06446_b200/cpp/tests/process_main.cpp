@@ -5,6 +5,7 @@
 // byte-identical JSONL with one line per window, and the lines equal those
 // of prime()/step() fed the same batches directly (CSV round trip exact).
 #include <cstdio>
+#include <cstdlib>
 #include <filesystem>
 #include <fstream>
 #include <iostream>
@@ -20,7 +21,35 @@
 
 using namespace cumstream;
 
-int main() {
+// process CSV DIM ORDER WINDOW UPDATE BLOCK: the stream of a CSV file, one
+// report line per window on stdout (the same CLI as oracle/ref_process.cpp,
+// which drives the reference library: tests/test_gpu_report_exact.py
+// compares the two outputs byte for byte)
+int process_file(int argc, char** argv) {
+  if (argc != 7) {
+    std::fprintf(stderr, "usage: %s CSV DIM ORDER WINDOW UPDATE BLOCK\n", argv[0]);
+    return 1;
+  }
+  StreamConfig cfg;
+  cfg.dim = std::atoi(argv[2]);
+  cfg.max_order = std::atoi(argv[3]);
+  cfg.window_len = std::strtoull(argv[4], nullptr, 10);
+  cfg.update_len = std::strtoull(argv[5], nullptr, 10);
+  cfg.block_size = std::atoi(argv[6]);
+  cfg.resync_every = 0;
+  try {
+    std::ifstream in(argv[1]);
+    CsvBatchSource source(in, cfg.dim);
+    run(cfg, source, [](const WindowReport& r) { std::cout << report_json_line(r) << "\n"; });
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "%s\n", e.what());
+    return 2;
+  }
+  return 0;
+}
+
+int main(int argc, char** argv) {
+  if (argc > 1) return process_file(argc, argv);
   namespace fs = std::filesystem;
   const fs::path dir = fs::temp_directory_path() / "cumstream_b200_process";
   fs::create_directories(dir);

@@ -286,6 +286,22 @@ __global__ void __launch_bounds__(S <= 4 ? 1024 : 256, S <= 4 ? 1 : 2) moms2cums
       P.c[boff + pos] = v;
       part = __fma_rn(v, v, part);
     }
+    if (P.fold_width) {
+      // the block's exact norm partial from the assembled block: knorm's own
+      // sequence (symten.cpp:257-276, vectorised like the reference build:
+      // fold_width-wide rounded squares added in order, then an FMA tail),
+      // one thread while the others write the block out
+      if (threadIdx.x == 0) {
+        const uint32_t nvec = vol & ~static_cast<uint32_t>(P.fold_width - 1);
+        double s = 0.0;
+        uint32_t q = 0;
+#pragma unroll 8
+        for (; q < nvec; ++q) s = __dadd_rn(s, __dmul_rn(cblk[q], cblk[q]));
+        for (; q < vol; ++q) s = __fma_rn(cblk[q], cblk[q], s);
+        P.partial[blockIdx.x] = s;
+      }
+      return;
+    }
   }
   const bool direct = !inblk && STAGED && full && P.canon && P.cstart;  // done in phase 1
   const bool listed = !inblk && STAGED && full && P.canon && (P.mlist || direct);
@@ -750,8 +766,8 @@ bool m2c_persist_ok(int S, const M2CParams& p) {
          2 * M2cStage<6, 4>::total() * sizeof(double) <= 200 * 1024;
 }
 
-void launch_moms2cums_v2(int S, const M2CParams& p, uint64_t nblocks, cudaStream_t st) {
-  if (nblocks == 0) return;
+bool launch_moms2cums_v2(int S, const M2CParams& p, uint64_t nblocks, cudaStream_t st) {
+  if (nblocks == 0) return false;
   if (m2c_persist_ok(S, p)) {
     static int sms = 0;
     if (!sms) CSB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
@@ -761,7 +777,7 @@ void launch_moms2cums_v2(int S, const M2CParams& p, uint64_t nblocks, cudaStream
     moms2cums_persist<6, 4><<<grid, M2CP_THREADS, smem, st>>>(p, static_cast<uint32_t>(nblocks));
     CSB_CUDA(cudaGetLastError());
     count_launch();
-    return;
+    return false;
   }
   const unsigned g = static_cast<unsigned>(nblocks);
   const size_t sm0 = moms2cums_stage_bytes(S, p.n, p.b);
@@ -778,6 +794,10 @@ void launch_moms2cums_v2(int S, const M2CParams& p, uint64_t nblocks, cudaStream
     q.inblk = false;
     if (q.mfix) fail(CSB_ERUNTIME, "moms2cums: deferred mirror without an in-block pass");
   }
+  // every block full and assembled in shared memory: its exact norm partial
+  // comes out of the same pass (else finalize computes them)
+  const bool exact = q.inblk && q.canon && p.n % p.b == 0 && p.fold_width > 0;
+  if (!exact) q.fold_width = 0;
   const int bb = p.b < p.n ? p.b : p.n;
   // big blocks outside shared memory: one wide CTA per SM (orders <= 4)
   const unsigned threads = S <= 4 && staged && !q.inblk && vol >= 16384 ? 1024u : 256u;
@@ -808,6 +828,7 @@ void launch_moms2cums_v2(int S, const M2CParams& p, uint64_t nblocks, cudaStream
   }
   CSB_CUDA(cudaGetLastError());
   count_launch();
+  return exact;
 }
 
 // The same work with the rows read through L1 instead of staged: a lean

@@ -318,46 +318,132 @@ __global__ void copy_c1_kernel(const double* m1, double* c1, double* partial, La
   }
 }
 
-__global__ void knorm_partials_kernel(const double* t, LayoutDev lay, uint64_t nblocks, double k,
-                                      double* partial) {
-  const uint64_t blk = blockIdx.x;
-  if (blk >= nblocks) return;
-  __shared__ double red[8];
+// Per-block sums of |e|^k in the reference's exact order (knorm,
+// symten.cpp:257-276): each block's entries folded one by one in storage
+// order.  The reference build vectorises the k = 2 fold without
+// reassociating it: `width`-wide rounded squares added one by one, then a
+// fused multiply-add tail for the last vol mod width entries (width = 4 for
+// an AVX2 build, 8 for AVX-512; the oracle documents both).
+//
+// One warp takes 32 consecutive blocks and lane g runs block g's
+// sequential chain, so one add instruction advances 32 chains.  The
+// entries arrive by coalesced loads, a 32 x 32 tile per chunk (lane l
+// loads entry l of every block's chunk, the next chunk's loads in flight
+// while this one is chained), transposed through shared memory: slot
+// [e][(g + e) mod 32] holds entry e of block g, so the stores (fixed g)
+// and the chain reads (fixed e) both hit distinct banks.
+constexpr int KN_CHUNK = 32;  // entries per block and chunk (one per lane)
+constexpr int KN_WARPS = 4;   // warps (x 32 blocks) per CTA
+__global__ void __launch_bounds__(KN_WARPS * 32) knorm_exact_kernel(const double* __restrict__ t, LayoutDev lay,
+                                                                    uint64_t blk0, uint64_t nblk, double k, int width,
+                                                                    double* __restrict__ partial) {
+  __shared__ double tile[KN_WARPS][KN_CHUNK][32];
+  __shared__ uint64_t boff[KN_WARPS][32];
+  __shared__ uint32_t bvol[KN_WARPS][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint64_t i = (static_cast<uint64_t>(blockIdx.x) * KN_WARPS + w) * 32 + lane;
+  const bool live = i < nblk;
+  const uint64_t blk = blk0 + (live ? i : 0);
+  const uint64_t off = lay.offset[blk];
+  const uint32_t vol = live ? static_cast<uint32_t>(lay.offset[blk + 1] - off) : 0;
+  boff[w][lane] = off;
+  bvol[w][lane] = vol;
+  uint32_t maxvol = vol;
+  for (int o = 16; o > 0; o >>= 1) maxvol = max(maxvol, __shfl_xor_sync(0xffffffffu, maxvol, o));
+  __syncwarp();
+  const uint32_t nchunk = (maxvol + KN_CHUNK - 1) / KN_CHUNK;
+  double (*tl)[32] = tile[w];
+  // entry `lane` of each block's chunks c and c + 1: two chunks of loads in
+  // flight (the tensor was just written, so mostly L2 hits)
+  double x[2][32];
+  auto load = [&](uint32_t c, int buf) {
+    const uint32_t q = c * KN_CHUNK + lane;
+#pragma unroll
+    for (int g = 0; g < 32; ++g) x[buf][g] = q < bvol[w][g] ? t[boff[w][g] + q] : 0.0;
+  };
+  const uint32_t nvec = vol & ~static_cast<uint32_t>(width - 1);
   double s = 0.0;
-  for (uint64_t i = lay.offset[blk] + threadIdx.x; i < lay.offset[blk + 1]; i += blockDim.x) {
-    const double v = t[i];
-    if (k == 2.0) s = __fma_rn(v, v, s);
-    else if (k == 1.0) s = __dadd_rn(s, fabs(v));
-    else s = __dadd_rn(s, pow(fabs(v), k));
+  if (nchunk) load(0, 0);
+  if (nchunk > 1) load(1, 1);
+  for (uint32_t c = 0; c < nchunk; ++c) {
+    if (c & 1) {
+#pragma unroll
+      for (int g = 0; g < 32; ++g) tl[lane][(g + lane) & 31] = x[1][g];
+    } else {
+#pragma unroll
+      for (int g = 0; g < 32; ++g) tl[lane][(g + lane) & 31] = x[0][g];
+    }
+    __syncwarp();
+    if (c + 2 < nchunk) {  // refill the buffer just stored: in flight during the next two chains
+      if (c & 1) load(c + 2, 1);
+      else load(c + 2, 0);
+    }
+    const uint32_t q0 = c * KN_CHUNK;
+    const uint32_t e1 = vol > q0 ? min(vol - q0, static_cast<uint32_t>(KN_CHUNK)) : 0;
+    auto at = [&](uint32_t e) { return tl[e][(lane + e) & 31]; };
+    if (k == 2.0) {
+      const uint32_t ev = nvec > q0 ? min(nvec - q0, e1) : 0;  // rounded squares, then the FMA tail
+      if (ev == KN_CHUNK) {
+        // whole chunk of rounded squares: form all 32 first (independent),
+        // so only the adds wait on one another
+        double sq[KN_CHUNK];
+#pragma unroll
+        for (int e = 0; e < KN_CHUNK; ++e) {
+          const double y = at(e);
+          sq[e] = __dmul_rn(y, y);
+        }
+#pragma unroll
+        for (int e = 0; e < KN_CHUNK; ++e) s = __dadd_rn(s, sq[e]);
+      } else {
+        uint32_t e = 0;
+        for (; e < ev; ++e) {
+          const double y = at(e);
+          s = __dadd_rn(s, __dmul_rn(y, y));
+        }
+        for (; e < e1; ++e) {
+          const double y = at(e);
+          s = __fma_rn(y, y, s);
+        }
+      }
+    } else if (k == 1.0) {
+      for (uint32_t e = 0; e < e1; ++e) s = __dadd_rn(s, fabs(at(e)));
+    } else {
+      for (uint32_t e = 0; e < e1; ++e) s = __dadd_rn(s, pow(fabs(at(e)), k));
+    }
+    __syncwarp();  // the tile is rewritten by the next chunk
   }
-  for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, o));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double a = 0.0;
-    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) a = __dadd_rn(a, red[w]);
-    partial[blk] = a;
-  }
+  if (live) partial[blk] = s;
 }
 
-// One CTA: fixed-order reductions of the per-block partials (x multiplicity)
-// and the diagonal gathers the report needs.  Deterministic for any GPU count.
-__global__ void __launch_bounds__(1024) norm_finalize_kernel(const NormParams P) {
-  __shared__ double red[32];
-  for (int s = 0; s < P.norders; ++s) {
+// The blocks' partial sums folded in block order, acc = acc + mult * s
+// (symten.cpp:268; the product is rounded, the reference build does not
+// contract it).  One CTA per order: the threads form the rounded products
+// of a slice of blocks in shared memory (coalesced, in parallel), thread 0
+// adds them in block order -- the reference's sequence bit for bit, with
+// only the adds on the sequential path.  CTA 0 also gathers the diagonals.
+constexpr int NF_THREADS = 256;
+constexpr int NF_SLICE = 2048;
+__global__ void __launch_bounds__(NF_THREADS) norm_finalize_kernel(const NormParams P) {
+  __shared__ double prod[2][NF_SLICE];
+  const int s = static_cast<int>(blockIdx.x);
+  if (s < P.norders) {
+    const double* __restrict__ mult = P.mult[s];
+    const double* __restrict__ part = P.partial[s];
+    const uint64_t nb = P.nblocks[s];
     double a = 0.0;
-    for (uint64_t i = threadIdx.x; i < P.nblocks[s]; i += blockDim.x)
-      a = __fma_rn(P.mult[s][i], P.partial[s][i], a);
-    for (int o = 16; o > 0; o >>= 1) a = __dadd_rn(a, __shfl_down_sync(0xffffffffu, a, o));
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double tot = 0.0;
-      for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) tot = __dadd_rn(tot, red[w]);
-      P.out[s] = tot;
+    for (uint64_t base = 0, it = 0; base < nb; base += NF_SLICE, ++it) {
+      double* pr = prod[it & 1];  // double buffer: slice it + 1 forms while thread 0 adds slice it
+      const uint64_t cnt = nb - base < NF_SLICE ? nb - base : NF_SLICE;
+      for (uint64_t i = threadIdx.x; i < cnt; i += NF_THREADS) pr[i] = __dmul_rn(mult[base + i], part[base + i]);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+#pragma unroll 8
+        for (uint64_t i = 0; i < cnt; ++i) a = __dadd_rn(a, pr[i]);
+      }
     }
-    __syncthreads();
+    if (threadIdx.x == 0) P.out[s] = a;
   }
+  if (s != 0) return;
   for (int q = 0; q < 3; ++q) {
     if (!P.diag_src[q]) continue;
     for (int i = threadIdx.x; i < P.n; i += blockDim.x)
@@ -431,15 +517,16 @@ void launch_copy_c1(const double* m1, double* c1, double* partial, const LayoutD
 }
 
 void launch_norm_finalize(const NormParams& p, cudaStream_t st) {
-  norm_finalize_kernel<<<1, 1024, 0, st>>>(p);
+  norm_finalize_kernel<<<std::max(1, p.norders), NF_THREADS, 0, st>>>(p);
   CSB_CUDA(cudaGetLastError());
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
-void launch_knorm_partials(const double* t, const LayoutDev& lay, uint64_t nblocks, double k,
-                           double* partial, cudaStream_t st) {
-  if (!nblocks) return;
-  knorm_partials_kernel<<<static_cast<unsigned>(nblocks), 256, 0, st>>>(t, lay, nblocks, k, partial);
+void launch_knorm_exact(const double* t, const LayoutDev& lay, uint64_t blk0, uint64_t nblk, double k, int width,
+                        double* partial, cudaStream_t st) {
+  if (!nblk) return;
+  const unsigned grid = static_cast<unsigned>((nblk + 32 * KN_WARPS - 1) / (32 * KN_WARPS));
+  knorm_exact_kernel<<<grid, KN_WARPS * 32, 0, st>>>(t, lay, blk0, nblk, k, width, partial);
   CSB_CUDA(cudaGetLastError());
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }

@@ -68,6 +68,7 @@ struct M2CParams {
   const uint32_t* cstart = nullptr;
   const uint32_t* cdst = nullptr;
   double* partial = nullptr;        // per block: sum over stored entries of v*v
+  int fold_width = 0;               // > 0: exact knorm partials (in-block path; see launch_moms2cums_v2)
 };
 
 // One canonical element of a low order (S <= d-2): indices and the offset
@@ -127,7 +128,8 @@ void launch_moment_pair(const MomParams& p, int ntiles, bool top_fma, cudaStream
 // whether moms2cums of order S assembles every block in shared memory
 // (then it can also fill M_S's symmetric copies: MomentPlan's deferred mirror)
 bool m2c_fuse_ok(int S, int n, int b);
-void launch_moms2cums_v2(int S, const M2CParams& p, uint64_t nblocks, cudaStream_t st);
+// returns whether the blocks' exact norm partials were written (p.fold_width)
+bool launch_moms2cums_v2(int S, const M2CParams& p, uint64_t nblocks, cudaStream_t st);
 void launch_moment_lower(int S, const LowerParams& p, cudaStream_t st);
 void launch_moment_lower2(int ST, int W, const Lower2Params& p, cudaStream_t st);
 // orders <= ST of few elements: one thread per element, TMA-staged rows
@@ -138,8 +140,11 @@ void launch_gather(const double* t, const uint64_t* off, uint64_t count, double*
 void launch_copy_c1(const double* m1, double* c1, double* partial, const LayoutDev& lay,
                     uint64_t nblocks, uint64_t stored, cudaStream_t st);
 void launch_norm_finalize(const NormParams& p, cudaStream_t st);
-void launch_knorm_partials(const double* t, const LayoutDev& lay, uint64_t nblocks, double k,
-                           double* partial, cudaStream_t st);
+// per-block sums of |e|^k of blocks [blk0, blk0 + nblk) in the reference's
+// exact order (partial indexed by absolute block); width: the reference
+// build's vector width of the k = 2 fold (4 or 8)
+void launch_knorm_exact(const double* t, const LayoutDev& lay, uint64_t blk0, uint64_t nblk, double k, int width,
+                        double* partial, cudaStream_t st);
 void launch_diag_pick(const double* c, const uint64_t* off, uint64_t lo, uint64_t hi, int n, double* out,
                       cudaStream_t st);
 void launch_combine(const double* a, const double* b, double w1, double w2, double* out,

@@ -801,8 +801,21 @@ void check_batch(uint64_t rows, uint64_t cols, const char* what) {
   if (rows > 0xffffffffull) fail(CSB_EINVAL, std::string(what) + ": too many rows");
 }
 
+// The vector width of the reference's knorm fold as built for this host
+// (-march=native): AVX-512 builds square-and-add 8 entries per chunk, AVX2
+// builds 4 (the oracle pins both; symten.cpp:266).  The device reproduces
+// that build bit for bit.
+int host_fold_width() {
+  static const int w = [] {
+    __builtin_cpu_init();
+    return (__builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512dq")) ? 8 : 4;
+  }();
+  return w;
+}
+
 // moms2cums into c, with per-block partial squared norms for every order.
 struct NormScratch {
+  uint32_t exact_mask = 0;  // orders whose partials are already exact (moms2cums' in-block pass)
   std::vector<DevBuf<double>> partial;  // per order
   DevBuf<double> diag;                  // gathered diagonal of a sharded C_d
   DevBuf<double> out;
@@ -842,9 +855,11 @@ void run_moms2cums(const csb_series* m, csb_series* c, NormScratch& ns, cudaStre
   }
   ProfScope ps("moms2cums", st);
   const auto& L1 = m->lay[0];
-  if (first <= 1)
+  if (first <= 1) {
     launch_copy_c1(m->data[0].ptr, c->data[0].ptr, ns.partial[0].ptr, L1->view(), L1->host.nblocks,
                    L1->host.stored, st);
+    ns.exact_mask &= ~1u;
+  }
   for (int s = std::max(2, first); s <= last; ++s) {
     M2CParams p;
     p.m = m->data[s - 1].ptr;
@@ -853,6 +868,7 @@ void run_moms2cums(const csb_series* m, csb_series* c, NormScratch& ns, cudaStre
     for (int k = 1; k <= s; ++k) p.lay[k - 1] = m->lay[k - 1]->view();
     p.n = m->n;
     p.b = m->b;
+    p.fold_width = host_fold_width();
     p.subs = get_subs(*m->dev, s, m->n, m->b)->ptr;
     {
       uint64_t vol = 1;
@@ -880,17 +896,15 @@ void run_moms2cums(const csb_series* m, csb_series* c, NormScratch& ns, cudaStre
       CSB_CUDA(cudaMemsetAsync(ns.partial[s - 1].ptr, 0, ns.partial[s - 1].bytes(), st));
       p.blk0 = lo;
       p.partial = ns.partial[s - 1].ptr + lo;
-      launch_moms2cums_v2(s, p, hi - lo, st);
-      if (sh.comm) {
-        ProfScope pc("allreduce", st);
-        sh.comm->allreduce_sum(ns.partial[s - 1].ptr, m->lay[s - 1]->host.nblocks, st);  // collective C3
-      }
+      const bool exact = launch_moms2cums_v2(s, p, hi - lo, st);
+      ns.exact_mask = exact ? ns.exact_mask | (1u << (s - 1)) : ns.exact_mask & ~(1u << (s - 1));
     } else {
       p.blk0 = 0;
       p.partial = ns.partial[s - 1].ptr;
       static const char* const tags[] = {"m2c_1", "m2c_2", "m2c_3", "m2c_4", "m2c_5", "m2c_6", "m2c_7", "m2c_8"};
       ProfScope po(tags[s - 1], st);
-      launch_moms2cums_v2(s, p, m->lay[s - 1]->host.nblocks, st);
+      const bool exact = launch_moms2cums_v2(s, p, m->lay[s - 1]->host.nblocks, st);
+      ns.exact_mask = exact ? ns.exact_mask | (1u << (s - 1)) : ns.exact_mask & ~(1u << (s - 1));
     }
   }
   c->window_len = m->window_len;
@@ -926,9 +940,35 @@ DiagTables& diag_tables(const csb_series* c) {
   return t;
 }
 
-// Norm sums of orders 1..d (from partials) + diagonals, to the host.
+// Exact per-block norm partials of order s (all blocks, or [lo, hi) of a
+// shard with zeros elsewhere, summed over ranks: x + 0 == x).
+void exact_partials(const csb_series* c, int s, double* partial, cudaStream_t st, uint64_t lo, uint64_t hi,
+                    double k = 2.0) {
+  const auto& L = c->lay[s - 1];
+  if (lo > 0 || hi < L->host.nblocks) CSB_CUDA(cudaMemsetAsync(partial, 0, L->host.nblocks * sizeof(double), st));
+  launch_knorm_exact(c->data[s - 1].ptr, L->view(), lo, hi - lo, k, host_fold_width(), partial, st);
+}
+
+// Norm sums of orders 1..d + diagonals, to the host: exact per-block
+// partials (each block summed in storage order), then the block-order fold
+// -- knorm's own sequence, so norms and nu are the reference's bit for bit.
 void finalize_norms(const csb_series* c, NormScratch& ns, cudaStream_t st, const ShardCtx& sh = ShardCtx{}) {
   const int d = c->d;
+  if (ns.partial.size() != static_cast<size_t>(d)) {
+    ns.partial.clear();
+    for (int s = 1; s <= d; ++s) ns.partial.emplace_back(c->lay[s - 1]->host.nblocks);
+  }
+  {
+    ProfScope ps("norm_partials", st);
+    for (int s = 1; s <= d; ++s) {
+      const uint64_t nb = c->lay[s - 1]->host.nblocks;
+      const bool shard = sh.active() && s == d;  // C_d: only the owned blocks are valid here
+      if (!(ns.exact_mask >> (s - 1) & 1u))
+        exact_partials(c, s, ns.partial[s - 1].ptr, st, shard ? sh.lo(0) : 0, shard ? sh.hi(0) : nb);
+      if (shard && sh.comm) sh.comm->allreduce_sum(ns.partial[s - 1].ptr, nb, st);  // collective C3
+    }
+    ns.exact_mask = 0;  // (the reduced C_d partials must not be reduced again)
+  }
   NormParams p;
   p.norders = d;
   for (int s = 1; s <= d; ++s) {
@@ -1007,7 +1047,7 @@ double knorm_device(const csb_series* s, int order, double k, cudaStream_t st) {
   if (!(k >= 1.0)) fail(CSB_EINVAL, "knorm: k must be >= 1");
   const auto& L = s->lay[order - 1];
   DevBuf<double> partial(L->host.nblocks);
-  launch_knorm_partials(s->data[order - 1].ptr, L->view(), L->host.nblocks, k, partial.ptr, st);
+  exact_partials(s, order, partial.ptr, st, 0, L->host.nblocks, k);
   NormParams p;
   p.norders = 1;
   p.partial[0] = partial.ptr;
@@ -1434,12 +1474,6 @@ int csb_window_report(const csb_series* c, uint64_t window, csb_report* out) {
     require(c && out, "window_report: null argument");
     if (c->d < 2) fail(CSB_EINVAL, "make_window_report: needs orders up to 2");
     NormScratch ns;
-    for (int s = 1; s <= c->d; ++s) {
-      const auto& L = c->lay[s - 1];
-      ns.partial.emplace_back(L->host.nblocks);
-      launch_knorm_partials(c->data[s - 1].ptr, L->view(), L->host.nblocks, 2.0, ns.partial.back().ptr,
-                            c->dev->stream);
-    }
     finalize_norms(c, ns, c->dev->stream);
     build_report(c, ns, window, out);
   });
@@ -1557,6 +1591,10 @@ int csb_stream_norm_partials(csb_stream* s, int order, double* host, uint64_t co
   return guard([&] {
     require(s && host, "null argument");
     if (order < 1 || order > s->cfg.max_order) fail(CSB_ERANGE, "norm_partials: order out of range");
+    if (!s->norms_valid) {  // the exact partials are made with the report
+      finalize_norms(s->C.get(), s->ns, s->st, s->sh);
+      s->norms_valid = true;
+    }
     const auto& buf = s->ns.partial.at(order - 1);
     require(count == buf.count, "norm_partials: size mismatch");
     CSB_CUDA(cudaStreamSynchronize(s->st));
