@@ -474,7 +474,15 @@ __global__ void __launch_bounds__(M2CP_THREADS, 1) moms2cums_persist(const M2CPa
       }
       const double v = __dsub_rn(mv, partition_correction<S>(f));
       P.c[boff + pos] = v;
-      for (uint32_t q = c0; q < c1; ++q) P.c[boff + __ldg(P.cdst + q)] = v;
+      if (P.mfix) {  // the update's symmetric copies of M_6 too (deferred by run_moments)
+        for (uint32_t q = c0; q < c1; ++q) {
+          const uint32_t dst = __ldg(P.cdst + q);
+          P.c[boff + dst] = v;
+          P.mfix[boff + dst] = mv;
+        }
+      } else {
+        for (uint32_t q = c0; q < c1; ++q) P.c[boff + __ldg(P.cdst + q)] = v;
+      }
       part = __fma_rn(static_cast<double>(1u + c1 - c0), __dmul_rn(v, v), part);
     }
     for (int s = 16; s > 0; s >>= 1) part = __dadd_rn(part, __shfl_down_sync(0xffffffffu, part, s));
@@ -753,6 +761,7 @@ size_t m2c_block_vol(int S, int n, int b) {
 
 bool m2c_fuse_ok(int S, int n, int b) {
   if (S < 2 || S > 6 || n % b != 0) return false;  // every block full
+  if (S == 6 && b == 4) return true;  // moms2cums_persist writes M's copies beside C's
   const size_t sm0 = moms2cums_stage_bytes(S, n, b);
   const size_t vol = m2c_block_vol(S, n, b);
   return sm0 <= 160 * 1024 && vol <= (1u << 20) && sm0 + vol * sizeof(double) <= kM2cInblkLimit;
@@ -762,7 +771,7 @@ bool m2c_fuse_ok(int S, int n, int b) {
 // b = 4), the direct canonical-list path (no in-block pass, no deferred M
 // mirror) -- two buffers of the 62 staged sub-blocks (2 x 92 KB) per SM.
 bool m2c_persist_ok(int S, const M2CParams& p) {
-  return S == 6 && p.b == 4 && p.n % 4 == 0 && p.canon && p.cstart && !p.mfix &&
+  return S == 6 && p.b == 4 && p.n % 4 == 0 && p.canon && p.cstart &&
          2 * M2cStage<6, 4>::total() * sizeof(double) <= 200 * 1024;
 }
 
