@@ -169,6 +169,15 @@ int csb_stream_step(csb_stream* st, const double* x, uint64_t rows, uint64_t col
  * (the call returns early when report and timing are NULL). */
 int csb_stream_step_dev(csb_stream* st, const double* x_dev, uint64_t rows, uint64_t cols,
                         csb_step_timing* timing, csb_report* report);
+/* Pipelined ingestion: csb_stream_upload starts the host-to-device copy of
+ * the next batch (update_len x dim) on a copy stream and returns at once;
+ * csb_stream_step_uploaded runs one step on the oldest uploaded batch
+ * (waiting for its copy on the device, not the host).  Up to two batches may
+ * be uploaded ahead, so batch k+1's copy overlaps step k.  x must stay valid
+ * and unchanged until the step that consumes it returns; use pinned host
+ * memory for the copy to be asynchronous. */
+int csb_stream_upload(csb_stream* st, const double* x, uint64_t rows, uint64_t cols);
+int csb_stream_step_uploaded(csb_stream* st, csb_step_timing* timing, csb_report* report);
 /* Report of the current window (after prime: window 1). */
 int csb_stream_report(csb_stream* st, csb_report* report);
 /* Borrowed views of the state (owned by the stream). */

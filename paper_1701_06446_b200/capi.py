@@ -131,6 +131,8 @@ def lib() -> C.CDLL:
             "csb_stream_step_dev": ([C.c_void_p, C.c_void_p, _u64, _u64, C.POINTER(StepTiming),
                                      C.POINTER(Report)], C.c_int),
             "csb_stream_report": ([C.c_void_p, C.POINTER(Report)], C.c_int),
+            "csb_stream_upload": ([C.c_void_p, _dp, _u64, _u64], C.c_int),
+            "csb_stream_step_uploaded": ([C.c_void_p, C.POINTER(StepTiming), C.POINTER(Report)], C.c_int),
             "csb_stream_moments": ([C.c_void_p, C.POINTER(C.c_void_p)], C.c_int),
             "csb_stream_cumulants": ([C.c_void_p, C.POINTER(C.c_void_p)], C.c_int),
             "csb_stream_window": ([C.c_void_p, C.POINTER(_u64)], C.c_int),
@@ -450,6 +452,20 @@ class Stream:
     def step_dev(self, x_dev_ptr: int, rows: int, cols: int, report: bool = False):
         check(lib().csb_stream_step_dev(self.h, C.c_void_p(x_dev_ptr), rows, cols, None,
                                         C.byref(self.rep) if report else None))
+        return self.rep.as_dict() if report else None
+
+    def upload(self, x: np.ndarray) -> None:
+        """Start the H2D copy of the next batch (csb_stream_upload); x must
+        stay unchanged until the step consuming it returns (pinned memory
+        for an asynchronous copy)."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        check(lib().csb_stream_upload(self.h, _dptr(x), x.shape[0], x.shape[1]))
+        self._uploads = getattr(self, "_uploads", []) + [x]
+
+    def step_uploaded(self, report: bool = True) -> dict | None:
+        """One window update on the oldest uploaded batch."""
+        check(lib().csb_stream_step_uploaded(self.h, None, C.byref(self.rep) if report else None))
+        self._uploads = self._uploads[1:]
         return self.rep.as_dict() if report else None
 
     def report(self) -> dict:

@@ -1076,6 +1076,15 @@ struct csb_stream {
   DevBuf<double> ring;      // window_len x dim, head = oldest row
   uint64_t head = 0;
   DevBuf<double> staging;   // update_len x dim
+  // asynchronous ingestion (csb_stream_upload): two batch buffers filled on
+  // a copy stream while earlier steps run; FIFO of uploaded slots
+  DevBuf<double> upload[2];
+  cudaStream_t copy_st = nullptr;
+  cudaEvent_t uploaded[2] = {nullptr, nullptr};  // H2D of the slot done (copy stream)
+  cudaEvent_t consumed[2] = {nullptr, nullptr};  // the step that read the slot done (engine stream)
+  int queue[2] = {0, 0};
+  int queued = 0, next_slot = 0;
+  bool slot_used[2] = {false, false};
   std::unique_ptr<csb_series> M, C;
   uint64_t window = 0;
   uint64_t steps_since_resync = 0;
@@ -1089,6 +1098,14 @@ struct csb_stream {
   ~csb_stream() {
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
+    for (int k = 0; k < 2; ++k) {
+      if (uploaded[k]) cudaEventDestroy(uploaded[k]);
+      if (consumed[k]) cudaEventDestroy(consumed[k]);
+    }
+    if (copy_st) {
+      cudaStreamSynchronize(copy_st);
+      cudaStreamDestroy(copy_st);
+    }
   }
 };
 
@@ -1523,6 +1540,50 @@ int csb_stream_prime(const csb_stream_config* cfg, const double* first, uint64_t
     s->steps_since_resync = 0;
     CSB_CUDA(cudaStreamSynchronize(s->st));
     *out = s.release();
+  });
+}
+
+int csb_stream_upload(csb_stream* s, const double* x, uint64_t rows, uint64_t cols) {
+  return guard([&] {
+    require(s != nullptr && x != nullptr, "upload: null argument");
+    if (rows != s->cfg.update_len || cols != static_cast<uint64_t>(s->cfg.dim))
+      fail(CSB_EINVAL, "upload: batch does not match the configured update");
+    if (s->queued == 2) fail(CSB_EINVAL, "upload: two batches already uploaded and not stepped");
+    CSB_CUDA(cudaSetDevice(s->dev->id));
+    if (!s->copy_st) {
+      CSB_CUDA(cudaStreamCreateWithFlags(&s->copy_st, cudaStreamNonBlocking));
+      for (int k = 0; k < 2; ++k) {
+        s->upload[k].alloc(rows * cols);
+        CSB_CUDA(cudaEventCreateWithFlags(&s->uploaded[k], cudaEventDisableTiming));
+        CSB_CUDA(cudaEventCreateWithFlags(&s->consumed[k], cudaEventDisableTiming));
+      }
+    }
+    const int slot = s->next_slot;
+    s->next_slot ^= 1;
+    // the step that last read this slot must be done with it
+    if (s->slot_used[slot]) CSB_CUDA(cudaStreamWaitEvent(s->copy_st, s->consumed[slot], 0));
+    CSB_CUDA(cudaMemcpyAsync(s->upload[slot].ptr, x, rows * cols * sizeof(double), cudaMemcpyHostToDevice,
+                             s->copy_st));
+    CSB_CUDA(cudaEventRecord(s->uploaded[slot], s->copy_st));
+    s->queue[s->queued++] = slot;
+  });
+}
+
+int csb_stream_step_uploaded(csb_stream* s, csb_step_timing* t, csb_report* r) {
+  int rc = guard([&] {
+    require(s != nullptr, "step_uploaded: null stream");
+    if (s->queued == 0) fail(CSB_EINVAL, "step_uploaded: no batch uploaded");
+    CSB_CUDA(cudaStreamWaitEvent(s->st, s->uploaded[s->queue[0]], 0));
+  });
+  if (rc != CSB_OK) return rc;
+  const int slot = s->queue[0];
+  rc = stream_step_impl(s, s->upload[slot].ptr, true, s->cfg.update_len, static_cast<uint64_t>(s->cfg.dim), t, r);
+  return guard([&] {
+    CSB_CUDA(cudaEventRecord(s->consumed[slot], s->st));
+    s->slot_used[slot] = true;
+    s->queue[0] = s->queue[1];
+    --s->queued;
+    if (rc != CSB_OK) fail(rc, csb_last_error());
   });
 }
 

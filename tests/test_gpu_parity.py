@@ -216,3 +216,26 @@ def test_cfg0_full_size(port):
     r = port.report(cw, cfg.n, cfg.b, 4, cfg.T)
     for o in (3, 4):
         assert abs(rep["nu"][o] - r["nu"][o]) <= 1e-12 * abs(r["nu"][o])
+
+
+def test_pipelined_upload_matches_step():
+    """csb_stream_upload / csb_stream_step_uploaded (batch k+1's copy
+    in flight during step k) give the same states and reports as step()."""
+    from paper_1701_06446_b200 import capi
+    rng = np.random.default_rng(77)
+    n, d, b, T, p, steps = 24, 4, 3, 96, 24, 5
+    rows = rng.standard_normal((T + steps * p, n))
+    a = capi.Stream(n, d, T, p, b, rows[:T], resync_every=0)
+    c = capi.Stream(n, d, T, p, b, rows[:T], resync_every=0)
+    batches = [rows[T + k * p: T + (k + 1) * p].copy() for k in range(steps)]
+    c.upload(batches[0])
+    for k in range(steps):
+        ra = a.step(batches[k])
+        if k + 1 < steps:
+            c.upload(batches[k + 1])
+        rc = c.step_uploaded()
+        assert ra == rc
+    for x, y in zip(a.moments(), c.moments()):
+        assert np.array_equal(x, y)
+    with pytest.raises(capi.CsbInvalidArgument):
+        c.step_uploaded()  # nothing uploaded

@@ -1,5 +1,5 @@
-for wb in tools/window_bench_t512u1 tools/window_bench_t512u2 tools/window_bench_t512u4; do
-for s in "6 48 4 2000 3 1" "6 48 4 2000 3 2"; do timeout 300 $wb $s; done > gpurun_out/windows.log 2>&1
+for wb in tools/window_bench tools/window_bench_kc64 tools/window_bench_kc16 tools/window_bench_u4; do
+timeout 300 $wb 6 48 4 2000 3 2 > gpurun_out/windows.log 2>&1
 echo $wb
 python3 -c "
 import json
