@@ -223,6 +223,14 @@ int csb_comm_init_ops(int nranks, int rank, const csb_comm_ops* ops);
 /* Releases this process's communicator; streams primed under it keep their
  * reference until they are destroyed. */
 int csb_comm_destroy(void);
+/* Collective over the stream's communicator: every rank receives the other
+ * ranks' blocks of M_d and C_d (an in-place allgather of the owners'
+ * contiguous block ranges), after which csb_stream_moments / _cumulants hold
+ * the whole tensors in block order on every rank -- what a tensor dump
+ * (serialize.cpp:13-75, tools/cumstream.cpp:90-96 --dump-cumulants) needs.
+ * The next step overwrites only the owned ranges again.  No-op on an
+ * unsharded stream. */
+int csb_stream_gather_shards(csb_stream* st);
 /* Block and element range of one shard: which = 0 for order d, 1 for d-1. */
 int csb_shard_range(int max_order, int dim, int block, int shard_index, int shard_count, int which,
                     uint64_t* blk_lo, uint64_t* blk_hi, uint64_t* elem_lo, uint64_t* elem_hi);

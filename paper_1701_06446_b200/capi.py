@@ -139,6 +139,7 @@ def lib() -> C.CDLL:
             "csb_stream_materialize": ([C.c_void_p, _dp, _u64], C.c_int),
             "csb_stream_norm_partials": ([C.c_void_p, C.c_int, _dp, _u64, C.POINTER(_u64)], C.c_int),
             "csb_stream_cuda_stream": ([C.c_void_p, C.POINTER(C.c_void_p)], C.c_int),
+            "csb_stream_gather_shards": ([C.c_void_p], C.c_int),
             "csb_comm_unique_id": ([C.c_char_p], C.c_int),
             "csb_comm_init": ([C.c_int, C.c_int, C.c_char_p], C.c_int),
             "csb_comm_init_ops": ([C.c_int, C.c_int, C.POINTER(CommOps)], C.c_int),
@@ -467,6 +468,10 @@ class Stream:
         check(lib().csb_stream_step_uploaded(self.h, None, C.byref(self.rep) if report else None))
         self._uploads = self._uploads[1:]
         return self.rep.as_dict() if report else None
+
+    def gather_shards(self) -> None:
+        """Collective: every rank receives all blocks of M_d and C_d (tensor dumps)."""
+        check(lib().csb_stream_gather_shards(self.h))
 
     def report(self) -> dict:
         check(lib().csb_stream_report(self.h, C.byref(self.rep)))

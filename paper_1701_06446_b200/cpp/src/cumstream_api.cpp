@@ -866,6 +866,8 @@ void StreamConfig::validate() const {
       {update_len >= 1 && update_len <= window_len, "StreamConfig: update_len must be in [1, window_len]"},
       {block_size >= 1 && block_size <= dim, "StreamConfig: block_size must be in [1, dim]"},
       {workers >= 0, "StreamConfig: workers must be >= 0"},
+      {shard_count >= 1 && shard_index >= 0 && shard_index < shard_count,
+       "StreamConfig: shard_index must be in [0, shard_count)"},
   };
   for (const auto& [ok, msg] : rules)
     if (!ok) throw std::invalid_argument(msg);
@@ -925,8 +927,8 @@ csb_stream_config to_c(const StreamConfig& c) {
   cc.block_size = c.block_size;
   cc.resync_every = c.resync_every;
   cc.workers = c.workers;
-  cc.shard_index = 0;
-  cc.shard_count = 1;
+  cc.shard_index = c.shard_index;
+  cc.shard_count = c.shard_count;
   return cc;
 }
 
@@ -985,6 +987,20 @@ CumulantSeries step(WindowState& state, const DataBatch& x, StepTiming* timing) 
                                  : state.steps_since_resync + 1;
   ++state.window;
   // the returned series is a value: snapshot the stream's cumulants
+  const csb_series* c = nullptr;
+  check(csb_stream_cumulants(dev.st, &c));
+  auto snap = DeviceSeries::create(cfg.dim, cfg.max_order, cfg.block_size);
+  check(csb_series_copy(snap->s, c));
+  return detail::wrap<CumulantSeries>(snap);
+}
+
+CumulantSeries gather_shards(WindowState& state) {
+  if (!state.device) throw std::invalid_argument("gather_shards: state was not created by prime()");
+  auto& dev = *state.device;
+  const StreamConfig& cfg = state.config;
+  detail::sync_into(state.moments.tensors, dev.m);
+  check(csb_stream_gather_shards(dev.st));
+  for (auto& tt : state.moments.tensors) DeviceSeries::attach(tt, dev.m);  // host mirrors are stale now
   const csb_series* c = nullptr;
   check(csb_stream_cumulants(dev.st, &c));
   auto snap = DeviceSeries::create(cfg.dim, cfg.max_order, cfg.block_size);

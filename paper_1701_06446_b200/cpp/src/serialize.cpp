@@ -15,18 +15,22 @@
 #include <string>
 #include <vector>
 
+#include <json.hpp>  // nlohmann/json 3.11.3, the reference's JSON dependency (number formatting only)
+
 namespace cumstream {
 namespace {
 
 [[noreturn]] void bad(const std::string& what) { throw std::runtime_error("sym_tensor_from_json: " + what); }
 
+// Numbers go through the number formatter of the reference's JSON library
+// (nlohmann/json 3.11.3, Grisu2: round-trip exact, and the shortest form
+// except in rare cases) so a dump equals the reference's byte for byte --
+// std::to_chars' always-shortest digits differ from it in those rare cases.
 std::string number(double v) {
   if (!std::isfinite(v)) return "null";  // JSON has no inf/nan (nlohmann writes null too)
   char buf[64];
-  const auto r = std::to_chars(buf, buf + sizeof buf, v);
-  std::string s(buf, r.ptr);
-  if (s.find_first_of(".eEn") == std::string::npos) s += ".0";
-  return s;
+  const char* end = nlohmann::detail::to_chars(buf, buf + sizeof buf, v);
+  return std::string(static_cast<const char*>(buf), end);
 }
 
 // Writer with nlohmann-like layout: compact for indent < 0, else one

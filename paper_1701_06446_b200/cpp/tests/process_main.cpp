@@ -17,17 +17,21 @@
 #include "cumstream/csv.hpp"
 #include "cumstream/cumulants.hpp"
 #include "cumstream/gauge.hpp"
+#include "cumstream/serialize.hpp"
 #include "cumstream/stream.hpp"
 
 using namespace cumstream;
 
-// process CSV DIM ORDER WINDOW UPDATE BLOCK: the stream of a CSV file, one
-// report line per window on stdout (the same CLI as oracle/ref_process.cpp,
-// which drives the reference library: tests/test_gpu_report_exact.py
-// compares the two outputs byte for byte)
+// process CSV DIM ORDER WINDOW UPDATE BLOCK [DUMPDIR]: the stream of a CSV
+// file, one report line per window on stdout (the same CLI as
+// oracle/ref_process.cpp, which drives the reference library:
+// tests/test_gpu_report_exact.py compares the two outputs byte for byte).
+// With DUMPDIR each window's cumulants go to DUMPDIR/window_<w>.json
+// (to_json, indent 1: the reference CLI's --dump-cumulants,
+// tools/cumstream.cpp:90-96), gathered from the shards when there are any.
 int process_file(int argc, char** argv) {
-  if (argc != 7) {
-    std::fprintf(stderr, "usage: %s CSV DIM ORDER WINDOW UPDATE BLOCK\n", argv[0]);
+  if (argc != 7 && argc != 8) {
+    std::fprintf(stderr, "usage: %s CSV DIM ORDER WINDOW UPDATE BLOCK [DUMPDIR]\n", argv[0]);
     return 1;
   }
   StreamConfig cfg;
@@ -40,6 +44,23 @@ int process_file(int argc, char** argv) {
   try {
     std::ifstream in(argv[1]);
     CsvBatchSource source(in, cfg.dim);
+    if (argc == 8) {
+      const std::string dir = argv[7];
+      const auto emit = [&](std::uint64_t w, const CumulantSeries& c) {
+        std::cout << report_json_line(make_window_report(w, c)) << "\n";
+        std::ofstream f(dir + "/window_" + std::to_string(w) + ".json");
+        f << to_json(c, w, 1) << "\n";
+      };
+      auto first = source.next(cfg.window_len);
+      if (!first || first->rows < cfg.window_len) throw std::runtime_error("short input");
+      WindowState state = prime(cfg, *first);
+      emit(state.window, gather_shards(state));
+      for (auto b = source.next(cfg.update_len); b && b->rows == cfg.update_len; b = source.next(cfg.update_len)) {
+        step(state, *b);
+        emit(state.window, gather_shards(state));
+      }
+      return 0;
+    }
     run(cfg, source, [](const WindowReport& r) { std::cout << report_json_line(r) << "\n"; });
   } catch (const std::exception& e) {
     std::fprintf(stderr, "%s\n", e.what());

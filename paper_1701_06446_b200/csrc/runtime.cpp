@@ -1648,6 +1648,27 @@ int csb_stream_materialize(const csb_stream* s, double* host, uint64_t count) {
   });
 }
 
+int csb_stream_gather_shards(csb_stream* s) {
+  return guard([&] {
+    require(s != nullptr, "gather_shards: null stream");
+    if (!s->sh.active()) return;  // the whole tensors already live here
+    CSB_CUDA(cudaSetDevice(s->dev->id));
+    const int d = s->cfg.max_order;
+    const auto& L = s->M->lay[d - 1];
+    const int G = s->sh.plan->count;
+    // rank r owns the blocks [top_blk[r], top_blk[r+1]) of order d: one
+    // contiguous range of the flat block storage (blocks are in lex order)
+    std::vector<uint64_t> off(G), cnt(G);
+    for (int r = 0; r < G; ++r) {
+      off[r] = L->host.offset[s->sh.plan->top_blk[r]];
+      cnt[r] = L->host.offset[s->sh.plan->top_blk[r + 1]] - off[r];
+    }
+    s->sh.comm->allgather_ranges(s->M->data[d - 1].ptr, off.data(), cnt.data(), s->st);
+    s->sh.comm->allgather_ranges(s->C->data[d - 1].ptr, off.data(), cnt.data(), s->st);
+    CSB_CUDA(cudaStreamSynchronize(s->st));
+  });
+}
+
 int csb_stream_norm_partials(csb_stream* s, int order, double* host, uint64_t count, uint64_t* first_block) {
   return guard([&] {
     require(s && host, "null argument");

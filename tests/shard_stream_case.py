@@ -59,6 +59,10 @@ def main():
     capi.check(capi.lib().csb_stream_norm_partials(st.h, d, capi._dptr(part), part.size, capi.C.byref(fb)))
     res["partials"] = part
     res["first_block"] = np.array([fb.value])
+    # tensor dumps from sharded state: gather the owners' block ranges
+    st.gather_shards()
+    res[f"M{d}_gathered"] = st.moments()[d - 1]
+    res[f"C{d}_gathered"] = st.cumulants()[d - 1]
     st.close()
     np.savez(out, **res)
     dist.barrier()

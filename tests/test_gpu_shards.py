@@ -72,5 +72,8 @@ def test_sharded_stream_equals_unsharded(case, tmp_path):
         assert np.array_equal(got["nu"], want_nu), f"rank {r}: nu"
         assert np.array_equal(got["norms"], want_norms), f"rank {r}: norms / diagonals"
         assert int(got["first_block"][0]) == 0
+        # csb_stream_gather_shards: the whole M_d / C_d in block order on every rank
+        assert np.array_equal(got[f"M{d}_gathered"], want_m[d - 1]), f"rank {r}: gathered M{d}"
+        assert np.array_equal(got[f"C{d}_gathered"], want_c[d - 1]), f"rank {r}: gathered C{d}"
         assert np.all(np.isfinite(got["partials"]))
     assert covered.all(), "the shards do not cover M_d"
