@@ -296,6 +296,7 @@ def main() -> None:
         uid = [capi.comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         capi.comm_init(world, rank, uid[0])
+        capi.comm_selftest(1 << 16)  # fail loudly before timing if the NCCL exchange is broken
     st = capi.Stream(cfg.n, cfg.d, cfg.T, cfg.p, cfg.b, window, resync_every=0,
                      shard_index=rank, shard_count=world)
     cs = torch.cuda.ExternalStream(st.cuda_stream(), device=dev)

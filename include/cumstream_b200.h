@@ -220,6 +220,11 @@ typedef struct {
   int (*allreduce_sum)(void* ctx, double* buf, uint64_t count, void* cuda_stream);
 } csb_comm_ops;
 int csb_comm_init_ops(int nranks, int rank, const csb_comm_ops* ops);
+/* Collective health check of the current communicator: one allgather of
+ * per-rank ranges and one sum allreduce of `count` doubles on device buffers,
+ * verified on the host (CSB_ERUNTIME with a message on any mismatch).  Valid
+ * for any rank count, including a single rank. */
+int csb_comm_selftest(uint64_t count);
 /* Releases this process's communicator; streams primed under it keep their
  * reference until they are destroyed. */
 int csb_comm_destroy(void);

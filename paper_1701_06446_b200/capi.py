@@ -144,6 +144,7 @@ def lib() -> C.CDLL:
             "csb_comm_init": ([C.c_int, C.c_int, C.c_char_p], C.c_int),
             "csb_comm_init_ops": ([C.c_int, C.c_int, C.POINTER(CommOps)], C.c_int),
             "csb_comm_destroy": ([], C.c_int),
+            "csb_comm_selftest": ([_u64], C.c_int),
             "csb_shard_range": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(_u64),
                                  C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64)], C.c_int),
             "csb_moments_update_shard": ([C.c_void_p, _dp, _dp, _u64, _u64, C.c_int, C.c_int], C.c_int),
@@ -223,6 +224,11 @@ def comm_init(nranks: int, rank: int, uid: bytes) -> None:
 
 def comm_destroy() -> None:
     check(lib().csb_comm_destroy())
+
+
+def comm_selftest(count: int = 4096) -> None:
+    """Collective: one allgather of ranges + one allreduce, verified (raises on mismatch)."""
+    check(lib().csb_comm_selftest(count))
 
 
 _comm_keepalive: list = []

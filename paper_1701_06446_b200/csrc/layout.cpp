@@ -326,7 +326,18 @@ void MomentPlan::build_dmma(int S_, int n_, int b_, const Layout& top, const Lay
           }
       }
     }
-    for (auto& [key, v] : groups) {
+    // longest tasks first: CTAs are handed out in order, one per SM, and a
+    // CTA of 8-row triangles runs ~9x longer than one of single rows, so the
+    // last wave should be made of the cheap ones
+    std::vector<std::pair<int, const std::vector<TailTask>*>> order;
+    for (const auto& [key, v] : groups) {
+      const int rl = std::get<1>(key);
+      const int per_row = std::get<0>(key) == TAIL_TRI ? LM1 - 1 + 2 * rl + rl * (rl + 1) / 2 : LM1 - 1 + 9 * rl;
+      order.emplace_back(per_row, &v);
+    }
+    std::stable_sort(order.begin(), order.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
+    for (const auto& [cost, vp] : order) {
+      const auto& v = *vp;
       for (const auto& tk : v) tail.push_back(tk);
       TailTask pad = v.front();
       pad.row0 = kNoRow;

@@ -646,7 +646,7 @@ __device__ __forceinline__ uint32_t sm_id() {
   return s;
 }
 
-template <int N, int LM1, int RL, int W, bool TRI>
+template <int N, int LM1, int RL, int W, bool TRI, bool ODD>
 __device__ __forceinline__ void tail_run(const MomParams& P, const TailTask& tk, const Ring& g, double* stash) {
   // TRI: the run is the column range, W == RL; else RL run rows x W columns
   constexpr int NA = TRI ? RL * (RL + 1) / 2 : RL * W;
@@ -668,17 +668,49 @@ __device__ __forceinline__ void tail_run(const MomParams& P, const TailTask& tk,
   for (uint32_t c = 0; c < g.chunks; ++c) {
     mbar_wait(g.xfull + cur.st, cur.ph);
     const double* xs = g.xs + cur.st * stage_elems;
+    // The prefix product of row r + 1 is formed while row r's chains run
+    // (software pipelining by hand: ptxas otherwise starts every row with
+    // the dependent DMUL chain P -> q -> first fma, ~28% of the kernel's
+    // stall samples with 3 warps per scheduler to hide it).
+    double pn = xs[pidx[0]];
+#pragma unroll
+    for (int u = 1; u < LM1; ++u) pn = __dmul_rn(pn, xs[pidx[u]]);
 #pragma unroll 8  // (measured: 2 -> 8 rows per iteration 7.38 -> 7.02 ms at cfg2)
     for (int r = 0; r < TAIL_KC; ++r) {
       const double* xr = xs + r * n;
-      double pv = xr[pidx[0]];
+      const double pv = pn;
+      {
+        const double* xn = xs + min(r + 1, TAIL_KC - 1) * n;
+        pn = xn[pidx[0]];
 #pragma unroll
-      for (int u = 1; u < LM1; ++u) pv = __dmul_rn(pv, xr[pidx[u]]);
+        for (int u = 1; u < LM1; ++u) pn = __dmul_rn(pn, xn[pidx[u]]);
+      }
+      // operand loads as 16-byte pairs: every shared-memory load instruction
+      // costs the FP64 pipe ~2.5 issue cycles (tools/fp64_occupancy.cu), so
+      // halving their number is worth more than any latency hiding here
       double xa[RL], xc[W];
+      {
+        int k = 0;
+        if (ODD) xa[k++] = xr[s];
 #pragma unroll
-      for (int k = 0; k < RL; ++k) xa[k] = xr[s + k];
+        for (; k + 1 < RL; k += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(xr + s + k);
+          xa[k] = v.x;
+          xa[k + 1] = v.y;
+        }
+        if (k < RL) xa[k] = xr[s + k];
+      }
+      if (TRI) {
 #pragma unroll
-      for (int k = 0; k < W; ++k) xc[k] = TRI ? xa[k < RL ? k : 0] : xr[c0 + k];
+        for (int k = 0; k < W; ++k) xc[k] = xa[k < RL ? k : 0];
+      } else {  // c0 is a multiple of 8
+#pragma unroll
+        for (int k = 0; k < W; k += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(xr + c0 + k);
+          xc[k] = v.x;
+          xc[k + 1] = v.y;
+        }
+      }
       int a = 0;
 #pragma unroll
       for (int i = 0; i < RL; ++i) {
@@ -735,24 +767,25 @@ __device__ __forceinline__ void tail_run(const MomParams& P, const TailTask& tk,
 template <int N, int LM1>
 __device__ __forceinline__ void tail_dispatch(const MomParams& P, const TailTask& tk, const Ring& g, double* stash) {
   const int rl = tk.e - tk.s;
+  const bool odd = tk.s & 1;  // warp-uniform: a warp's tasks share s
   if (tk.kind == TAIL_TRI) {
     switch (rl) {
-      case 1: tail_run<N, LM1, 1, 1, true>(P, tk, g, stash); break;
-      case 2: tail_run<N, LM1, 2, 2, true>(P, tk, g, stash); break;
-      case 3: tail_run<N, LM1, 3, 3, true>(P, tk, g, stash); break;
-      case 4: tail_run<N, LM1, 4, 4, true>(P, tk, g, stash); break;
-      case 5: tail_run<N, LM1, 5, 5, true>(P, tk, g, stash); break;
-      case 6: tail_run<N, LM1, 6, 6, true>(P, tk, g, stash); break;
-      case 7: tail_run<N, LM1, 7, 7, true>(P, tk, g, stash); break;
-      case 8: tail_run<N, LM1, 8, 8, true>(P, tk, g, stash); break;
+      case 1: if (odd) tail_run<N, LM1, 1, 1, true, true>(P, tk, g, stash); else tail_run<N, LM1, 1, 1, true, false>(P, tk, g, stash); break;
+      case 2: if (odd) tail_run<N, LM1, 2, 2, true, true>(P, tk, g, stash); else tail_run<N, LM1, 2, 2, true, false>(P, tk, g, stash); break;
+      case 3: if (odd) tail_run<N, LM1, 3, 3, true, true>(P, tk, g, stash); else tail_run<N, LM1, 3, 3, true, false>(P, tk, g, stash); break;
+      case 4: if (odd) tail_run<N, LM1, 4, 4, true, true>(P, tk, g, stash); else tail_run<N, LM1, 4, 4, true, false>(P, tk, g, stash); break;
+      case 5: if (odd) tail_run<N, LM1, 5, 5, true, true>(P, tk, g, stash); else tail_run<N, LM1, 5, 5, true, false>(P, tk, g, stash); break;
+      case 6: if (odd) tail_run<N, LM1, 6, 6, true, true>(P, tk, g, stash); else tail_run<N, LM1, 6, 6, true, false>(P, tk, g, stash); break;
+      case 7: if (odd) tail_run<N, LM1, 7, 7, true, true>(P, tk, g, stash); else tail_run<N, LM1, 7, 7, true, false>(P, tk, g, stash); break;
+      case 8: if (odd) tail_run<N, LM1, 8, 8, true, true>(P, tk, g, stash); else tail_run<N, LM1, 8, 8, true, false>(P, tk, g, stash); break;
       default: break;
     }
   } else {
     switch (rl) {
-      case 1: tail_run<N, LM1, 1, 8, false>(P, tk, g, stash); break;
-      case 2: tail_run<N, LM1, 2, 8, false>(P, tk, g, stash); break;
-      case 3: tail_run<N, LM1, 3, 8, false>(P, tk, g, stash); break;
-      case 4: tail_run<N, LM1, 4, 8, false>(P, tk, g, stash); break;
+      case 1: if (odd) tail_run<N, LM1, 1, 8, false, true>(P, tk, g, stash); else tail_run<N, LM1, 1, 8, false, false>(P, tk, g, stash); break;
+      case 2: if (odd) tail_run<N, LM1, 2, 8, false, true>(P, tk, g, stash); else tail_run<N, LM1, 2, 8, false, false>(P, tk, g, stash); break;
+      case 3: if (odd) tail_run<N, LM1, 3, 8, false, true>(P, tk, g, stash); else tail_run<N, LM1, 3, 8, false, false>(P, tk, g, stash); break;
+      case 4: if (odd) tail_run<N, LM1, 4, 8, false, true>(P, tk, g, stash); else tail_run<N, LM1, 4, 8, false, false>(P, tk, g, stash); break;
       default: break;
     }
   }
@@ -959,7 +992,8 @@ uint32_t sm_id_slots() {  // %nsmid of the current device (SM ids can exceed the
 
 }  // namespace
 
-bool tail_supported(int n, int /*b*/) { return tail_stages(n) >= 2; }
+// even rows: the operand pairs are 16-byte loads
+bool tail_supported(int n, int /*b*/) { return n % 2 == 0 && tail_stages(n) >= 2; }
 
 size_t tail_scratch_doubles() { return static_cast<size_t>(sm_id_slots()) * TAIL_THREADS * TAIL_STASH; }
 
@@ -970,6 +1004,8 @@ int tail_windows(int S, int n, int b) {
   double tasks = 1.0;
   for (int k = 1; k <= S - 2; ++k) tasks = tasks * (n + k - 1) / k;  // C(n + S - 3, S - 2)
   if (tasks < 4.0 * 148 * 32) return 0;
+  // (measured at cfg2: a third window on the CUDA cores costs what it saves,
+  // 1.23 + 9.34 ms against 3.60 + 7.02 ms)
   return 2;  // the last two windows (one when n is not a multiple of 8)
 }
 

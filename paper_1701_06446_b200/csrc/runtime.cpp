@@ -1698,7 +1698,7 @@ int csb_comm_init(int nranks, int rank, const unsigned char* id) {
     require(id != nullptr && nranks >= 1 && rank >= 0 && rank < nranks, "comm_init: bad arguments");
     Device& dev = device();
     dev.comm.reset();  // live streams keep theirs
-    if (nranks > 1) dev.comm = make_nccl_comm(nranks, rank, id);
+    dev.comm = make_nccl_comm(nranks, rank, id);  // one rank is a valid (trivial) communicator
   });
 }
 
@@ -1708,6 +1708,43 @@ int csb_comm_init_ops(int nranks, int rank, const csb_comm_ops* ops) {
     Device& dev = device();
     dev.comm.reset();
     if (nranks > 1) dev.comm = make_ops_comm(nranks, rank, *ops);
+  });
+}
+
+int csb_comm_selftest(uint64_t count) {
+  return guard([&] {
+    Device& dev = device();
+    require(dev.comm != nullptr, "comm_selftest: no communicator (csb_comm_init first)");
+    require(count >= 1 && count <= (1u << 24), "comm_selftest: count must be in [1, 2^24]");
+    Comm& cm = *dev.comm;
+    const int G = cm.nranks;
+    const auto value = [](int r, uint64_t i) { return static_cast<double>(r + 1) + 1e-3 * static_cast<double>(i % 997); };
+    // collective C2's shape: rank r owns [r * count, (r + 1) * count); the rest starts as NaN
+    std::vector<double> h(static_cast<size_t>(G) * count, std::nan(""));
+    for (uint64_t i = 0; i < count; ++i) h[static_cast<size_t>(cm.rank) * count + i] = value(cm.rank, i);
+    DevBuf<double> buf(h.size());
+    CSB_CUDA(cudaMemcpyAsync(buf.ptr, h.data(), buf.bytes(), cudaMemcpyHostToDevice, dev.stream));
+    std::vector<uint64_t> off(G), cnt(G, count);
+    for (int r = 0; r < G; ++r) off[r] = static_cast<uint64_t>(r) * count;
+    cm.allgather_ranges(buf.ptr, off.data(), cnt.data(), dev.stream);
+    CSB_CUDA(cudaMemcpyAsync(h.data(), buf.ptr, buf.bytes(), cudaMemcpyDeviceToHost, dev.stream));
+    CSB_CUDA(cudaStreamSynchronize(dev.stream));
+    for (int r = 0; r < G; ++r)
+      for (uint64_t i = 0; i < count; ++i)
+        if (h[static_cast<size_t>(r) * count + i] != value(r, i))
+          fail(CSB_ERUNTIME, "comm_selftest: allgather_ranges returned a wrong value for rank " + std::to_string(r));
+    // collective C3's shape: elementwise sum over ranks
+    std::vector<double> a(count);
+    for (uint64_t i = 0; i < count; ++i) a[i] = value(cm.rank, i);
+    CSB_CUDA(cudaMemcpyAsync(buf.ptr, a.data(), count * sizeof(double), cudaMemcpyHostToDevice, dev.stream));
+    cm.allreduce_sum(buf.ptr, count, dev.stream);
+    CSB_CUDA(cudaMemcpyAsync(a.data(), buf.ptr, count * sizeof(double), cudaMemcpyDeviceToHost, dev.stream));
+    CSB_CUDA(cudaStreamSynchronize(dev.stream));
+    for (uint64_t i = 0; i < count; ++i) {
+      double want = 0.0;
+      for (int r = 0; r < G; ++r) want += value(r, i);
+      if (std::fabs(a[i] - want) > 1e-12 * want) fail(CSB_ERUNTIME, "comm_selftest: allreduce_sum returned a wrong value");
+    }
   });
 }
 

@@ -37,6 +37,7 @@ def main():
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     capi.check(capi.lib().csb_set_device(0))
     capi.comm_init_torch()
+    capi.comm_selftest(1000)  # the library's own check of the exchange interface
     rows = case_rows(n, T, p, steps, seed)
     st = capi.Stream(n, d, T, p, b, rows[:T], resync_every=0, shard_index=rank, shard_count=world)
     capi.comm_destroy()  # the stream keeps its communicator alive (refcount)

@@ -77,3 +77,24 @@ def test_sharded_stream_equals_unsharded(case, tmp_path):
         assert np.array_equal(got[f"C{d}_gathered"], want_c[d - 1]), f"rank {r}: gathered C{d}"
         assert np.all(np.isfinite(got["partials"]))
     assert covered.all(), "the shards do not cover M_d"
+
+
+def test_nccl_communicator_single_rank_selftest():
+    """The production transport: libnccl.so.2 resolved at run time, a real
+    (one-rank) communicator, and the engine's two collectives -- grouped
+    broadcasts of per-rank ranges and a sum allreduce -- on device buffers,
+    verified by csb_comm_selftest.  More ranks need more GPUs than this pool
+    grants; bench.py --gpus N runs the same self-test on every rank first."""
+    from paper_1701_06446_b200 import capi
+
+    capi.check(capi.lib().csb_set_device(0))
+    uid = capi.comm_unique_id()
+    assert len(uid) == 128
+    capi.comm_init(1, 0, uid)
+    try:
+        capi.comm_selftest(1)
+        capi.comm_selftest(100_000)
+    finally:
+        capi.comm_destroy()
+    with pytest.raises(capi.CsbError):
+        capi.comm_selftest(16)  # no communicator any more

@@ -34,7 +34,7 @@ def main():
         st.step_dev(xs[k].data_ptr(), cfg.p, cfg.n, report=True)
     torch.cuda.synchronize()
     capi.profile_enable(True)
-    for tag in ("moment_top", "mirror", "moment_low", "moms2cums", "norm_partials", "norms", "m2c_2", "m2c_3", "m2c_4", "m2c_5", "m2c_6", "step_update", "step_m2c", "step_report"):
+    for tag in ("moment_top", "moment_tail", "mirror", "moment_low", "moms2cums", "norm_partials", "norms", "m2c_2", "m2c_3", "m2c_4", "m2c_5", "m2c_6", "step_update", "step_m2c", "step_report"):
         capi.profile_read(tag)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     cs = torch.cuda.ExternalStream(st.cuda_stream())
@@ -44,7 +44,7 @@ def main():
     e1.record(cs)
     torch.cuda.synchronize()
     out = {"label": args.label, "config": cfg.name, "step_ms": e0.elapsed_time(e1) / args.steps}
-    for tag in ("moment_top", "mirror", "moment_low", "moms2cums", "norm_partials", "norms", "m2c_2", "m2c_3", "m2c_4", "m2c_5", "m2c_6", "step_update", "step_m2c", "step_report"):
+    for tag in ("moment_top", "moment_tail", "mirror", "moment_low", "moms2cums", "norm_partials", "norms", "m2c_2", "m2c_3", "m2c_4", "m2c_5", "m2c_6", "step_update", "step_m2c", "step_report"):
         ms, n = capi.profile_read(tag)
         out[tag + "_ms"] = ms / max(1, n)
     print(json.dumps(out))
