@@ -191,6 +191,14 @@ int csb_stream_materialize(const csb_stream* st, double* host, uint64_t count);
  * (collective C3), so every entry is valid and first_block is 0. */
 int csb_stream_norm_partials(csb_stream* st, int order, double* host, uint64_t count,
                              uint64_t* first_block);
+/* CUDA graphs: a step's launch sequence depends only on the ring head, the
+ * batch's device address and whether a report is wanted, so the engine
+ * captures one graph per such key on its second visit and replays it
+ * afterwards (on by default; steps with timing, profiling, a resync or
+ * shards run eagerly).  csb_stream_use_graphs(st, 0) turns it off;
+ * csb_stream_graph_replays counts the steps run from a graph. */
+int csb_stream_use_graphs(csb_stream* st, int on);
+int csb_stream_graph_replays(const csb_stream* st, uint64_t* replays);
 /* Device stream (cudaStream_t) the engine launches on, for interop. */
 int csb_stream_cuda_stream(csb_stream* st, void** cuda_stream);
 

@@ -140,6 +140,8 @@ def lib() -> C.CDLL:
             "csb_stream_norm_partials": ([C.c_void_p, C.c_int, _dp, _u64, C.POINTER(_u64)], C.c_int),
             "csb_stream_cuda_stream": ([C.c_void_p, C.POINTER(C.c_void_p)], C.c_int),
             "csb_stream_gather_shards": ([C.c_void_p], C.c_int),
+            "csb_stream_use_graphs": ([C.c_void_p, C.c_int], C.c_int),
+            "csb_stream_graph_replays": ([C.c_void_p, C.POINTER(_u64)], C.c_int),
             "csb_comm_unique_id": ([C.c_char_p], C.c_int),
             "csb_comm_init": ([C.c_int, C.c_int, C.c_char_p], C.c_int),
             "csb_comm_init_ops": ([C.c_int, C.c_int, C.POINTER(CommOps)], C.c_int),
@@ -474,6 +476,14 @@ class Stream:
         check(lib().csb_stream_step_uploaded(self.h, None, C.byref(self.rep) if report else None))
         self._uploads = self._uploads[1:]
         return self.rep.as_dict() if report else None
+
+    def use_graphs(self, on: bool) -> None:
+        check(lib().csb_stream_use_graphs(self.h, 1 if on else 0))
+
+    def graph_replays(self) -> int:
+        v = _u64()
+        check(lib().csb_stream_graph_replays(self.h, C.byref(v)))
+        return v.value
 
     def gather_shards(self) -> None:
         """Collective: every rank receives all blocks of M_d and C_d (tensor dumps)."""

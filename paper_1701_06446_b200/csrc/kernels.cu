@@ -474,6 +474,7 @@ std::atomic<uint64_t> g_launches{0};
 
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void add_launches(uint64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }  // a replayed graph's kernels
 
 void launch_moment_pair(const MomParams& p, int ntiles, bool top_fma, cudaStream_t st) {
   if (ntiles <= 0) return;

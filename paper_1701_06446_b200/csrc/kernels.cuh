@@ -156,6 +156,7 @@ constexpr int kMomThreads = 256;
 // gpu_launches claim).
 uint64_t launch_count();
 void count_launch();
+void add_launches(uint64_t k);
 
 // FP64 tensor-core (DMMA) kernel for the top pair of orders (moment_dmma.cu)
 bool dmma_supported(const MomParams& p);

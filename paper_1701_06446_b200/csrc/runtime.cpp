@@ -2,6 +2,7 @@
 // cached layouts and launch plans, and the extern "C" entry points declared
 // in include/cumstream_b200.h.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <atomic>
 #include <chrono>
@@ -209,11 +210,15 @@ struct Profiler {
 };
 Profiler g_prof;
 
+// Every scope is also an NVTX range (header-only NVTX 3: a no-op unless a
+// tool such as nsys or ncu --nvtx is attached), so timelines show the
+// step's phases by the same tags csb_profile_read uses.
 struct ProfScope {
   cudaEvent_t a = nullptr, b = nullptr;
   cudaStream_t st;
   const char* tag;
   ProfScope(const char* tag_, cudaStream_t st_) : st(st_), tag(tag_) {
+    nvtxRangePushA(tag);
     if (!g_prof.on) return;
     {
       std::lock_guard<std::mutex> lk(g_prof.mu);
@@ -223,6 +228,7 @@ struct ProfScope {
     CSB_CUDA(cudaEventRecord(a, st));
   }
   ~ProfScope() {
+    nvtxRangePop();
     if (!a) return;
     cudaEventRecord(b, st);
     std::lock_guard<std::mutex> lk(g_prof.mu);
@@ -952,7 +958,8 @@ void exact_partials(const csb_series* c, int s, double* partial, cudaStream_t st
 // Norm sums of orders 1..d + diagonals, to the host: exact per-block
 // partials (each block summed in storage order), then the block-order fold
 // -- knorm's own sequence, so norms and nu are the reference's bit for bit.
-void finalize_norms(const csb_series* c, NormScratch& ns, cudaStream_t st, const ShardCtx& sh = ShardCtx{}) {
+void finalize_norms(const csb_series* c, NormScratch& ns, cudaStream_t st, const ShardCtx& sh = ShardCtx{},
+                    bool wait = true) {
   const int d = c->d;
   if (ns.partial.size() != static_cast<size_t>(d)) {
     ns.partial.clear();
@@ -1001,7 +1008,7 @@ void finalize_norms(const csb_series* c, NormScratch& ns, cudaStream_t st, const
   }
   ns.host.resize(need);
   CSB_CUDA(cudaMemcpyAsync(ns.host.data(), ns.out.ptr, need * sizeof(double), cudaMemcpyDeviceToHost, st));
-  CSB_CUDA(cudaStreamSynchronize(st));
+  if (wait) CSB_CUDA(cudaStreamSynchronize(st));  // (a captured step waits after the graph launch)
 }
 
 // make_window_report from the finalized sums (gauge.cpp:35-41,64-94,142-154).
@@ -1095,7 +1102,25 @@ struct csb_stream {
   std::shared_ptr<Comm> comm;        // kept alive for the stream's lifetime
   ShardCtx sh;
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  // One CUDA graph per (ring head, batch pointer, report?): a step's launch
+  // sequence depends on nothing else, and the ring revisits window_len /
+  // gcd(window_len, update_len) heads.  The first visit of a key runs
+  // eagerly (tables, scratch and plans get built), the second is captured,
+  // later ones are one cudaGraphLaunch -- the small configurations are
+  // launch-bound otherwise (cfg0: ~20 launches around a 0.09 ms kernel).
+  struct StepGraph {
+    cudaGraphExec_t exec = nullptr;
+    bool seen = false;
+    uint32_t exact_mask_after = 0;
+    int early_m2c = 0;
+    uint64_t launches = 0;
+  };
+  std::map<std::tuple<uint64_t, const double*, int>, StepGraph> graphs;
+  bool use_graphs = true;
+  uint64_t graph_replays = 0;
   ~csb_stream() {
+    for (auto& [key, g] : graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     for (int k = 0; k < 2; ++k) {
@@ -1192,22 +1217,88 @@ int stream_step_impl(csb_stream* s, const double* x, bool on_device, uint64_t ro
       CSB_CUDA(cudaMemcpyAsync(s->staging.ptr, x, rows * cols * sizeof(double), cudaMemcpyHostToDevice, s->st));
       xd = s->staging.ptr;
     }
-    if (timing) CSB_CUDA(cudaEventRecord(s->ev[0], s->st));  // StepTiming only when asked
-    {
-      ProfScope pu("step_update", s->st);
-      stream_exchange_and_update(s, xd);
+    // the enqueue-only part of a step (no host wait): what a graph captures
+    const auto enqueue = [&](bool want_report) {
+      if (timing) CSB_CUDA(cudaEventRecord(s->ev[0], s->st));  // StepTiming only when asked
+      {
+        ProfScope pu("step_update", s->st);
+        stream_exchange_and_update(s, xd);
+      }
+      if (timing) CSB_CUDA(cudaEventRecord(s->ev[1], s->st));
+      {
+        ProfScope pc("step_m2c", s->st);
+        run_moms2cums(s->M.get(), s->C.get(), s->ns, s->st, s->sh, 1 + s->early_m2c);
+      }
+      if (timing) CSB_CUDA(cudaEventRecord(s->ev[2], s->st));
+      if (want_report) {
+        ProfScope pr("step_report", s->st);
+        finalize_norms(s->C.get(), s->ns, s->st, s->sh, false);
+      }
+    };
+    const bool resync = cfg.resync_every > 0 && s->steps_since_resync + 1 >= cfg.resync_every;
+    const bool graphable = s->use_graphs && !timing && !g_prof.on && !s->sh.active() && !resync &&
+                           s->M->mirror_defer == 0;
+    csb_stream::StepGraph* sg = nullptr;
+    if (graphable) {
+      const auto key = std::make_tuple(s->head, xd, report ? 1 : 0);
+      auto it = s->graphs.find(key);
+      if (it != s->graphs.end()) sg = &it->second;
+      else if (s->graphs.size() < 256) sg = &s->graphs[key];  // (callers cycling through many buffers stay eager)
     }
-    if (timing) CSB_CUDA(cudaEventRecord(s->ev[1], s->st));
-    {
-      ProfScope pc("step_m2c", s->st);
-      run_moms2cums(s->M.get(), s->C.get(), s->ns, s->st, s->sh, 1 + s->early_m2c);
+    if (sg && sg->exec) {
+      // replay: the device work of the captured step, then its host-side bookkeeping
+      CSB_CUDA(cudaGraphLaunch(sg->exec, s->st));
+      s->head = (s->head + cfg.update_len) % cfg.window_len;
+      ++s->steps_since_resync;
+      g_rows_read.fetch_add(2 * cfg.update_len, std::memory_order_relaxed);
+      s->early_m2c = sg->early_m2c;
+      s->ns.exact_mask = sg->exact_mask_after;
+      s->C->window_len = s->M->window_len;
+      add_launches(sg->launches);
+      ++s->graph_replays;
+    } else if (sg && sg->seen) {
+      // second visit of this key: capture the step, then run it from the graph
+      const uint64_t head0 = s->head, since0 = s->steps_since_resync;
+      const uint32_t mask0 = s->ns.exact_mask;
+      const uint64_t l0 = launch_count();
+      const uint64_t rows0 = g_rows_read.load(std::memory_order_relaxed);
+      cudaGraph_t graph = nullptr;
+      bool ok = cudaStreamBeginCapture(s->st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+      if (ok) {
+        try {
+          enqueue(report != nullptr);
+        } catch (const std::exception&) {
+          ok = false;
+        }
+        if (cudaStreamEndCapture(s->st, &graph) != cudaSuccess || !graph) ok = false;
+      }
+      if (ok && cudaGraphInstantiate(&sg->exec, graph, 0) != cudaSuccess) ok = false;
+      if (graph) cudaGraphDestroy(graph);
+      if (ok) {
+        sg->launches = launch_count() - l0;
+        sg->exact_mask_after = s->ns.exact_mask;
+        sg->early_m2c = s->early_m2c;
+        CSB_CUDA(cudaGraphLaunch(sg->exec, s->st));
+      } else {
+        // not capturable here: forget graphs for this stream and run the step eagerly
+        cudaGetLastError();
+        sg->exec = nullptr;
+        s->use_graphs = false;
+        s->head = head0;
+        s->steps_since_resync = since0;
+        s->ns.exact_mask = mask0;
+        s->M->mirror_defer = 0;
+        g_rows_read.store(rows0, std::memory_order_relaxed);
+        enqueue(report != nullptr);
+      }
+    } else {
+      if (sg) sg->seen = true;
+      enqueue(report != nullptr);
     }
-    if (timing) CSB_CUDA(cudaEventRecord(s->ev[2], s->st));
     s->norms_valid = false;
     ++s->window;
     if (report) {
-      ProfScope pr("step_report", s->st);
-      finalize_norms(s->C.get(), s->ns, s->st, s->sh);
+      CSB_CUDA(cudaStreamSynchronize(s->st));
       s->norms_valid = true;
       build_report(s->C.get(), s->ns, s->window, report);
     }
@@ -1645,6 +1736,20 @@ int csb_stream_materialize(const csb_stream* s, double* host, uint64_t count) {
     CSB_CUDA(cudaMemcpy(host, s->ring.ptr + s->head * n, tail * n * sizeof(double), cudaMemcpyDeviceToHost));
     if (s->head)
       CSB_CUDA(cudaMemcpy(host + tail * n, s->ring.ptr, s->head * n * sizeof(double), cudaMemcpyDeviceToHost));
+  });
+}
+
+int csb_stream_use_graphs(csb_stream* s, int on) {
+  return guard([&] {
+    require(s != nullptr, "use_graphs: null stream");
+    s->use_graphs = on != 0;
+  });
+}
+
+int csb_stream_graph_replays(const csb_stream* s, uint64_t* replays) {
+  return guard([&] {
+    require(s && replays, "graph_replays: null argument");
+    *replays = s->graph_replays;
   });
 }
 
