@@ -41,7 +41,13 @@ extern "C" {
 #define CSB_EDOMAIN 3
 #define CSB_ERUNTIME 4
 
-#define CSB_MAX_ORDER 8 /* device path; the reference allows 20 (symten.hpp:87) */
+/* Tensor orders 1..20 as in the reference (symten.hpp:87); cumulants up to
+ * order 16 (set partitions, cumulants.hpp:24: larger orders are
+ * CSB_EINVAL).  Moments up to order 8 and cumulants up to 6 run on the
+ * specialised kernels; above that the any-order kernels take over (one
+ * thread per stored element, the same arithmetic sequence; not tuned, and
+ * sharding is limited to orders <= 8). */
+#define CSB_MAX_ORDER 20
 
 typedef struct csb_series csb_series; /* device-resident M_1..M_d or C_1..C_d */
 typedef struct csb_stream csb_stream; /* device-resident WindowState (stream.hpp:54-60) */

@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("CSB_LIB_PATH") or os.path.join(PKG, "lib", "libcumstr
 HEADER = os.path.join(os.path.dirname(PKG), "include", "cumstream_b200.h")
 
 OK, EINVAL, ERANGE, EDOMAIN, ERUNTIME = 0, 1, 2, 3, 4
-MAX_ORDER = 8
+MAX_ORDER = 20
 
 _u64 = C.c_uint64
 _dp = C.POINTER(C.c_double)

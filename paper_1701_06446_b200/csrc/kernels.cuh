@@ -40,6 +40,7 @@ struct LayoutDev {
   const uint16_t* index = nullptr;   // nblocks x order
   const uint64_t* prefix = nullptr;  // order x (grid + 1)
   int order = 0, grid = 0;
+  uint64_t nblocks = 0;
 };
 
 struct M2CParams {
@@ -114,15 +115,38 @@ struct Lower2Params {
 };
 
 struct NormParams {
-  const double* partial[kMaxOrder];  // per order, nblocks each
-  const double* mult[kMaxOrder];     // per order block multiplicities (as double)
-  uint64_t nblocks[kMaxOrder];
+  const double* partial[kMaxOrderAny];  // per order, nblocks each
+  const double* mult[kMaxOrderAny];     // per order block multiplicities (as double)
+  uint64_t nblocks[kMaxOrderAny];
   int norders = 0;                   // orders 1..norders
   const double* diag_src[3];         // C_2, C_3, C_4 (nullptr if absent)
   const uint64_t* diag_off[3];       // n offsets each
   int n = 0;
   double* out = nullptr;             // [norders sums][3 x n diagonals]
 };
+
+// any-order kernels (generic.cu): one thread per stored element
+struct GenMomParams {
+  RowSource src[2];
+  int npass = 1;
+  uint32_t K = 0;
+  int n = 0, b = 0;
+  bool top = false;  // this is the series' top order: acc = fma(q, x, acc) (moments.cpp:47)
+  double* m = nullptr;
+  LayoutDev lay;
+  uint64_t stored = 0;
+  double c = 0.0, inv = 1.0;
+};
+struct GenM2CParams {
+  const double* m = nullptr;  // M_s
+  double* c = nullptr;        // C_s
+  const double* lower[kMaxCumOrderAny];  // C_1 .. C_{s-1}
+  LayoutDev lay[kMaxCumOrderAny];        // layouts of orders 1..s
+  int n = 0, b = 0, s = 0;
+  uint64_t stored = 0;
+};
+void launch_moment_generic(const GenMomParams& p, cudaStream_t st);
+void launch_moms2cums_generic(const GenM2CParams& p, cudaStream_t st);
 
 void launch_moment_pair(const MomParams& p, int ntiles, bool top_fma, cudaStream_t st);
 // whether moms2cums of order S assembles every block in shared memory

@@ -22,7 +22,14 @@
 
 namespace csb {
 
-constexpr int kMaxOrder = CSB_MAX_ORDER;
+// kMaxOrder: the specialised kernels (DMMA / DFMA top pair, mirror lists,
+// staged moms2cums up to 6); above it the any-order kernels of generic.cu
+// take over, up to the reference's limits (symten.hpp:87, cumulants.hpp:24).
+constexpr int kMaxOrder = 8;
+constexpr int kMaxOrderAny = CSB_MAX_ORDER;  // 20
+constexpr int kMaxCumOrder = 6;              // generated partition code
+constexpr int kMaxCumOrderAny = 16;
+static_assert(kMaxOrderAny == 20, "CSB_MAX_ORDER follows the reference's SymTensor::kMaxOrder");
 
 struct Layout {
   int order = 0, dim = 0, block = 0, grid = 0;

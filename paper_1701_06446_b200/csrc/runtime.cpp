@@ -52,6 +52,7 @@ struct DevLayout {
     v.prefix = prefix.ptr;
     v.order = host.order;
     v.grid = host.grid;
+    v.nblocks = host.nblocks;
     return v;
   }
 };
@@ -550,7 +551,7 @@ namespace {
 
 std::unique_ptr<csb_series> make_series(int n, int d, int b) {
   require(n >= 1, "series: dim must be positive");
-  require(d >= 1 && d <= kMaxOrder, "series: max_order must be in [1, 8] on the device path");
+  require(d >= 1 && d <= kMaxOrderAny, "series: max_order must be in [1, 20]");
   require(b >= 1 && b <= n, "series: block_size must be in [1, dim]");
   Device& dev = device();
   auto s = std::make_unique<csb_series>();
@@ -630,6 +631,29 @@ void run_moments(csb_series* m, const RowSource src[2], int npass, uint64_t K, d
   Device& dev = *m->dev;
   const int d = m->d;
   const int S = only_order ? only_order : d;
+  if (S > kMaxOrder) {
+    // any-order kernels: every stored element of every order from its own
+    // sorted index (no pyramid, no mirror pass); not sharded
+    if (sh.active()) fail(CSB_EINVAL, "sharding supports orders up to 8");
+    ProfScope ps("moment_generic", st);
+    for (int s = only_order ? only_order : 1; s <= S; ++s) {
+      GenMomParams g;
+      g.src[0] = src[0];
+      g.src[1] = src[1];
+      g.npass = npass;
+      g.K = static_cast<uint32_t>(K);
+      g.n = m->n;
+      g.b = m->b;
+      g.top = s == S;
+      g.m = m->data[s - 1].ptr;
+      g.lay = m->lay[s - 1]->view();
+      g.stored = m->lay[s - 1]->host.stored;
+      g.c = c;
+      g.inv = 1.0 / static_cast<double>(K);
+      launch_moment_generic(g, st);
+    }
+    return;
+  }
   Scratch& sc = g_scratch[dev.id];
   const bool lower = !only_order && d > 2;
   MomParams p;
@@ -855,6 +879,8 @@ void run_moms2cums(const csb_series* m, csb_series* c, NormScratch& ns, cudaStre
                    const ShardCtx& sh = ShardCtx{}, int first = 1, int last = 0) {
   const int d = m->d;
   if (last <= 0) last = d;
+  // (checked before any order is converted: s = 16 alone is 10^10 partitions per element)
+  if (last > kMaxCumOrderAny) fail(CSB_EINVAL, "partitions: s must be in [1, 16]");
   if (ns.partial.size() != static_cast<size_t>(d)) {
     ns.partial.clear();
     for (int s = 1; s <= d; ++s) ns.partial.emplace_back(m->lay[s - 1]->host.nblocks);
@@ -867,6 +893,24 @@ void run_moms2cums(const csb_series* m, csb_series* c, NormScratch& ns, cudaStre
     ns.exact_mask &= ~1u;
   }
   for (int s = std::max(2, first); s <= last; ++s) {
+    if (s > kMaxCumOrder) {
+      // any-order kernel: restricted growth strings walked on the device
+      if (s > kMaxCumOrderAny) fail(CSB_EINVAL, "partitions: s must be in [1, 16]");
+      if (sh.active()) fail(CSB_EINVAL, "sharding supports cumulants up to order 6");
+      GenM2CParams g;
+      g.m = m->data[s - 1].ptr;
+      g.c = c->data[s - 1].ptr;
+      for (int k = 1; k < s; ++k) g.lower[k - 1] = c->data[k - 1].ptr;
+      for (int k = 1; k <= s; ++k) g.lay[k - 1] = m->lay[k - 1]->view();
+      g.n = m->n;
+      g.b = m->b;
+      g.s = s;
+      g.stored = m->lay[s - 1]->host.stored;
+      ProfScope po("m2c_generic", st);
+      launch_moms2cums_generic(g, st);
+      ns.exact_mask &= ~(1u << (s - 1));
+      continue;
+    }
     M2CParams p;
     p.m = m->data[s - 1].ptr;
     p.c = c->data[s - 1].ptr;
@@ -907,7 +951,7 @@ void run_moms2cums(const csb_series* m, csb_series* c, NormScratch& ns, cudaStre
     } else {
       p.blk0 = 0;
       p.partial = ns.partial[s - 1].ptr;
-      static const char* const tags[] = {"m2c_1", "m2c_2", "m2c_3", "m2c_4", "m2c_5", "m2c_6", "m2c_7", "m2c_8"};
+      static const char* const tags[] = {"m2c_1", "m2c_2", "m2c_3", "m2c_4", "m2c_5", "m2c_6"};
       ProfScope po(tags[s - 1], st);
       const bool exact = launch_moms2cums_v2(s, p, m->lay[s - 1]->host.nblocks, st);
       ns.exact_mask = exact ? ns.exact_mask | (1u << (s - 1)) : ns.exact_mask & ~(1u << (s - 1));
@@ -1609,6 +1653,7 @@ int csb_stream_prime(const csb_stream_config* cfg, const double* first, uint64_t
     if (cfg->shard_count > 1) {
       if (cfg->shard_index < 0 || cfg->shard_index >= cfg->shard_count)
         fail(CSB_EINVAL, "StreamConfig: shard_index must be in [0, shard_count)");
+      if (cfg->max_order > kMaxCumOrder) fail(CSB_EINVAL, "StreamConfig: sharding supports orders up to 6");
       const auto& cm = s->dev->comm;
       if (!cm || cm->nranks != cfg->shard_count || cm->rank != cfg->shard_index)
         fail(CSB_EINVAL, "prime: shard_count > 1 needs csb_comm_init(shard_count, shard_index, id) first");
@@ -1918,8 +1963,12 @@ uint64_t csb_launch_count(void) { return csb::launch_count(); }
 int csb_top_kernel(int dim, int max_order, int block, char* out, uint64_t cap) {
   return guard([&] {
     require(out && cap > 0, "top_kernel: null output");
-    require(dim >= 1 && block >= 1 && block <= dim && max_order >= 1 && max_order <= kMaxOrder,
+    require(dim >= 1 && block >= 1 && block <= dim && max_order >= 1 && max_order <= kMaxOrderAny,
             "top_kernel: bad shape");
+    if (max_order > kMaxOrder) {
+      std::snprintf(out, cap, "%s", "moment_generic_kernel (any order, one thread per stored element)");
+      return;
+    }
     MomParams p;
     p.n = dim;
     p.b = block;

@@ -206,3 +206,27 @@ def test_exact_sampled_oracle_matches_full_port(port):
             if s >= 2:
                 cv = port.sample_cumulants(c[:s - 1], n, b, s, idx, m[s - 1][off])
                 assert np.array_equal(cv, c[s - 1][off]), (n, d, s)
+
+
+HIGH = [(12, 3, 9, 2), (10, 4, 10, 3), (9, 3, 7, 2), (8, 2, 12, 1)]
+
+
+@pytest.mark.parametrize("shape", HIGH, ids=[f"r{a}_n{b}_d{c}_b{d}" for a, b, c, d in HIGH])
+def test_port_matches_live_reference_high_orders(port, ref, shape):
+    """Orders above the specialised kernels' range (the any-order device
+    kernels are checked against the port in tests/test_gpu_high_order.py)."""
+    rows, n, d, b = shape
+    rng = np.random.default_rng(4000 + rows + d)
+    x = rng.standard_normal((rows, n)) * 0.9 + 0.2
+    p = max(1, rows // 3)
+    xin = rng.standard_normal((p, n))
+    mp, mr = port.moment_series(x, d, b), ref.moment_series(x, d, b)
+    port.moments_update(mp, rows, xin, x[:p], b)
+    ref.moments_update(mr, rows, xin, x[:p], b)
+    for s in range(d):
+        assert np.array_equal(mp[s], mr[s]), f"M{s + 1}"
+    if d <= 10:
+        cp, cr = port.moms2cums(mp, n, b), ref.moms2cums(mr, n, b)
+        for s in range(d):
+            assert np.array_equal(cp[s], cr[s]), f"C{s + 1}"
+        assert port.report(cp, n, b, 2, rows) == ref.report(cr, n, b, 2, rows)
