@@ -21,6 +21,7 @@
 #include "cumstream_b200.h"
 
 #if __has_include(<json.hpp>)
+#include <exception>
 #include <json.hpp>  // nlohmann/json 3.11.3, the reference's JSON dependency
 #define CSB_HAVE_NLOHMANN 1
 #else
@@ -1018,19 +1019,39 @@ void run(const StreamConfig& config, BatchSource& source, const ReportSink& sink
   csb_report r{};
   check(csb_stream_report(state.device->st, &r));
   sink(to_report(r));
-  for (;;) {
+  // Pipelined ingestion: while the device runs step k, the
+  // host reads batch k + 1 from the source and starts its copy on the
+  // engine's copy stream; the report of step k is fetched afterwards.
+  const auto take = [&]() -> std::optional<DataBatch> {
     auto batch = source.next(config.update_len);
-    if (!batch) break;
+    if (!batch) return std::nullopt;
     if (batch->rows < config.update_len) {
       if (batch->rows > 0)
         std::cerr << "warning: discarding " << batch->rows << " trailing rows shorter than one update\n";
-      break;
+      return std::nullopt;
     }
     if (batch->cols != static_cast<std::size_t>(config.dim))
       throw std::invalid_argument("step: batch does not match the configured update");
-    check(csb_stream_step(state.device->st, batch->values.data(), batch->rows, batch->cols, nullptr, &r));
+    return batch;
+  };
+  csb_stream* st = state.device->st;
+  std::optional<DataBatch> cur = take();
+  if (cur) check(csb_stream_upload(st, cur->values.data(), cur->rows, cur->cols));
+  while (cur) {
+    check(csb_stream_step_uploaded(st, nullptr, nullptr));  // queued; returns at once
+    std::optional<DataBatch> next;
+    std::exception_ptr bad;  // a failing read surfaces after this step's report, as in the reference's loop
+    try {
+      next = take();  // host ingestion under the step
+      if (next) check(csb_stream_upload(st, next->values.data(), next->rows, next->cols));
+    } catch (...) {
+      bad = std::current_exception();
+    }
+    check(csb_stream_report(st, &r));  // waits for the step
     ++state.window;
     sink(to_report(r));
+    if (bad) std::rethrow_exception(bad);
+    cur = std::move(next);
   }
 }
 
