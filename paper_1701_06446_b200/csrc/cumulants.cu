@@ -355,7 +355,12 @@ __global__ void __launch_bounds__(S <= 4 ? 1024 : 256, S <= 4 ? 1 : 2) moms2cums
 // the buffer with the block after next.  The arithmetic per canonical
 // entry is moms2cums_v2's (partition_correction<S>, the reference's order),
 // written with its symmetric copies straight to global memory.
-// (Measured at cfg2 order 6: 1.76 ms for moms2cums_v2 -> 1.53 ms.  A variant
+// (Measured at cfg2 order 6: 1.76 ms for moms2cums_v2 -> 1.53 ms; 1.30 ms
+// with the refill's stage offsets from a shared table -- the refill is the
+// critical path between two blocks -- and the block bookkeeping and copy
+// targets requested ahead of their use.  Timing-only experiments: without
+// any store 1.46 of 1.51 ms; with 6 instead of 62 bulk copies per block
+// 1.42 of 1.57 ms: neither the stores nor the copy count bound it.  A variant
 // handing out 32-entry chunks of the oldest open block through a shared
 // cursor, so no warp waits for a block's stragglers, measured 1.66 ms:
 // the per-chunk hand-off costs more than the waits it removes.)
@@ -394,18 +399,25 @@ __global__ void __launch_bounds__(M2CP_THREADS, 1) moms2cums_persist(const M2CPa
   const uint32_t nmine = blockIdx.x < nblocks ? (nblocks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   // one warp: TMA bulk copies of block k's sub-blocks into buffer buf, the
   // lanes' copies (and their offset loads) in parallel
+  // (stage offsets and sizes per mask from a shared table: the refill sits on
+  // the critical path between two blocks, and deriving them per call cost
+  // the issuing warp thousands of dependent integer instructions)
+  __shared__ uint32_t soff[NM], svol[NM];
   auto issue = [&](uint32_t k, int buf) {
     const uint64_t blk = block_of(k);
     const uint64_t* subs = P.subs + blk * (NM - 1);
     if (lane == 0) ptx::mbar_expect_tx(&full[buf], STAGE * static_cast<uint32_t>(sizeof(double)));
     __syncwarp();
-    for (int m = 1 + lane; m < NM; m += 32) {
-      uint32_t o = 0;  // G::off(m) at run time
-      for (int q = 1; q < m; ++q) o += G::vol(q);
-      ptx::bulk_g2s(sfac + buf * STAGE + o, P.lower[popcount_c(m) - 1] + subs[m - 1],
-                    G::vol(m) * static_cast<uint32_t>(sizeof(double)), &full[buf]);
-    }
+    for (int m = 1 + lane; m < NM; m += 32)
+      ptx::bulk_g2s(sfac + buf * STAGE + soff[m], P.lower[__popc(m) - 1] + subs[m - 1],
+                    svol[m] * static_cast<uint32_t>(sizeof(double)), &full[buf]);
   };
+  for (int m = 1 + threadIdx.x; m < NM; m += M2CP_THREADS) {
+    uint32_t o = 0;
+    for (int q = 1; q < m; ++q) o += G::vol(q);
+    soff[m] = o;
+    svol[m] = G::vol(m);
+  }
   if (threadIdx.x == 0) {
     ptx::mbar_init(&full[0], 1);
     ptx::mbar_init(&full[1], 1);
@@ -419,35 +431,61 @@ __global__ void __launch_bounds__(M2CP_THREADS, 1) moms2cums_persist(const M2CPa
   bp[0] = 1;
 #pragma unroll
   for (int k = 1; k < S; ++k) bp[k] = bp[k - 1] * B;
+  // Block bookkeeping runs one block ahead of the arithmetic: block k + 1's
+  // coordinates and offset are requested when block k starts, its canonical
+  // list range and this thread's first entry (position, copy range, M value)
+  // before block k's reduction, so a block starts with its operands in
+  // registers instead of a chain of four dependent global loads.
+  uint16_t jn[S];
+  uint64_t boffn = 0;
+  auto request_block = [&](uint32_t k) {
+    const uint64_t blk = block_of(k);
+#pragma unroll
+    for (int q = 0; q < S; ++q) jn[q] = LS.index[blk * S + q];
+    boffn = LS.offset[blk];
+  };
+  uint32_t cbase_n = 0, cnt_n = 0;  // canonical list of the requested block
+  uint32_t npos = 0, nc0 = 0, nc1 = 0;
+  double nm = 0.0;
+  auto request_first = [&]() {
+    uint32_t pat = 0;
+#pragma unroll
+    for (int q = 1; q < S; ++q) pat |= static_cast<uint32_t>(jn[q] == jn[q - 1]) << (q - 1);
+    cbase_n = P.canon_off[pat];
+    cnt_n = P.canon_off[pat + 1] - cbase_n;
+    if (threadIdx.x < cnt_n) {
+      npos = __ldg(P.canon + cbase_n + threadIdx.x);
+      nc0 = __ldg(P.cstart + cbase_n + threadIdx.x);
+      nc1 = __ldg(P.cstart + cbase_n + threadIdx.x + 1);
+      nm = P.m[boffn + npos];
+    }
+  };
+  if (nmine) {
+    request_block(0);
+    request_first();
+  }
   for (uint32_t k = 0; k < nmine; ++k) {
     const int buf = static_cast<int>(k & 1);
     const uint64_t blk = block_of(k);
-    int j[S];
-#pragma unroll
-    for (int q = 0; q < S; ++q) j[q] = LS.index[blk * S + q];
-    const uint64_t boff = LS.offset[blk];
-    uint32_t pat = 0;
-#pragma unroll
-    for (int q = 1; q < S; ++q) pat |= static_cast<uint32_t>(j[q] == j[q - 1]) << (q - 1);
-    const uint32_t cbase = P.canon_off[pat];
-    const uint32_t cnt = P.canon_off[pat + 1] - cbase;
+    const uint64_t boff = boffn;
+    const uint32_t cbase = cbase_n, cnt = cnt_n;
+    if (k + 1 < nmine) request_block(k + 1);
     const double* sb = sfac + buf * STAGE;
     // software pipeline: the next entry's position, M value and copy range
     // are loaded before this entry's partition sum
     uint32_t i = threadIdx.x;
-    uint32_t npos = 0, nc0 = 0, nc1 = 0;
-    double nm = 0.0;
-    if (i < cnt) {
-      npos = __ldg(P.canon + cbase + i);
-      nc0 = __ldg(P.cstart + cbase + i);
-      nc1 = __ldg(P.cstart + cbase + i + 1);
-      nm = P.m[boff + npos];
-    }
     ptx::mbar_wait(&full[buf], (k >> 1) & 1u);
     double part = 0.0;
     for (; i < cnt; i += M2CP_THREADS) {
       const uint32_t pos = npos, c0 = nc0, c1 = nc1;
       const double mv = nm;
+      // this entry's first copy targets too: the stores after the partition
+      // sum then find their addresses in registers (a dependent global load
+      // there idled the whole CTA, whose warps reach it together)
+      constexpr uint32_t NPRE = 3;
+      uint32_t dpre[NPRE];
+#pragma unroll
+      for (uint32_t q = 0; q < NPRE; ++q) dpre[q] = c0 + q < c1 ? __ldg(P.cdst + c0 + q) : 0u;
       const uint32_t in = i + M2CP_THREADS;
       if (in < cnt) {
         npos = __ldg(P.canon + cbase + in);
@@ -474,17 +512,21 @@ __global__ void __launch_bounds__(M2CP_THREADS, 1) moms2cums_persist(const M2CPa
       }
       const double v = __dsub_rn(mv, partition_correction<S>(f));
       P.c[boff + pos] = v;
-      if (P.mfix) {  // the update's symmetric copies of M_6 too (deferred by run_moments)
-        for (uint32_t q = c0; q < c1; ++q) {
-          const uint32_t dst = __ldg(P.cdst + q);
-          P.c[boff + dst] = v;
-          P.mfix[boff + dst] = mv;
+      const bool fix = P.mfix != nullptr;  // the update's symmetric copies of M_6 too (deferred by run_moments)
+#pragma unroll
+      for (uint32_t q = 0; q < NPRE; ++q)
+        if (c0 + q < c1) {
+          P.c[boff + dpre[q]] = v;
+          if (fix) P.mfix[boff + dpre[q]] = mv;
         }
-      } else {
-        for (uint32_t q = c0; q < c1; ++q) P.c[boff + __ldg(P.cdst + q)] = v;
+      for (uint32_t q = c0 + NPRE; q < c1; ++q) {
+        const uint32_t dst = __ldg(P.cdst + q);
+        P.c[boff + dst] = v;
+        if (fix) P.mfix[boff + dst] = mv;
       }
       part = __fma_rn(static_cast<double>(1u + c1 - c0), __dmul_rn(v, v), part);
     }
+    if (k + 1 < nmine) request_first();  // lands under the reduction and the next buffer's wait
     for (int s = 16; s > 0; s >>= 1) part = __dadd_rn(part, __shfl_down_sync(0xffffffffu, part, s));
     __syncwarp();  // every lane's reads of the buffer precede lane 0's release below
     uint32_t last = 0;
