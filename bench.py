@@ -379,14 +379,17 @@ def main() -> None:
     top_avg_s = (top_ms / max(1, top_n)) * 1e-3
     achieved = flops["F_top_launch"] / top_avg_s / 1e12 if top_n else None
     traffic = None
-    tr_path = os.path.join(ROOT, "profiles", "moment_top_traffic.json")
-    if os.path.exists(tr_path):
+    tr_src = None
+    for tr_path in (os.path.join(ROOT, "profiles", "r02", "moment_top_traffic_cfg2.json"),
+                    os.path.join(ROOT, "profiles", "moment_top_traffic.json")):
         try:
             tr = json.load(open(tr_path))
             if tr.get("workload") == cfg.name:
                 traffic = tr.get("bytes_per_launch")
+                tr_src = os.path.relpath(tr_path, ROOT)
+                break
         except (OSError, ValueError):
-            traffic = None
+            continue
     hbm_peak = None
     try:
         hbm_peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs")
@@ -420,7 +423,7 @@ def main() -> None:
                          "note": "FP64 path: bound is the FP64 pipe (DFMA/DMMA), not bf16 tensor",
                          "hbm": ({"traffic_bytes": traffic, "achieved_gbs": traffic / top_avg_s / 1e9,
                                   "peak_gbs": hbm_peak, "frac": traffic / top_avg_s / 1e9 / hbm_peak,
-                                  "source": "ncu dram__bytes_read+write of one launch (profiles/moment_top_traffic.json)"}
+                                  "source": f"ncu dram__bytes_read+write of one launch ({tr_src})"}
                                  if traffic and top_n else None)},
             "step_flops": {"F_alg": flops["F_alg"], "F_mom": flops["F_mom"], "F_m2c": flops["F_m2c"],
                            "alg_tflops_per_s": flops["F_alg"] / (dev_s / args.steps) / 1e12},
