@@ -359,12 +359,20 @@ def main() -> None:
     ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
     torch.cuda.synchronize()
+    # the library's pipelined ingestion (csb_stream_upload / csb_stream_step_uploaded, what the C++ run() loop
+    # uses): step k is queued, then batch k+1's host-to-device copy is started on the copy stream and runs under
+    # it, then step k's report is read back; every batch is copied inside a timed interval (batch 0 inside step
+    # 0's, serialized)
     for k in range(args.steps):
         flush.fill_(float(k))
         torch.cuda.synchronize()
         ev2[k][0].record(cs)
-        xk = pinned[k].numpy()
-        rep2 = st.step(xk, report=True)
+        if k == 0:
+            st.upload(pinned[0].numpy())
+        st.step_uploaded(report=False)       # queued; returns at once
+        if k + 1 < args.steps:
+            st.upload(pinned[k + 1].numpy())  # the next batch's copy, under this step
+        rep2 = st.report()                    # waits for the step, reads the report back
         ev2[k][1].record(cs)
     torch.cuda.synchronize()
     e2e_s = sum(a.elapsed_time(b) for a, b in ev2) * 1e-3
@@ -428,7 +436,9 @@ def main() -> None:
             "step_flops": {"F_alg": flops["F_alg"], "F_mom": flops["F_mom"], "F_m2c": flops["F_m2c"],
                            "alg_tflops_per_s": flops["F_alg"] / (dev_s / args.steps) / 1e12},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": cfg.p * cfg.n * 8,
-                    "d2h_bytes_per_step": (cfg.d + 3 * cfg.n) * 8},
+                    "d2h_bytes_per_step": (cfg.d + 3 * cfg.n) * 8,
+                    "api": "csb_stream_upload + csb_stream_step_uploaded with pinned host rows (batch k+1's copy "
+                           "under step k, as the C++ run() loop does) + report read back every step"},
             "gpu_launches": launches,
             "clocks": clocks.summary(),
             "wall_s_timed_region": wall,
