@@ -5,7 +5,9 @@
 #include <cuda_runtime.h>
 #include <cstdio>
 
-template <int RI, int CJ, bool ROWMAJOR>
+// ORDER 0: column-major (x shared by consecutive DFMAs), 1: row-major (q
+// shared), 2: diagonal sweeps (consecutive DFMAs share no operand)
+template <int RI, int CJ, int ROWMAJOR>
 __global__ void __launch_bounds__(384, 1) k(double* out, int iters, double a) {
   extern __shared__ double sm[];
   double acc[RI][CJ], q[RI], x[CJ];
@@ -18,7 +20,21 @@ __global__ void __launch_bounds__(384, 1) k(double* out, int iters, double a) {
 #pragma unroll
     for (int j = 0; j < CJ; ++j) acc[i][j] = i + j;
   for (int it = 0; it < iters; ++it) {
-    if (ROWMAJOR) {
+    if (ROWMAJOR == 2) {
+#pragma unroll
+      for (int t = 0; t < CJ; ++t)
+#pragma unroll
+        for (int i = 0; i < RI; ++i) {
+          asm volatile("fma.rn.f64 %0, %1, %2, %0;" : "+d"(acc[i][(i + t) % CJ]) : "d"(q[i]), "d"(x[(i + t) % CJ]));
+        }
+    } else if (ROWMAJOR == 3) {  // row-major through volatile asm (order kept at the PTX level)
+#pragma unroll
+      for (int i = 0; i < RI; ++i)
+#pragma unroll
+        for (int j = 0; j < CJ; ++j) {
+          asm volatile("fma.rn.f64 %0, %1, %2, %0;" : "+d"(acc[i][j]) : "d"(q[i]), "d"(x[j]));
+        }
+    } else if (ROWMAJOR == 1) {
 #pragma unroll
       for (int i = 0; i < RI; ++i)
 #pragma unroll
@@ -38,7 +54,7 @@ __global__ void __launch_bounds__(384, 1) k(double* out, int iters, double a) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
-template <int RI, int CJ, bool ROWMAJOR>
+template <int RI, int CJ, int ROWMAJOR>
 void run(int sms, double* out, double mhz) {
   const int threads = 384, iters = 20000;
   const size_t smem = 120 * 1024;
@@ -60,7 +76,11 @@ void run(int sms, double* out, double mhz) {
   const double dfma = (double)sms * threads * RI * CJ * iters;
   const double per = dfma / (best * 1e-3) / (mhz * 1e6) / sms;
   printf("{\"tile\": \"%dx%d\", \"order\": \"%s\", \"dfma_per_clk_sm\": %.2f, \"frac_of_64\": %.3f}\n", RI, CJ,
-         ROWMAJOR ? "row-major (q shared by consecutive DFMAs)" : "column-major (x shared)", per, per / 64.0);
+         ROWMAJOR == 1 ? "row-major (q shared by consecutive DFMAs)"
+         : ROWMAJOR == 0 ? "column-major (x shared)"
+         : ROWMAJOR == 2 ? "diagonal sweeps via volatile asm (nothing shared)"
+                         : "row-major via volatile asm",
+         per, per / 64.0);
 }
 
 int main() {
@@ -72,11 +92,13 @@ int main() {
   cudaMalloc(&out, sizeof(double) * p.multiProcessorCount * 1024);
   const int sms = p.multiProcessorCount;
   const double mhz = khz / 1000.0;
-  run<4, 8, true>(sms, out, mhz);
-  run<4, 8, false>(sms, out, mhz);
-  run<8, 4, true>(sms, out, mhz);
-  run<8, 8, true>(sms, out, mhz);
-  run<6, 6, true>(sms, out, mhz);
-  run<2, 16, true>(sms, out, mhz);
+  run<4, 8, 1>(sms, out, mhz);
+  run<4, 8, 0>(sms, out, mhz);
+  run<4, 8, 2>(sms, out, mhz);
+  run<4, 8, 3>(sms, out, mhz);
+  run<8, 8, 1>(sms, out, mhz);
+  run<8, 8, 2>(sms, out, mhz);
+  run<8, 8, 3>(sms, out, mhz);
+  run<6, 6, 1>(sms, out, mhz);
   return cudaDeviceSynchronize() != cudaSuccess;
 }
