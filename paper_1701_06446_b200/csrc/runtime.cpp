@@ -7,6 +7,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <thread>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -573,17 +574,29 @@ void check_order(const csb_series* s, int order) {
   if (order < 1 || order > s->d) fail(CSB_ERANGE, "series: order out of range");
 }
 
+// Captured step graphs hold raw scratch pointers: every (re)allocation or
+// release of a scratch buffer bumps this generation, and a graph captured
+// under an older one is dropped and captured again instead of replayed.
+std::atomic<uint64_t> g_scratch_gen{1};
+
 // Scratch buffer for the pass-0 stash of the update kernel (per device).
 struct Scratch {
   DevBuf<double> buf;
   DevBuf<uint32_t> flags;
+  ~Scratch() { g_scratch_gen.fetch_add(1, std::memory_order_relaxed); }
   double* get(uint64_t count) {
-    if (buf.count < count) buf.alloc(count);
+    if (buf.count < count) {
+      buf.alloc(count);
+      g_scratch_gen.fetch_add(1, std::memory_order_relaxed);
+    }
     return buf.ptr;
   }
   DevBuf<double> tail;  // the tail kernel's per-SM stash (beside the DMMA kernel's scratch)
   double* get_tail(uint64_t count) {
-    if (tail.count < count) tail.alloc(count);
+    if (tail.count < count) {
+      tail.alloc(count);
+      g_scratch_gen.fetch_add(1, std::memory_order_relaxed);
+    }
     return tail.ptr;
   }
   DevBuf<double> zeros;
@@ -591,6 +604,7 @@ struct Scratch {
     if (zeros.count < count) {
       zeros.alloc(count);
       memset_sync(zeros.ptr, 0, zeros.bytes());
+      g_scratch_gen.fetch_add(1, std::memory_order_relaxed);
     }
     return zeros.ptr;
   }
@@ -598,6 +612,7 @@ struct Scratch {
     if (flags.count < count) {
       flags.alloc(count);
       memset_sync(flags.ptr, 0, flags.bytes());
+      g_scratch_gen.fetch_add(1, std::memory_order_relaxed);
     }
     return flags.ptr;
   }
@@ -1158,6 +1173,8 @@ struct csb_stream {
     uint32_t exact_mask_after = 0;
     int early_m2c = 0;
     uint64_t launches = 0;
+    uint64_t scratch_gen = 0;  // g_scratch_gen at capture: the graph's scratch pointers are valid under it
+    std::thread::id owner;     // the capturing thread (scratch buffers are per thread)
   };
   std::map<std::tuple<uint64_t, const double*, int>, StepGraph> graphs;
   bool use_graphs = true;
@@ -1289,6 +1306,12 @@ int stream_step_impl(csb_stream* s, const double* x, bool on_device, uint64_t ro
       if (it != s->graphs.end()) sg = &it->second;
       else if (s->graphs.size() < 256) sg = &s->graphs[key];  // (callers cycling through many buffers stay eager)
     }
+    if (sg && sg->exec && (sg->scratch_gen != g_scratch_gen.load(std::memory_order_relaxed) ||
+                           sg->owner != std::this_thread::get_id())) {
+      // a scratch buffer moved since the capture, or another thread (with its own scratch) steps now
+      cudaGraphExecDestroy(sg->exec);
+      sg->exec = nullptr;  // seen stays set: captured again below
+    }
     if (sg && sg->exec) {
       // replay: the device work of the captured step, then its host-side bookkeeping
       CSB_CUDA(cudaGraphLaunch(sg->exec, s->st));
@@ -1319,6 +1342,8 @@ int stream_step_impl(csb_stream* s, const double* x, bool on_device, uint64_t ro
       if (ok && cudaGraphInstantiate(&sg->exec, graph, 0) != cudaSuccess) ok = false;
       if (graph) cudaGraphDestroy(graph);
       if (ok) {
+        sg->scratch_gen = g_scratch_gen.load(std::memory_order_relaxed);
+        sg->owner = std::this_thread::get_id();
         sg->launches = launch_count() - l0;
         sg->exact_mask_after = s->ns.exact_mask;
         sg->early_m2c = s->early_m2c;

@@ -71,3 +71,35 @@ def test_resync_steps_stay_eager():
     for s in range(4):
         assert np.array_equal(m0[s], m1[s]) and np.array_equal(c0[s], c1[s])
     assert r0 == r1
+
+
+def test_graphs_survive_scratch_growth():
+    """A captured graph holds raw scratch pointers; a larger shape used in
+    between reallocates the scratch, so the graph must be dropped and
+    captured again (generation check), not replayed on freed memory."""
+    from paper_1701_06446_b200 import capi
+
+    case = (24, 4, 3, 64, 16, 30, 56)
+    n, d, b, T, p, steps, seed = case
+    rows = case_rows(n, T, p, steps, seed)
+
+    def run(graphs, disturb):
+        st = capi.Stream(n, d, T, p, b, rows[:T], resync_every=0)
+        st.use_graphs(graphs)
+        reps = []
+        for k in range(steps):
+            if disturb and k == 14:  # graphs are replaying by now: grow the scratch under them
+                # more tiles than any shape this process has run: the DMMA stash must grow
+                big = np.random.default_rng(1).standard_normal((64, 56))
+                capi.moments_update(capi.moment_series(big, 6, 4), big[:16], big[16:32])
+            reps.append(st.step(rows[T + k * p: T + (k + 1) * p]))
+        out = (st.moments(), st.cumulants(), reps, st.graph_replays())
+        st.close()
+        return out
+
+    m0, c0, r0, _ = run(False, False)
+    m1, c1, r1, n1 = run(True, True)
+    assert n1 >= 4
+    assert r0 == r1
+    for s in range(d):
+        assert np.array_equal(m0[s], m1[s]) and np.array_equal(c0[s], c1[s])
