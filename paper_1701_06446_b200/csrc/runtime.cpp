@@ -933,7 +933,12 @@ void run_moms2cums(const csb_series* m, csb_series* c, NormScratch& ns, cudaStre
     for (int k = 1; k <= s; ++k) p.lay[k - 1] = m->lay[k - 1]->view();
     p.n = m->n;
     p.b = m->b;
-    p.fold_width = host_fold_width();
+    // the block's exact norm partial inside moms2cums (one thread chains the
+    // assembled block while the CTA writes it out) pays for few blocks; with
+    // thousands the chain-per-lane kernel of finalize_norms is cheaper
+    // (measured: cfg2 C_5, 4368 blocks, 0.293 -> 0.187 ms against +0.039 ms there;
+    // cfg1/cfg2 C_4, 1365 blocks: in-kernel wins)
+    p.fold_width = m->lay[s - 1]->host.nblocks > 3000 ? 0 : host_fold_width();
     p.subs = get_subs(*m->dev, s, m->n, m->b)->ptr;
     {
       uint64_t vol = 1;
