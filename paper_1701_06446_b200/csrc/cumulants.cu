@@ -346,16 +346,20 @@ __global__ void __launch_bounds__(S <= 4 ? 1024 : 256, S <= 4 ? 1 : 2) moms2cums
 
 // ---------------------------------------------------------------------------
 // moms2cums of a high order over full blocks (every extent B), persistent:
-// one CTA per SM walks its blocks blockIdx.x, + gridDim.x, ... with the
-// 2^S - 2 lower-order sub-blocks of the NEXT block landing by TMA bulk
-// copies in a second buffer while the current one is computed, and no
-// CTA-wide barrier per block: each warp reduces its share of the block's
-// sum of squares, the last warp to finish a block (shared-memory counter)
-// adds the warp sums in warp order, writes the block's partial and refills
-// the buffer with the block after next.  The arithmetic per canonical
+// one CTA per SM, two halves of 8 warps; each half walks its share of the
+// CTA's blocks with the block's 2^S - 2 lower-order sub-blocks landing by TMA
+// bulk copies in the half's own buffer, and no CTA-wide barrier: each warp
+// reduces its share of the block's sum of squares, the last warp of the
+// half to finish a block (shared-memory counter) adds the warp sums in warp
+// order, writes the block's partial and refills the buffer with the half's
+// next block -- whose wait the other half's arithmetic covers.  The arithmetic per canonical
 // entry is moms2cums_v2's (partition_correction<S>, the reference's order),
 // written with its symmetric copies straight to global memory.
 // (Measured at cfg2 order 6: 1.76 ms for moms2cums_v2 -> 1.53 ms; 1.30 ms
+// double-buffered with all 16 warps on one block; 1.17 ms as two halves of
+// 8 warps with a block and a buffer each -- one half computes while the other
+// waits for its sub-blocks; 1.10 ms with the blocks dealt in descending
+// order of canonical entries.  Earlier steps: 1.30 ms
 // with the refill's stage offsets from a shared table -- the refill is the
 // critical path between two blocks -- and the block bookkeeping and copy
 // targets requested ahead of their use.  Timing-only experiments: without
@@ -395,8 +399,19 @@ __global__ void __launch_bounds__(M2CP_THREADS, 1) moms2cums_persist(const M2CPa
   __shared__ double red[2][M2CP_WARPS];
   const LayoutDev& LS = P.lay[S - 1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  auto block_of = [&](uint32_t k) { return P.blk0 + blockIdx.x + static_cast<uint64_t>(k) * gridDim.x; };
-  const uint32_t nmine = blockIdx.x < nblocks ? (nblocks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  // The CTA works as two halves of 8 warps, each on a block of its own in a
+  // buffer of its own (the CTA's blocks alternate between them): while one
+  // half waits for its next block's sub-blocks the other keeps the FP64 pipe
+  // busy, instead of all 16 warps reaching the same hand-off together.
+  constexpr int HW = M2CP_WARPS / 2, HT = M2CP_THREADS / 2;
+  const int half = warp / HW, hw = warp % HW;
+  const uint32_t ht = threadIdx.x % HT;
+  const uint32_t ncta = blockIdx.x < nblocks ? (nblocks - 1 - blockIdx.x) / gridDim.x + 1 : 0;  // this CTA's blocks
+  const uint32_t nmine = (ncta + 1 - half) / 2;                                                   // this half's
+  auto block_of = [&](uint32_t k) {
+    const uint64_t idx = blockIdx.x + static_cast<uint64_t>(2 * k + half) * gridDim.x;
+    return P.blk0 + (P.order ? static_cast<uint64_t>(__ldg(P.order + idx)) : idx);
+  };
   // one warp: TMA bulk copies of block k's sub-blocks into buffer buf, the
   // lanes' copies (and their offset loads) in parallel
   // (stage offsets and sizes per mask from a shared table: the refill sits on
@@ -425,8 +440,7 @@ __global__ void __launch_bounds__(M2CP_THREADS, 1) moms2cums_persist(const M2CPa
     ptx::fence_mbar_init();
   }
   __syncthreads();
-  if (warp == 0)
-    for (uint32_t k = 0; k < 2 && k < nmine; ++k) issue(k, static_cast<int>(k));
+  if (hw == 0 && nmine) issue(0, half);
   uint32_t bp[S];  // B^0 .. B^(S-1)
   bp[0] = 1;
 #pragma unroll
@@ -453,10 +467,10 @@ __global__ void __launch_bounds__(M2CP_THREADS, 1) moms2cums_persist(const M2CPa
     for (int q = 1; q < S; ++q) pat |= static_cast<uint32_t>(jn[q] == jn[q - 1]) << (q - 1);
     cbase_n = P.canon_off[pat];
     cnt_n = P.canon_off[pat + 1] - cbase_n;
-    if (threadIdx.x < cnt_n) {
-      npos = __ldg(P.canon + cbase_n + threadIdx.x);
-      nc0 = __ldg(P.cstart + cbase_n + threadIdx.x);
-      nc1 = __ldg(P.cstart + cbase_n + threadIdx.x + 1);
+    if (ht < cnt_n) {
+      npos = __ldg(P.canon + cbase_n + ht);
+      nc0 = __ldg(P.cstart + cbase_n + ht);
+      nc1 = __ldg(P.cstart + cbase_n + ht + 1);
       nm = P.m[boffn + npos];
     }
   };
@@ -465,7 +479,7 @@ __global__ void __launch_bounds__(M2CP_THREADS, 1) moms2cums_persist(const M2CPa
     request_first();
   }
   for (uint32_t k = 0; k < nmine; ++k) {
-    const int buf = static_cast<int>(k & 1);
+    const int buf = half;
     const uint64_t blk = block_of(k);
     const uint64_t boff = boffn;
     const uint32_t cbase = cbase_n, cnt = cnt_n;
@@ -473,10 +487,10 @@ __global__ void __launch_bounds__(M2CP_THREADS, 1) moms2cums_persist(const M2CPa
     const double* sb = sfac + buf * STAGE;
     // software pipeline: the next entry's position, M value and copy range
     // are loaded before this entry's partition sum
-    uint32_t i = threadIdx.x;
-    ptx::mbar_wait(&full[buf], (k >> 1) & 1u);
+    uint32_t i = ht;
+    ptx::mbar_wait(&full[buf], k & 1u);
     double part = 0.0;
-    for (; i < cnt; i += M2CP_THREADS) {
+    for (; i < cnt; i += HT) {
       const uint32_t pos = npos, c0 = nc0, c1 = nc1;
       const double mv = nm;
       // this entry's first copy targets too: the stores after the partition
@@ -486,7 +500,7 @@ __global__ void __launch_bounds__(M2CP_THREADS, 1) moms2cums_persist(const M2CPa
       uint32_t dpre[NPRE];
 #pragma unroll
       for (uint32_t q = 0; q < NPRE; ++q) dpre[q] = c0 + q < c1 ? __ldg(P.cdst + c0 + q) : 0u;
-      const uint32_t in = i + M2CP_THREADS;
+      const uint32_t in = i + HT;
       if (in < cnt) {
         npos = __ldg(P.canon + cbase + in);
         nc0 = __ldg(P.cstart + cbase + in);
@@ -531,21 +545,21 @@ __global__ void __launch_bounds__(M2CP_THREADS, 1) moms2cums_persist(const M2CPa
     __syncwarp();  // every lane's reads of the buffer precede lane 0's release below
     uint32_t last = 0;
     if (lane == 0) {
-      red[buf][warp] = part;
+      red[buf][hw] = part;
       __threadfence_block();
-      last = atomicAdd(&done[buf], 1u) == M2CP_WARPS - 1;
+      last = atomicAdd(&done[buf], 1u) == HW - 1;
     }
     if (__shfl_sync(0xffffffffu, last, 0)) {  // the last warp of this block
       __threadfence_block();
       if (lane == 0) {
         double s = 0.0;
-        for (int w = 0; w < M2CP_WARPS; ++w) s = __dadd_rn(s, red[buf][w]);
+        for (int w = 0; w < HW; ++w) s = __dadd_rn(s, red[buf][w]);
         P.partial[blk - P.blk0] = s;
         *reinterpret_cast<volatile uint32_t*>(&done[buf]) = 0;
       }
-      if (k + 2 < nmine) {
+      if (k + 1 < nmine) {
         ptx::fence_proxy_async();  // every warp's generic reads of the buffer before the async-proxy refill
-        issue(k + 2, buf);
+        issue(k + 1, buf);
       }
     }
   }

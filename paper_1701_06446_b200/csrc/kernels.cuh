@@ -68,6 +68,10 @@ struct M2CParams {
   // them and weights the norm term by 1 + copies right after computing it
   const uint32_t* cstart = nullptr;
   const uint32_t* cdst = nullptr;
+  // persistent kernel: the blocks in descending order of canonical entries
+  // (nullptr: block order); CTAs take them round-robin, so every CTA's -- and
+  // each of its halves' -- share of the arithmetic is the same within a block
+  const uint32_t* order = nullptr;
   double* partial = nullptr;        // per block: sum over stored entries of v*v
   int fold_width = 0;               // > 0: exact knorm partials (in-block path; see launch_moms2cums_v2)
 };

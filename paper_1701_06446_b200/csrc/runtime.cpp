@@ -7,6 +7,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <numeric>
 #include <thread>
 #include <cstdlib>
 #include <cstring>
@@ -69,6 +70,7 @@ struct Device {
   std::map<std::tuple<int, int, int>, std::shared_ptr<DevBuf<LowerElem>>> lower;
   std::map<std::tuple<int, int, int>, std::shared_ptr<DevBuf<LowerThread>>> lower2;
   std::map<std::tuple<int, int, int>, std::shared_ptr<DevBuf<uint64_t>>> subs;
+  std::map<std::tuple<int, int, int>, std::shared_ptr<DevBuf<uint32_t>>> m2c_order;
   std::map<std::pair<int, int>, std::pair<std::shared_ptr<DevBuf<uint32_t>>, std::shared_ptr<DevBuf<uint32_t>>>> canon;
   std::map<std::pair<int, int>, std::pair<std::shared_ptr<DevBuf<uint2>>, std::shared_ptr<DevBuf<uint32_t>>>> mirror;
   std::map<std::pair<int, int>, std::pair<std::shared_ptr<DevBuf<uint32_t>>, std::shared_ptr<DevBuf<uint32_t>>>> copies;
@@ -291,6 +293,37 @@ std::shared_ptr<DevBuf<uint64_t>> get_subs(Device& dev, int S, int n, int b) {
       }
     auto buf = std::make_shared<DevBuf<uint64_t>>(v.size());
     if (!v.empty()) h2d_sync(buf->ptr, v.data(), buf->bytes());
+    slot = buf;
+  }
+  return slot;
+}
+
+// Blocks of order S sorted by descending number of canonical entries
+// (prod over runs of equal block coordinate of C(e + r - 1, r), e the run's
+// extent), ties in block order: the persistent moms2cums kernel deals them
+// round-robin to its CTAs.
+std::shared_ptr<DevBuf<uint32_t>> get_m2c_order(Device& dev, int S, int n, int b) {
+  auto lay = get_layout(dev, S, n, b);
+  std::lock_guard<std::mutex> lk(dev.mu);
+  auto& slot = dev.m2c_order[{S, n, b}];
+  if (!slot) {
+    const Layout& L = lay->host;
+    std::vector<uint64_t> cost(L.nblocks);
+    for (uint64_t r = 0; r < L.nblocks; ++r) {
+      uint64_t c = 1;
+      for (int k = 0; k < S;) {
+        int e = k + 1;
+        while (e < S && L.index[r * S + e] == L.index[r * S + k]) ++e;
+        c *= multiset_count(L.ext(L.index[r * S + k]), e - k);
+        k = e;
+      }
+      cost[r] = c;
+    }
+    std::vector<uint32_t> ord(L.nblocks);
+    std::iota(ord.begin(), ord.end(), 0u);
+    std::stable_sort(ord.begin(), ord.end(), [&](uint32_t a, uint32_t c2) { return cost[a] > cost[c2]; });
+    auto buf = std::make_shared<DevBuf<uint32_t>>(ord.size());
+    if (!ord.empty()) h2d_sync(buf->ptr, ord.data(), buf->bytes());
     slot = buf;
   }
   return slot;
@@ -959,6 +992,7 @@ void run_moms2cums(const csb_series* m, csb_series* c, NormScratch& ns, cudaStre
       p.mfix = m->data[s - 1].ptr;  // write M_s's copies too (run_moments deferred them)
       m->mirror_defer &= ~(1u << (s - 1));
     }
+    if (s == 6 && !(s == d && sh.active())) p.order = get_m2c_order(*m->dev, s, m->n, m->b)->ptr;  // persistent kernel
     if (s == d && sh.active()) {
       // C_d only for the owned blocks; the other partials stay zero so a
       // sum over ranks reproduces the unsharded partial array exactly
