@@ -817,7 +817,7 @@ size_t m2c_block_vol(int S, int n, int b) {
 
 bool m2c_fuse_ok(int S, int n, int b) {
   if (S < 2 || S > 6 || n % b != 0) return false;  // every block full
-  if (S == 6 && b == 4) return true;  // moms2cums_persist writes M's copies beside C's
+  if ((S == 6 || S == 5) && b == 4) return true;  // moms2cums_persist writes M's copies beside C's
   const size_t sm0 = moms2cums_stage_bytes(S, n, b);
   const size_t vol = m2c_block_vol(S, n, b);
   return sm0 <= 160 * 1024 && vol <= (1u << 20) && sm0 + vol * sizeof(double) <= kM2cInblkLimit;
@@ -827,21 +827,28 @@ bool m2c_fuse_ok(int S, int n, int b) {
 // b = 4), the direct canonical-list path (no in-block pass, no deferred M
 // mirror) -- two buffers of the 62 staged sub-blocks (2 x 92 KB) per SM.
 bool m2c_persist_ok(int S, const M2CParams& p) {
-  return S == 6 && p.b == 4 && p.n % 4 == 0 && p.canon && p.cstart &&
+  return (S == 6 || S == 5) && p.b == 4 && p.n % 4 == 0 && p.canon && p.cstart &&
          2 * M2cStage<6, 4>::total() * sizeof(double) <= 200 * 1024;
+}
+
+template <int S>
+void launch_m2c_persist(const M2CParams& p, uint64_t nblocks, cudaStream_t st) {
+  static int sms = 0;
+  if (!sms) CSB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  const size_t smem = 2 * M2cStage<S, 4>::total() * sizeof(double);
+  ensure_smem(moms2cums_persist<S, 4>, smem);
+  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(nblocks, static_cast<uint64_t>(sms)));
+  moms2cums_persist<S, 4><<<grid, M2CP_THREADS, smem, st>>>(p, static_cast<uint32_t>(nblocks));
+  CSB_CUDA(cudaGetLastError());
+  count_launch();
 }
 
 bool launch_moms2cums_v2(int S, const M2CParams& p, uint64_t nblocks, cudaStream_t st) {
   if (nblocks == 0) return false;
-  if (m2c_persist_ok(S, p)) {
-    static int sms = 0;
-    if (!sms) CSB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
-    const size_t smem = 2 * M2cStage<6, 4>::total() * sizeof(double);
-    ensure_smem(moms2cums_persist<6, 4>, smem);
-    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(nblocks, static_cast<uint64_t>(sms)));
-    moms2cums_persist<6, 4><<<grid, M2CP_THREADS, smem, st>>>(p, static_cast<uint32_t>(nblocks));
-    CSB_CUDA(cudaGetLastError());
-    count_launch();
+  // (order 5 only with thousands of blocks: with few, the in-block pass and its exact norm partials win)
+  if (m2c_persist_ok(S, p) && (S == 6 || nblocks > 3000)) {
+    if (S == 6) launch_m2c_persist<6>(p, nblocks, st);
+    else launch_m2c_persist<5>(p, nblocks, st);
     return false;
   }
   const unsigned g = static_cast<unsigned>(nblocks);

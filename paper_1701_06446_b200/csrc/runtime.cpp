@@ -992,7 +992,8 @@ void run_moms2cums(const csb_series* m, csb_series* c, NormScratch& ns, cudaStre
       p.mfix = m->data[s - 1].ptr;  // write M_s's copies too (run_moments deferred them)
       m->mirror_defer &= ~(1u << (s - 1));
     }
-    if (s == 6 && !(s == d && sh.active())) p.order = get_m2c_order(*m->dev, s, m->n, m->b)->ptr;  // persistent kernel
+    if ((s == 6 || s == 5) && m->b == 4 && !(s == d && sh.active()))
+      p.order = get_m2c_order(*m->dev, s, m->n, m->b)->ptr;  // persistent kernel
     if (s == d && sh.active()) {
       // C_d only for the owned blocks; the other partials stay zero so a
       // sum over ranks reproduces the unsharded partial array exactly
