@@ -1270,8 +1270,9 @@ void stream_exchange_and_update(csb_stream* s, const double* x_dev) {
     src[0].seg0 = x_dev;
     src[0].len0 = static_cast<uint32_t>(p);
     src[1] = out;
-    // C_1, C_2 need only M_1, M_2 (the low-order kernel's): on the side stream
-    const int early = s->sh.active() ? 0 : std::min(2, cfg.max_order - 2);
+    // C_1 .. C_{d-2} need only M_1 .. M_{d-2} (the low-order kernel's): on
+    // the side stream, under the top pair (cfg2: C_1..C_4, 0.04 ms off the step)
+    const int early = s->sh.active() ? 0 : std::min(4, cfg.max_order - 2);
     std::function<void(cudaStream_t)> tail;
     if (early >= 1)
       tail = [s, early](cudaStream_t side) { run_moms2cums(s->M.get(), s->C.get(), s->ns, side, s->sh, 1, early); };
