@@ -214,13 +214,26 @@ def shard_range(max_order: int, dim: int, block: int, shard: int, count: int, wh
     return tuple(x.value for x in v)
 
 
+def _prefer_torch_nccl() -> None:
+    """The library resolves NCCL at run time and reuses a copy the process
+    already holds.  If PyTorch is going to be imported in this process, import
+    it first: its bundled libnccl.so.2 then is the one both sides use (loading
+    the system's first would leave torch's import with a mismatched NCCL)."""
+    try:
+        import torch  # noqa: F401
+    except ImportError:
+        pass
+
+
 def comm_unique_id() -> bytes:
+    _prefer_torch_nccl()
     buf = C.create_string_buffer(128)
     check(lib().csb_comm_unique_id(buf))
     return buf.raw
 
 
 def comm_init(nranks: int, rank: int, uid: bytes) -> None:
+    _prefer_torch_nccl()
     check(lib().csb_comm_init(nranks, rank, uid))
 
 

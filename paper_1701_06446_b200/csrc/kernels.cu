@@ -426,7 +426,7 @@ constexpr int NF_SLICE = 2048;
 __global__ void __launch_bounds__(NF_THREADS) norm_finalize_kernel(const NormParams P) {
   __shared__ double prod[2][NF_SLICE];
   const int s = static_cast<int>(blockIdx.x);
-  if (s < P.norders) {
+  if (P.fold && s < P.norders) {
     const double* __restrict__ mult = P.mult[s];
     const double* __restrict__ part = P.partial[s];
     const uint64_t nb = P.nblocks[s];
@@ -518,7 +518,7 @@ void launch_copy_c1(const double* m1, double* c1, double* partial, const LayoutD
 }
 
 void launch_norm_finalize(const NormParams& p, cudaStream_t st) {
-  norm_finalize_kernel<<<std::max(1, p.norders), NF_THREADS, 0, st>>>(p);
+  norm_finalize_kernel<<<p.fold ? std::max(1, p.norders) : 1, NF_THREADS, 0, st>>>(p);
   CSB_CUDA(cudaGetLastError());
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }

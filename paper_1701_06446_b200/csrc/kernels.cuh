@@ -123,6 +123,7 @@ struct NormParams {
   const double* mult[kMaxOrderAny];     // per order block multiplicities (as double)
   uint64_t nblocks[kMaxOrderAny];
   int norders = 0;                   // orders 1..norders
+  bool fold = true;                  // false: only the diagonals are gathered (the host folds the blocks)
   const double* diag_src[3];         // C_2, C_3, C_4 (nullptr if absent)
   const uint64_t* diag_off[3];       // n offsets each
   int n = 0;

@@ -40,9 +40,16 @@ Api& api() {
   static Api a;
   static std::once_flag once;
   std::call_once(once, [] {
+    // an NCCL the process already holds (e.g. the one PyTorch bundles) first;
+    // else the system's, loaded RTLD_LOCAL so its symbols do not shadow a
+    // different NCCL that a later import brings along
     for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
-      a.h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+      a.h = dlopen(name, RTLD_NOW | RTLD_NOLOAD);
       if (a.h) break;
+    }
+    for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+      if (a.h) break;
+      a.h = dlopen(name, RTLD_NOW | RTLD_LOCAL);
     }
     if (!a.h) return;
     a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(a.h, "ncclGetUniqueId"));

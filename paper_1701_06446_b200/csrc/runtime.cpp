@@ -38,6 +38,7 @@ struct DevLayout {
   DevBuf<uint16_t> index;
   DevBuf<uint64_t> prefix;
   DevBuf<double> mult;
+  std::vector<double> mult_host;  // the same, for the report's block fold on the host
   DevBuf<uint32_t> diag;  // blocks with equal neighbouring coordinates
   uint32_t ndiag = 0;
   std::vector<uint32_t> diag_host;
@@ -124,6 +125,7 @@ std::shared_ptr<DevLayout> get_layout(Device& dev, int order, int n, int b) {
     h2d_sync(L->index.ptr, h.index.data(), L->index.bytes());
     h2d_sync(L->prefix.ptr, h.prefix.data(), L->prefix.bytes());
     h2d_sync(L->mult.ptr, mult.data(), L->mult.bytes());
+    L->mult_host = mult;
     std::vector<uint32_t> diag;
     for (uint64_t r = 0; r < h.nblocks; ++r) {
       bool runs = false;
@@ -894,9 +896,19 @@ int host_fold_width() {
 // moms2cums into c, with per-block partial squared norms for every order.
 struct NormScratch {
   uint32_t exact_mask = 0;  // orders whose partials are already exact (moms2cums' in-block pass)
-  std::vector<DevBuf<double>> partial;  // per order
+  // one device buffer [d sums | 3 n diagonals | per-block partials of orders
+  // 1..d]: the report reads it back with a single copy and folds the blocks
+  // on the host (knorm's sequential block fold, symten.cpp:268: a chain of
+  // nblocks dependent adds costs a CPU core a fraction of what it costs one
+  // GPU thread -- cfg2: 12376 blocks, 0.097 ms in the kernel)
+  DevBuf<double> all;
+  std::vector<uint64_t> poff;  // d + 1 offsets of the partials inside `all`
+  int pd = 0, pn = 0, pb = 0;
+  void ensure(const csb_series* c);
+  double* part(int s) { return all.ptr + poff[s - 1]; }
+  uint64_t nblk(int s) const { return poff[s] - poff[s - 1]; }
+  double* out() { return all.ptr; }
   DevBuf<double> diag;                  // gathered diagonal of a sharded C_d
-  DevBuf<double> out;
   // pinned: the report's D2H is a direct DMA, not a staged pageable copy
   struct Pinned {
     double* p = nullptr;
@@ -920,6 +932,20 @@ struct NormScratch {
   } host;
 };
 
+void NormScratch::ensure(const csb_series* c) {
+  if (pd == c->d && pn == c->n && pb == c->b && all.ptr) return;
+  pd = c->d;
+  pn = c->n;
+  pb = c->b;
+  poff.assign(static_cast<size_t>(pd) + 1, 0);
+  poff[0] = static_cast<uint64_t>(pd) + 3ull * pn;
+  for (int s = 1; s <= pd; ++s) poff[s] = poff[s - 1] + c->lay[s - 1]->host.nblocks;
+  all.alloc(poff[pd]);
+  CSB_CUDA(cudaMemsetAsync(all.ptr, 0, all.bytes(), c->dev->stream));
+  CSB_CUDA(cudaStreamSynchronize(c->dev->stream));
+  host.resize(poff[pd]);
+}
+
 // orders [first, last] of moms2cums (C_1 is a copy of M_1), with per-block
 // partial squared norms; the stream step may run the low orders early on
 // the side stream (run_moments' side_tail) and the rest here
@@ -929,14 +955,11 @@ void run_moms2cums(const csb_series* m, csb_series* c, NormScratch& ns, cudaStre
   if (last <= 0) last = d;
   // (checked before any order is converted: s = 16 alone is 10^10 partitions per element)
   if (last > kMaxCumOrderAny) fail(CSB_EINVAL, "partitions: s must be in [1, 16]");
-  if (ns.partial.size() != static_cast<size_t>(d)) {
-    ns.partial.clear();
-    for (int s = 1; s <= d; ++s) ns.partial.emplace_back(m->lay[s - 1]->host.nblocks);
-  }
+  ns.ensure(m);
   ProfScope ps("moms2cums", st);
   const auto& L1 = m->lay[0];
   if (first <= 1) {
-    launch_copy_c1(m->data[0].ptr, c->data[0].ptr, ns.partial[0].ptr, L1->view(), L1->host.nblocks,
+    launch_copy_c1(m->data[0].ptr, c->data[0].ptr, ns.part(1), L1->view(), L1->host.nblocks,
                    L1->host.stored, st);
     ns.exact_mask &= ~1u;
   }
@@ -998,14 +1021,14 @@ void run_moms2cums(const csb_series* m, csb_series* c, NormScratch& ns, cudaStre
       // C_d only for the owned blocks; the other partials stay zero so a
       // sum over ranks reproduces the unsharded partial array exactly
       const uint64_t lo = sh.lo(0), hi = sh.hi(0);
-      CSB_CUDA(cudaMemsetAsync(ns.partial[s - 1].ptr, 0, ns.partial[s - 1].bytes(), st));
+      CSB_CUDA(cudaMemsetAsync(ns.part(s), 0, ns.nblk(s) * sizeof(double), st));
       p.blk0 = lo;
-      p.partial = ns.partial[s - 1].ptr + lo;
+      p.partial = ns.part(s) + lo;
       const bool exact = launch_moms2cums_v2(s, p, hi - lo, st);
       ns.exact_mask = exact ? ns.exact_mask | (1u << (s - 1)) : ns.exact_mask & ~(1u << (s - 1));
     } else {
       p.blk0 = 0;
-      p.partial = ns.partial[s - 1].ptr;
+      p.partial = ns.part(s);
       static const char* const tags[] = {"m2c_1", "m2c_2", "m2c_3", "m2c_4", "m2c_5", "m2c_6"};
       ProfScope po(tags[s - 1], st);
       const bool exact = launch_moms2cums_v2(s, p, m->lay[s - 1]->host.nblocks, st);
@@ -1057,31 +1080,26 @@ void exact_partials(const csb_series* c, int s, double* partial, cudaStream_t st
 // Norm sums of orders 1..d + diagonals, to the host: exact per-block
 // partials (each block summed in storage order), then the block-order fold
 // -- knorm's own sequence, so norms and nu are the reference's bit for bit.
+void fold_norms_host(const csb_series* c, NormScratch& ns);
+
 void finalize_norms(const csb_series* c, NormScratch& ns, cudaStream_t st, const ShardCtx& sh = ShardCtx{},
                     bool wait = true) {
   const int d = c->d;
-  if (ns.partial.size() != static_cast<size_t>(d)) {
-    ns.partial.clear();
-    for (int s = 1; s <= d; ++s) ns.partial.emplace_back(c->lay[s - 1]->host.nblocks);
-  }
+  ns.ensure(c);
   {
     ProfScope ps("norm_partials", st);
     for (int s = 1; s <= d; ++s) {
       const uint64_t nb = c->lay[s - 1]->host.nblocks;
       const bool shard = sh.active() && s == d;  // C_d: only the owned blocks are valid here
       if (!(ns.exact_mask >> (s - 1) & 1u))
-        exact_partials(c, s, ns.partial[s - 1].ptr, st, shard ? sh.lo(0) : 0, shard ? sh.hi(0) : nb);
-      if (shard && sh.comm) sh.comm->allreduce_sum(ns.partial[s - 1].ptr, nb, st);  // collective C3
+        exact_partials(c, s, ns.part(s), st, shard ? sh.lo(0) : 0, shard ? sh.hi(0) : nb);
+      if (shard && sh.comm) sh.comm->allreduce_sum(ns.part(s), nb, st);  // collective C3
     }
     ns.exact_mask = 0;  // (the reduced C_d partials must not be reduced again)
   }
   NormParams p;
   p.norders = d;
-  for (int s = 1; s <= d; ++s) {
-    p.partial[s - 1] = ns.partial[s - 1].ptr;
-    p.mult[s - 1] = c->lay[s - 1]->mult.ptr;
-    p.nblocks[s - 1] = c->lay[s - 1]->host.nblocks;
-  }
+  p.fold = false;  // the block fold runs on the host (fold_norms_host); the kernel gathers the diagonals
   DiagTables& dt = diag_tables(c);
   for (int q = 0; q < 3; ++q) {
     p.diag_src[q] = (q + 2 <= d) ? c->data[q + 1].ptr : nullptr;
@@ -1098,16 +1116,36 @@ void finalize_norms(const csb_series* c, NormScratch& ns, cudaStream_t st, const
     p.diag_off[d - 2] = dt.iota.ptr;
   }
   p.n = c->n;
-  const uint64_t need = d + 3ull * c->n;
-  if (ns.out.count < need) ns.out.alloc(need);
-  p.out = ns.out.ptr;
+  p.out = ns.out();
   {
     ProfScope ps("norms", st);
     launch_norm_finalize(p, st);
   }
-  ns.host.resize(need);
-  CSB_CUDA(cudaMemcpyAsync(ns.host.data(), ns.out.ptr, need * sizeof(double), cudaMemcpyDeviceToHost, st));
-  if (wait) CSB_CUDA(cudaStreamSynchronize(st));  // (a captured step waits after the graph launch)
+  // diagonals and every order's per-block partials in one copy
+  CSB_CUDA(cudaMemcpyAsync(ns.host.data(), ns.all.ptr, ns.all.bytes(), cudaMemcpyDeviceToHost, st));
+  if (wait) {
+    CSB_CUDA(cudaStreamSynchronize(st));
+    fold_norms_host(c, ns);
+  }  // (a captured step waits after the graph launch, then folds)
+}
+
+// The blocks' partial sums folded in block order, acc = acc + mult * s
+// (symten.cpp:268; the product is rounded, the reference build does not
+// contract it -- this file is compiled -ffp-contract=off): the reference's
+// sequence bit for bit, after finalize_norms' copy has landed.
+void fold_norms_host(const csb_series* c, NormScratch& ns) {
+  double* h = ns.host.data();
+  for (int s = 1; s <= c->d; ++s) {
+    const double* part = h + ns.poff[s - 1];
+    const std::vector<double>& mult = c->lay[s - 1]->mult_host;
+    const uint64_t nb = ns.nblk(s);
+    double acc = 0.0;
+    for (uint64_t r = 0; r < nb; ++r) {
+      const double prod = mult[r] * part[r];  // rounded product, then the add (no contraction)
+      acc = acc + prod;
+    }
+    h[s - 1] = acc;
+  }
 }
 
 // make_window_report from the finalized sums (gauge.cpp:35-41,64-94,142-154).
@@ -1409,6 +1447,7 @@ int stream_step_impl(csb_stream* s, const double* x, bool on_device, uint64_t ro
     ++s->window;
     if (report) {
       CSB_CUDA(cudaStreamSynchronize(s->st));
+      fold_norms_host(s->C.get(), s->ns);
       s->norms_valid = true;
       build_report(s->C.get(), s->ns, s->window, report);
     }
@@ -1893,10 +1932,9 @@ int csb_stream_norm_partials(csb_stream* s, int order, double* host, uint64_t co
       finalize_norms(s->C.get(), s->ns, s->st, s->sh);
       s->norms_valid = true;
     }
-    const auto& buf = s->ns.partial.at(order - 1);
-    require(count == buf.count, "norm_partials: size mismatch");
+    require(count == s->ns.nblk(order), "norm_partials: size mismatch");
     CSB_CUDA(cudaStreamSynchronize(s->st));
-    CSB_CUDA(cudaMemcpy(host, buf.ptr, buf.bytes(), cudaMemcpyDeviceToHost));
+    CSB_CUDA(cudaMemcpy(host, s->ns.part(order), count * sizeof(double), cudaMemcpyDeviceToHost));
     // a sharded stream's order-d partials are allreduced: the whole array is valid
     if (first_block) *first_block = 0;
   });
