@@ -65,6 +65,7 @@ struct Device {
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // low-order kernel beside the top pair
   cudaEvent_t fork = nullptr, join = nullptr;
+  cudaEvent_t nfork = nullptr, njoin = nullptr;  // exact norm partials of C_s beside moms2cums of order s + 1
   std::mutex mu;
   std::map<std::tuple<int, int, int>, std::shared_ptr<DevLayout>> layouts;
   std::map<std::tuple<int, int, int, int>, std::shared_ptr<MomentPlan>> plans;
@@ -100,6 +101,8 @@ Device& device() {
     CSB_CUDA(cudaStreamCreateWithFlags(&slot->side, cudaStreamNonBlocking));
     CSB_CUDA(cudaEventCreateWithFlags(&slot->fork, cudaEventDisableTiming));
     CSB_CUDA(cudaEventCreateWithFlags(&slot->join, cudaEventDisableTiming));
+    CSB_CUDA(cudaEventCreateWithFlags(&slot->nfork, cudaEventDisableTiming));
+    CSB_CUDA(cudaEventCreateWithFlags(&slot->njoin, cudaEventDisableTiming));
   }
   return *slot;
 }
@@ -932,6 +935,9 @@ struct NormScratch {
   } host;
 };
 
+void exact_partials(const csb_series* c, int s, double* partial, cudaStream_t st, uint64_t lo, uint64_t hi,
+                    double k);
+
 void NormScratch::ensure(const csb_series* c) {
   if (pd == c->d && pn == c->n && pb == c->b && all.ptr) return;
   pd = c->d;
@@ -956,6 +962,8 @@ void run_moms2cums(const csb_series* m, csb_series* c, NormScratch& ns, cudaStre
   // (checked before any order is converted: s = 16 alone is 10^10 partitions per element)
   if (last > kMaxCumOrderAny) fail(CSB_EINVAL, "partitions: s must be in [1, 16]");
   ns.ensure(m);
+  Device& dev = *m->dev;
+  bool side_norms = false;
   ProfScope ps("moms2cums", st);
   const auto& L1 = m->lay[0];
   if (first <= 1) {
@@ -1030,11 +1038,28 @@ void run_moms2cums(const csb_series* m, csb_series* c, NormScratch& ns, cudaStre
       p.blk0 = 0;
       p.partial = ns.part(s);
       static const char* const tags[] = {"m2c_1", "m2c_2", "m2c_3", "m2c_4", "m2c_5", "m2c_6"};
-      ProfScope po(tags[s - 1], st);
-      const bool exact = launch_moms2cums_v2(s, p, m->lay[s - 1]->host.nblocks, st);
+      bool exact;
+      {
+        ProfScope po(tags[s - 1], st);
+        exact = launch_moms2cums_v2(s, p, m->lay[s - 1]->host.nblocks, st);
+      }
+      if (!exact && s < last && s <= kMaxCumOrder && st != dev.side && !sh.active()) {
+        // C_s is final: its exact norm partials on the side stream, under the
+        // next order's conversion, instead of in the report's critical path
+        CSB_CUDA(cudaEventRecord(dev.nfork, st));
+        CSB_CUDA(cudaStreamWaitEvent(dev.side, dev.nfork, 0));
+        {
+          ProfScope pk("norm_partials_side", dev.side);
+          exact_partials(c, s, ns.part(s), dev.side, 0, m->lay[s - 1]->host.nblocks, 2.0);
+        }
+        CSB_CUDA(cudaEventRecord(dev.njoin, dev.side));
+        side_norms = true;
+        exact = true;
+      }
       ns.exact_mask = exact ? ns.exact_mask | (1u << (s - 1)) : ns.exact_mask & ~(1u << (s - 1));
     }
   }
+  if (side_norms) CSB_CUDA(cudaStreamWaitEvent(st, dev.njoin, 0));  // (long done when the last order ends)
   c->window_len = m->window_len;
 }
 
@@ -1071,7 +1096,7 @@ DiagTables& diag_tables(const csb_series* c) {
 // Exact per-block norm partials of order s (all blocks, or [lo, hi) of a
 // shard with zeros elsewhere, summed over ranks: x + 0 == x).
 void exact_partials(const csb_series* c, int s, double* partial, cudaStream_t st, uint64_t lo, uint64_t hi,
-                    double k = 2.0) {
+                    double k) {
   const auto& L = c->lay[s - 1];
   if (lo > 0 || hi < L->host.nblocks) CSB_CUDA(cudaMemsetAsync(partial, 0, L->host.nblocks * sizeof(double), st));
   launch_knorm_exact(c->data[s - 1].ptr, L->view(), lo, hi - lo, k, host_fold_width(), partial, st);
@@ -1092,7 +1117,7 @@ void finalize_norms(const csb_series* c, NormScratch& ns, cudaStream_t st, const
       const uint64_t nb = c->lay[s - 1]->host.nblocks;
       const bool shard = sh.active() && s == d;  // C_d: only the owned blocks are valid here
       if (!(ns.exact_mask >> (s - 1) & 1u))
-        exact_partials(c, s, ns.part(s), st, shard ? sh.lo(0) : 0, shard ? sh.hi(0) : nb);
+        exact_partials(c, s, ns.part(s), st, shard ? sh.lo(0) : 0, shard ? sh.hi(0) : nb, 2.0);
       if (shard && sh.comm) sh.comm->allreduce_sum(ns.part(s), nb, st);  // collective C3
     }
     ns.exact_mask = 0;  // (the reduced C_d partials must not be reduced again)
