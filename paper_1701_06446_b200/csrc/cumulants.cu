@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(S <= 4 ? 1024 : 256, S <= 4 ? 1 : 2) moms2cums
       if (inblk) ptx::bulk_g2s(cblk, P.m + boff, vol * sizeof(double), &mbar);
       for (int m = 1; m < NM; ++m) {
         const uint32_t svol = static_cast<uint32_t>((m + 1 < NM ? sbase[m + 1] : soff) - sbase[m]);
-        ptx::bulk_g2s(sfac + sbase[m], P.lower[popcount_c(m) - 1] + subs[m - 1], svol * sizeof(double), &mbar);
+        ptx::bulk_g2s(sfac + sbase[m], P.lower[__popc(m) - 1] + subs[m - 1], svol * sizeof(double), &mbar);
       }
     }
   }
@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(S <= 4 ? 1024 : 256, S <= 4 ? 1 : 2) moms2cums
 #pragma unroll
       for (int k = 0; k < S; ++k)
         if (m >> k & 1) svol *= static_cast<uint32_t>(e[k]);
-      const double* src = P.lower[popcount_c(m) - 1] + subs[m - 1];
+      const double* src = P.lower[__popc(m) - 1] + subs[m - 1];
       double* dst = sfac + sbase[m];
       if (inblk)
         for (uint32_t t = threadIdx.x; t < svol; t += blockDim.x) cp_async8(dst + t, src + t);
@@ -194,7 +194,12 @@ __global__ void __launch_bounds__(S <= 4 ? 1024 : 256, S <= 4 ? 1 : 2) moms2cums
   // on the non-canonical copies of diagonal blocks -- and address a factor
   // in its staged sub-block with compile-time powers of b; edge blocks test
   // every position.
-  if (STAGED && full && P.canon) {
+  // (also without staging when b is a compile-time constant: the factors
+  // then come from global memory (L1 / L2) at sub-block base + offset, but the
+  // canonical list, the constant powers of b and the copy lists still apply --
+  // cfg4's order 6, whose 2.1 MB of sub-blocks per block cannot be staged, ran
+  // the position-by-position path at ~6100 instructions per entry before)
+  if (full && P.canon && (STAGED || B != 0)) {
     uint32_t pat = 0;
 #pragma unroll
     for (int k = 1; k < S; ++k) pat |= static_cast<uint32_t>(j[k] == j[k - 1]) << (k - 1);
@@ -232,7 +237,10 @@ __global__ void __launch_bounds__(S <= 4 ? 1024 : 256, S <= 4 ? 1 : 2) moms2cums
 #pragma unroll
         for (int k = S - 1; k >= 0; --k)
           if (m >> k & 1) a += static_cast<uint32_t>(o[k]) * bp[after++];
-        f[m] = sfac[(S <= 5 ? sb[m < NB ? m : 0] : static_cast<uint32_t>(sbase[m])) + a];
+        if (STAGED)
+          f[m] = sfac[(S <= 5 ? sb[m < NB ? m : 0] : static_cast<uint32_t>(sbase[m])) + a];
+        else
+          f[m] = __ldg(P.lower[__popc(m) - 1] + sbase[m] + a);
       }
       const double corr = partition_correction<S>(f);
       if (inblk) {
@@ -262,7 +270,7 @@ __global__ void __launch_bounds__(S <= 4 ? 1024 : 256, S <= 4 ? 1 : 2) moms2cums
         if (STAGED)
           f[m] = sfac[sbase[m] + a];
         else
-          f[m] = P.lower[popcount_c(m) - 1][sbase[m] + a];
+          f[m] = P.lower[__popc(m) - 1][sbase[m] + a];
       }
       const double corr = partition_correction<S>(f);
       P.c[boff + pos] = __dsub_rn(P.m[boff + pos], corr);
@@ -303,8 +311,9 @@ __global__ void __launch_bounds__(S <= 4 ? 1024 : 256, S <= 4 ? 1 : 2) moms2cums
       return;
     }
   }
-  const bool direct = !inblk && STAGED && full && P.canon && P.cstart;  // done in phase 1
-  const bool listed = !inblk && STAGED && full && P.canon && (P.mlist || direct);
+  const bool lists_ok = (STAGED || B != 0) && full && P.canon;            // phase 1 walked the canonical list
+  const bool direct = !inblk && lists_ok && P.cstart;                    // copies and norm term done in phase 1
+  const bool listed = !inblk && lists_ok && (P.mlist || direct);
   if (listed && !direct) {
     // copies from the canonical entries this CTA just wrote (visible to the
     // block after the barrier above), then the sum of squares in order
@@ -889,6 +898,8 @@ bool launch_moms2cums_v2(int S, const M2CParams& p, uint64_t nblocks, cudaStream
       } else {                                                                                              \
         CSB_M2C_B(SS, 0)                                                                                    \
       }                                                                                                     \
+    } else if (bb == 8 && SS >= 5) {                                                                        \
+      moms2cums_v2<SS, false, 8><<<g, 256, 0, st>>>(q);                                                     \
     } else {                                                                                                \
       moms2cums_v2<SS, false, 0><<<g, 256, 0, st>>>(q);                                                     \
     }                                                                                                       \

@@ -1046,6 +1046,7 @@ void run_moms2cums(const csb_series* m, csb_series* c, NormScratch& ns, cudaStre
       if (!exact && s < last && s <= kMaxCumOrder && st != dev.side && !sh.active()) {
         // C_s is final: its exact norm partials on the side stream, under the
         // next order's conversion, instead of in the report's critical path
+        std::lock_guard<std::mutex> lk(dev.mu);  // the side stream and its events are shared per device
         CSB_CUDA(cudaEventRecord(dev.nfork, st));
         CSB_CUDA(cudaStreamWaitEvent(dev.side, dev.nfork, 0));
         {
@@ -1059,7 +1060,10 @@ void run_moms2cums(const csb_series* m, csb_series* c, NormScratch& ns, cudaStre
       ns.exact_mask = exact ? ns.exact_mask | (1u << (s - 1)) : ns.exact_mask & ~(1u << (s - 1));
     }
   }
-  if (side_norms) CSB_CUDA(cudaStreamWaitEvent(st, dev.njoin, 0));  // (long done when the last order ends)
+  if (side_norms) {
+    std::lock_guard<std::mutex> lk(dev.mu);
+    CSB_CUDA(cudaStreamWaitEvent(st, dev.njoin, 0));  // (long done when the last order ends)
+  }
   c->window_len = m->window_len;
 }
 

@@ -125,3 +125,25 @@ def test_full_size_sampled(port, cfg, steps, count):
     got = check_stream_sampled(port, st, rows, c.n, c.d, c.b, c.T, c.p, steps, count=count, seed=cfg)
     assert got[f"M{c.d}"] > count // 2
     st.close()
+
+
+@pytest.mark.parametrize("shape", [(16, 6, 8), (16, 5, 8), (24, 5, 8)], ids=["n16_d6_b8", "n16_d5_b8", "n24_d5_b8"])
+def test_cfg4_moms2cums_path_full_compare(port, shape):
+    """cfg4's cumulant conversion (b = 8, orders 5 and 6): the sub-blocks of a
+    block (210 KB / 2.1 MB) cannot be staged, so full blocks run the
+    list-driven global-load path moms2cums_v2<S, false, 8>.  Whole-array
+    bitwise compare of M and C at a small n with the same block geometry
+    (the full-size sampled check is test_full_size_sampled[cfg4])."""
+    n, d, b = shape
+    T, p = 40, 13
+    rng = np.random.default_rng(8600 + n + d)
+    rows = rng.standard_normal((T + p, n)) * 0.9 + 0.15
+    m = capi.moment_series(rows[:T], d, b)
+    capi.moments_update(m, rows[T:], rows[:p])
+    want = port.moment_series(rows[:T], d, b)
+    port.moments_update(want, T, rows[T:], rows[:p], b)
+    c = capi.moms2cums(m)
+    cw = port.moms2cums(want, n, b)
+    for s in range(d):
+        assert np.array_equal(m.tensors()[s], want[s]), f"M{s + 1}"
+        assert np.array_equal(c.tensors()[s], cw[s]), f"C{s + 1}"
