@@ -817,7 +817,11 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) moment_tail_kernel(const MomP
   __shared__ __align__(8) uint64_t bars[MAX_STAGES];
   __shared__ uint32_t rel[MAX_STAGES];
   const int warp = threadIdx.x >> 5;
-  const uint32_t live = min(static_cast<uint32_t>(TAIL_WARPS), P.tail_warps - blockIdx.x * TAIL_WARPS);
+  // (the block may be launched narrower than TAIL_THREADS: few tasks are
+  // spread over all SMs, one or two warps per scheduler, rather than
+  // packed 12 warps deep on a few)
+  const uint32_t tw = blockDim.x >> 5;
+  const uint32_t live = min(tw, P.tail_warps - blockIdx.x * tw);
   Ring g;
   g.stages = static_cast<uint32_t>(P.stages);
   g.xs = smem;
@@ -840,7 +844,7 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) moment_tail_kernel(const MomP
   }
   __syncthreads();
   if (static_cast<uint32_t>(warp) >= live) return;
-  const TailTask tk = P.tail[(static_cast<size_t>(blockIdx.x) * TAIL_WARPS + warp) * 32 + (threadIdx.x & 31)];
+  const TailTask tk = P.tail[(static_cast<size_t>(blockIdx.x) * tw + warp) * 32 + (threadIdx.x & 31)];
   tail_dispatch<N, LM1>(P, tk, g, stash);
 }
 
@@ -1023,6 +1027,9 @@ int tail_windows(int S, int n, int b) {
   // per SM the CUDA-core kernel is latency-bound and the DMMA tile wins
   double tasks = 1.0;
   for (int k = 1; k <= S - 2; ++k) tasks = tasks * (n + k - 1) / k;  // C(n + S - 3, S - 2)
+  // (measured at cfg1, 4656 prefixes: with the two last windows here, spread
+  // one warp per scheduler over the SMs, the DMMA kernel saves 0.17 ms and
+  // this kernel costs 0.20 ms)
   if (tasks < 4.0 * 148 * 32) return 0;
   // (measured at cfg2: a third window on the CUDA cores costs what it saves,
   // 1.23 + 9.34 ms against 3.60 + 7.02 ms)
@@ -1051,8 +1058,13 @@ void launch_moment_tail(const MomParams& p_in, cudaStream_t st) {
   else if (lm1 == 4) kern = moment_tail_kernel<0, 4>;
   else fail(CSB_EINVAL, "moment_tail: order out of range");
   ensure_smem(kern, smem);
-  const unsigned grid = (p.tail_warps + TAIL_WARPS - 1) / TAIL_WARPS;
-  kern<<<grid, TAIL_THREADS, smem, st>>>(p);
+  // warps per CTA: 12 when there is work for every SM at that depth, else
+  // as few as still cover the SMs (one CTA per SM either way)
+  static int sms = 0;
+  if (!sms) CSB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  const unsigned tw = std::max(1u, std::min<unsigned>(TAIL_WARPS, (p.tail_warps + sms - 1) / sms));
+  const unsigned grid = (p.tail_warps + tw - 1) / tw;
+  kern<<<grid, tw * 32, smem, st>>>(p);
   CSB_CUDA(cudaGetLastError());
   count_launch();
 }
