@@ -907,14 +907,16 @@ __global__ void __launch_bounds__(256) mirror_kernel(double* __restrict__ m, Lay
     }
     return;
   }
-  const uint64_t vol = lay.offset[blk + 1] - base;
-  for (uint64_t pos = threadIdx.x; pos < vol; pos += blockDim.x) {
+  // (32-bit positions: a block of b^S <= 2^32 entries; the 64-bit divisions
+  // here were calls into a division routine -- cfg4's M_6, 26 GB, took 32 ms)
+  const uint32_t vol = static_cast<uint32_t>(lay.offset[blk + 1] - base);
+  for (uint32_t pos = threadIdx.x; pos < vol; pos += blockDim.x) {
     int o[S];
-    uint64_t rem = pos;
+    uint32_t rem = pos;
 #pragma unroll
     for (int k = S - 1; k >= 0; --k) {
-      o[k] = static_cast<int>(rem % e[k]);
-      rem /= e[k];
+      o[k] = static_cast<int>(rem % static_cast<uint32_t>(e[k]));
+      rem /= static_cast<uint32_t>(e[k]);
     }
     bool canonical = true;
 #pragma unroll
@@ -931,9 +933,9 @@ __global__ void __launch_bounds__(256) mirror_kernel(double* __restrict__ m, Lay
           o[k] = o[k - 1];
           o[k - 1] = t;
         }
-    uint64_t src = 0;
+    uint32_t src = 0;
 #pragma unroll
-    for (int k = 0; k < S; ++k) src = src * e[k] + o[k];
+    for (int k = 0; k < S; ++k) src = src * static_cast<uint32_t>(e[k]) + static_cast<uint32_t>(o[k]);
     mb[pos] = mb[src];
   }
 }
@@ -1091,6 +1093,11 @@ uint32_t dmma_chunk_rows(int n, int b) {
 void launch_mirror(int S, double* m, const LayoutDev& lay, const uint32_t* blocks, uint32_t nblocks, int n, int b,
                    const uint2* lists, const uint32_t* list_off, cudaStream_t st) {
   if (!nblocks) return;
+  {
+    double vol = 1.0;
+    for (int k = 0; k < S; ++k) vol *= static_cast<double>(b);
+    if (vol > 4294967295.0) fail(CSB_EINVAL, "mirror: a block of more than 2^32 entries");
+  }
   switch (S) {
 #define CSB_MIRROR(SS) \
   case SS: mirror_kernel<SS><<<nblocks, 256, 0, st>>>(m, lay, blocks, n, b, lists, list_off); break;
