@@ -245,7 +245,7 @@ int ShardPlan::owner(const int* jp) const {
 }
 
 void MomentPlan::build_dmma(int S_, int n_, int b_, const Layout& top, const Layout* low, uint64_t scratch,
-                            int tail_windows, const ShardPlan* shard, int shard_index) {
+                            int tail_windows, const ShardPlan* shard, int shard_index, int sm_count) {
   S = S_;
   L = S_ - 1;
   n = n_;
@@ -344,6 +344,11 @@ void MomentPlan::build_dmma(int S_, int n_, int b_, const Layout& top, const Lay
       for (size_t k = v.size(); k % 32; ++k) tail.push_back(pad);
     }
   }
+  struct Win {
+    uint32_t rs0, nrs;
+    int h;
+  };
+  std::vector<Win> windows;
   for (int h = 0; h < nh_dmma; ++h) {
     const int hi = std::min(8 * h + 8, n);
     const uint32_t rs0 = static_cast<uint32_t>(pairs.size() / 32);
@@ -380,13 +385,32 @@ void MomentPlan::build_dmma(int S_, int n_, int b_, const Layout& top, const Lay
     }
     const uint32_t nrs = static_cast<uint32_t>(pairs.size() / 32) - rs0;
     if (!nrs) continue;
-    // R row sets x 4/R column ranges of at most 4 column tiles per DMMA warp
+    windows.push_back({rs0, nrs, h});
+  }
+  // R row sets per CTA, up to kMaxNc column tiles per DMMA warp (8 warps):
+  // each row set's tiles spread over 4/R sub-partitions; the base choice keeps
+  // the busiest sub-partition's share per row set smallest.  When that leaves
+  // fewer CTAs than SMs (cfg0: ~45 row sets, 12 CTAs at R = 4), R is halved:
+  // the rows of a pass are a serial chain, so a small problem's time is set by
+  // one CTA's DMMAs per row step, and fewer row sets per CTA shorten exactly that.
+  constexpr int kMaxNc = 3;
+  auto base_r = [](int ncg) { return ncg <= 6 ? 4 : ncg <= 12 ? 2 : 1; };
+  int shrink = 0;
+  for (; shrink < 2; ++shrink) {
+    uint64_t ctas = 0;
+    for (const auto& w : windows) {
+      const int ncg = (n - 8 * w.h + 7) / 8;
+      const int R = std::max(1, base_r(ncg) >> shrink);
+      const int per_cta = kMaxNc * 8 / R;
+      ctas += static_cast<uint64_t>((ncg + per_cta - 1) / per_cta) * ((w.nrs + R - 1) / R);
+    }
+    if (ctas >= static_cast<uint64_t>(sm_count)) break;
+  }
+  for (const auto& w : windows) {
+    const int h = w.h;
+    const uint32_t rs0 = w.rs0, nrs = w.nrs;
     const int ncg = (n - 8 * h + 7) / 8;
-    // R row sets per CTA, up to kMaxNc column tiles per DMMA warp (8 warps):
-    // each row set's tiles spread over 4/R sub-partitions; the choice keeps
-    // the busiest sub-partition's share per row set smallest
-    constexpr int kMaxNc = 3;
-    const int R = ncg <= 6 ? 4 : ncg <= 12 ? 2 : 1;
+    const int R = std::max(1, base_r(ncg) >> shrink);
     const int per_cta = kMaxNc * 8 / R;
     const int nranges = (ncg + per_cta - 1) / per_cta;
     for (int q = 0; q < nranges; ++q) {

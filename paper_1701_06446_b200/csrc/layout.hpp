@@ -140,7 +140,7 @@ struct MomentPlan {
   // tail_windows: the last so many column windows become TailTasks
   // (moment_tail_kernel) instead of DMMA tiles
   void build_dmma(int S, int n, int b, const Layout& top, const Layout* low, uint64_t scratch_per_tile,
-                  int tail_windows, const ShardPlan* shard = nullptr, int shard_index = 0);
+                  int tail_windows, const ShardPlan* shard = nullptr, int shard_index = 0, int sm_count = 148);
   void upload();
 
  private:
