@@ -299,6 +299,10 @@ def main() -> None:
         capi.comm_selftest(1 << 16)  # fail loudly before timing if the NCCL exchange is broken
     st = capi.Stream(cfg.n, cfg.d, cfg.T, cfg.p, cfg.b, window, resync_every=0,
                      shard_index=rank, shard_count=world)
+    # steps run eagerly here: the engine would capture a CUDA graph on the second visit of a (ring head, batch
+    # address) key -- a one-off cost of a few ms per key that pays back over a long stream but would land inside
+    # this short timed region (at cfg2 graphs change nothing: the step is 12 ms of kernels)
+    st.use_graphs(False)
     cs = torch.cuda.ExternalStream(st.cuda_stream(), device=dev)
     xdev = [torch.from_numpy(b).to(dev) for b in batches]
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
